@@ -1,0 +1,450 @@
+"""Pins of the fp64 oracle against facts fixed by the paper and by mathematics
+(DESIGN.md "Oracle pins").  CPU only.
+
+Each test names the pin and the passage it checks.  None of them compares the oracle
+with itself: references are numpy.fft (a library routine), closed forms, brute force,
+or numbers printed in PAPER.md (tests/golden/paper_examples.json).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import closed_form as cf
+from oracle import direct as od
+from oracle import metrics as me
+from oracle import operators as op
+from oracle import planner as pl
+from oracle import symplectic as sy
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))
+
+
+def paper_matrix(name):
+    return sy.polar_project(np.array(GOLD[name]["M"], float))
+
+
+def cdft2(g):
+    """Centered 2D DFT sum_m sum_n exp(-j2pi(pm+qn)/N) g[m,n] via numpy.fft (even N)."""
+    return np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(g, axes=(-2, -1))), axes=(-2, -1))
+
+
+def cidft2_sum(g):
+    """Centered sum_m sum_n exp(+j2pi(pm+qn)/N) g[m,n] via numpy.fft (even N)."""
+    n = g.shape[-1]
+    return np.fft.fftshift(np.fft.ifft2(np.fft.ifftshift(g, axes=(-2, -1))), axes=(-2, -1)) * n * n
+
+
+def rng(seed=0):
+    return np.random.default_rng(seed)
+
+
+# ---------------------------------------------------------------- symplectic algebra
+def test_validity_forms_equivalent():
+    """Eq. Intro12 <=> Eq. Intro16 on valid and perturbed matrices."""
+    r, _ = synth.config_streams(11)
+    for i in range(50):
+        M = synth.random_symplectic(r)
+        assert max(sy.residuals(M)) < 1e-12 and max(sy.residuals_dual(M)) < 1e-12
+        P = M.copy()
+        P[i % 4, (i * 3) % 4] += 1e-3
+        assert max(sy.residuals(P)) > 1e-6 and max(sy.residuals_dual(P)) > 1e-6
+    I = np.eye(4)
+    I[0, 0] = 1.1
+    assert not sy.is_valid(I)
+
+
+def test_inverse_and_compose():
+    """(A,B;C,D)^{-1} = (D^T,-B^T;-C^T,A^T) (Eq. CCCMCCCM20)."""
+    r, _ = synth.config_streams(12)
+    for _ in range(10):
+        M = synth.random_symplectic(r)
+        assert np.abs(sy.inverse(M) @ M - np.eye(4)).max() < 1e-12
+        assert np.array_equal(sy.inverse(sy.inverse(M)), M)
+    F = synth.dft_matrix4()
+    assert np.array_equal(sy.inverse(F), synth.idft_matrix4())
+    assert np.array_equal(sy.compose(F, F), -np.eye(4))
+
+
+def test_polar_projection_of_paper_matrices():
+    """Reading R6: the printed matrices miss Eq. Intro12 at ~1e-4;
+    the projection is symplectic to rounding and moves entries by <= 3e-3 (A3, whose
+    entries reach 12.8, moves most)."""
+    for name in ("A1", "A2", "A3", "A4"):
+        M0 = np.array(GOLD[name]["M"], float)
+        assert 1e-6 < max(sy.residuals(M0)) < 1e-3
+        M = sy.polar_project(M0)
+        assert max(sy.residuals(M)) < 1e-13
+        assert np.abs(M - M0).max() < 3e-3
+
+
+def test_gamma_values():
+    """gamma of Eq. HA16: gamma(0) = 1; gamma((1,2;2,3)) = 24."""
+    assert pl.gamma(np.zeros((2, 2))) == 1.0
+    assert pl.gamma(np.array([[1.0, 2.0], [2.0, 3.0]])) == 24.0
+    assert pl.gamma(np.array([[1.0, -2.0], [-2.0, 3.0]])) == 24.0
+
+
+# ---------------------------------------------------------------- P1, P2: exact DFT reductions
+@pytest.mark.parametrize("n", [32, 34])
+def test_p1_dft(n):
+    """P1: M = (0,I;-I,0) -> O_plan = Eq. BasicDFT16 exactly,
+    checked against numpy.fft; the direct method (Eq. Intro32) agrees too."""
+    dx = math.sqrt(2 * math.pi / n)
+    g = synth.iid_cn(rng(n), (n, n))
+    ref = dx * dx / (2j * math.pi) * cdft2(g)
+    G, plan = op.nsdlct(g, synth.dft_matrix4(), dx)
+    assert plan["kind"] == "I"
+    assert me.rel_l2(G, ref) < 1e-13
+    assert me.rel_l2(od.direct(g, synth.dft_matrix4(), dx), ref) < 1e-13
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_p1_idft_is_exact_inverse(n):
+    """P1/reading R3: M = (0,-I;I,0) takes form II (tr B = -2, Eq. Reversible08) and gives
+    the exact inverse of Eq. BasicDFT16, which is MINUS the printed Eq. BasicDFT20."""
+    dx = math.sqrt(2 * math.pi / n)
+    g = synth.iid_cn(rng(n + 1), (n, n))
+    printed = dx * dx / (2j * math.pi) * cidft2_sum(g)
+    G, plan = op.nsdlct(g, synth.idft_matrix4(), dx)
+    assert plan["kind"] == "II"
+    assert me.rel_l2(G, -printed) < 1e-13
+    assert me.rel_l2(op.idft2_printed(g, dx), printed) < 1e-13
+    # and the oracle's exact inverse really inverts Eq. BasicDFT16
+    assert me.rel_l2(op.idft2_exact(op.dft2(g, dx), dx), g) < 1e-14
+
+
+@pytest.mark.parametrize("n", [32, 33, 34])
+def test_p2_gyrator_half_pi(n):
+    """P2: gyrator alpha = pi/2, M = (0,J;-J,0) -> the twisted DFT
+    G[p,q] = (1/N) sum exp(-j2pi(mq+np)/N) g[m,n] exactly, for any N."""
+    dx = math.sqrt(2 * math.pi / n)
+    g = synth.iid_cn(rng(n + 2), (n, n))
+    k = np.arange(n) - n // 2
+    W = np.exp(-2j * math.pi * np.outer(k, k) / n)
+    ref = (W @ g @ W.T).T / n          # brute-force twisted DFT
+    G, _ = op.nsdlct(g, synth.gyrator_matrix4(math.pi / 2), dx)
+    assert me.rel_l2(G, ref) < 1e-13
+    assert me.rel_l2(od.direct(g, synth.gyrator_matrix4(math.pi / 2), dx), ref) < 1e-13
+
+
+# ---------------------------------------------------------------- P3 identity, P4 Parseval, P5 reversibility
+def test_p3_identity_bit_exact():
+    """P3: (I,0;0,I) is the B = 0 case (Eq. Intro20) with D = I: output = input exactly."""
+    g = synth.iid_cn(rng(3), (32, 32))
+    G, plan = op.nsdlct(g, np.eye(4))
+    assert plan["kind"] == "B0"
+    assert np.array_equal(G, g)
+
+
+@pytest.mark.parametrize("n", [32, 48])
+def test_p4_parseval_and_p5_reversibility(n):
+    """P4: every stage is unitary (CMs unit-modulus, F^{-1} CM F with the exact inverse,
+    reading R3) so sum|G|^2 = sum|g|^2.  P5: O(M^{-1}) O(M) = I under Eq. Reversible08 +
+    reading R7 (Eq. CCCMCCCM30)."""
+    r, _ = synth.config_streams(20 + n)
+    dx = math.sqrt(2 * math.pi / n)
+    g = synth.iid_cn(rng(n + 3), (n, n))
+    for _ in range(3):
+        M = synth.random_symplectic(r)
+        G, plan = op.nsdlct(g, M, dx)
+        back, plan_inv = op.nsdlct(G, sy.inverse(M), dx)
+        assert {plan["kind"], plan_inv["kind"]} == {"I", "II"}
+        assert abs(np.sum(np.abs(G) ** 2) / np.sum(np.abs(g) ** 2) - 1.0) < 1e-13
+        assert me.nmse(back, g) < 1e-26
+
+
+def test_c7_gyrator_tr_b_zero_reversible():
+    """Reading R7: the gyrator has tr B = 0 (outside Eq. Reversible08); the odd key still
+    pairs M and M^{-1} on opposite forms, so alpha = 2.5 is perfectly reversible."""
+    n = 32
+    dx = math.sqrt(2 * math.pi / n)
+    g = synth.iid_cn(rng(5), (n, n))
+    M = synth.gyrator_matrix4(2.5)
+    G, p1 = op.nsdlct(g, M, dx)
+    back, p2 = op.nsdlct(G, sy.inverse(M), dx)
+    assert {p1["kind"], p2["kind"]} == {"I", "II"}
+    assert me.nmse(back, g) < 1e-26
+
+
+# ---------------------------------------------------------------- P6 separable (pins O_direct's constant)
+def test_p6_separable_direct_is_kron_of_1d():
+    """P6: for block-diagonal M, Eq. Intro32 factorises into two 1D direct sums with
+    constant 1/sqrt(j 2 pi b) each (sign -1 iff b1, b2 < 0, reading R4)."""
+    n = 24
+    dx = math.sqrt(2 * math.pi / n)
+    g = synth.iid_cn(rng(6), (n, n))
+    for (a, b, c) in [((0.7, -1.3), (0.9, 1.4), (0.2, -0.5)), ((1.2, 0.6), (-0.8, -1.1), (0.3, 0.4)),
+                      ((-0.9, 1.1), (0.5, -0.7), (-1.0, 0.8))]:
+        M = synth.separable_matrix4(a, b, c)
+        d = (1 + np.array(b) * np.array(c)) / np.array(a)
+        G2 = od.direct(g, M, dx)
+        Gx = od.direct_1d(g, a[0], b[0], d[0], dx)                     # along x (rows)
+        Gxy = od.direct_1d(Gx.T, a[1], b[1], d[1], dx).T               # then along y
+        sgn = -1.0 if (b[0] < 0 and b[1] < 0) else 1.0
+        assert me.rel_l2(G2, sgn * Gxy) < 1e-13
+
+
+# ---------------------------------------------------------------- P7 Gaussian closed form
+def test_p7_direct_matches_gaussian_closed_form():
+    """P7: Eq. Intro32 on a 4x refined input grid reproduces the Gaussian-beam closed form
+    derived from Eq. Intro08 (mod the metaplectic sign, reading R4)."""
+    n = 32
+    dx = math.sqrt(2 * math.pi / n)
+    K = np.array([[0.4 + 1.0j, 0.2 + 0.1j], [0.2 + 0.1j, -0.3 + 0.8j]])
+    r, _ = synth.config_streams(30)
+    for _ in range(3):
+        M = synth.random_symplectic(r)
+        ref = cf.gaussian_lct(M, K, n, dx)
+        Gd = od.direct(cf.gaussian(K, 4 * n, dx / 4), M, dx / 4, dx_out=dx, n_out=n)
+        # limited by the Gaussian tail at the window edge (exp(-0.8 * 7.1^2 / 2) ~ 2e-9)
+        assert me.rel_l2(me.align_sign(Gd, ref), ref) < 1e-8
+
+
+@pytest.mark.parametrize("alpha", [0.3, 1.0, 2.5])
+def test_p7_gyrator_gaussian_eigenfunction(alpha):
+    """P7: every gyrator maps exp(-|z|^2/2) to itself (closed form with K = jI:
+    det(A+BK) = 1, (C+DK)(A+BK)^{-1} = jI)."""
+    n = 64
+    dx = math.sqrt(2 * math.pi / n)
+    g = cf.gaussian(1j * np.eye(2), n, dx)
+    G, _ = op.nsdlct(g, synth.gyrator_matrix4(alpha), dx)
+    assert me.rel_l2(me.align_sign(G, g), g) < 1e-10
+
+
+def test_p7_fast_general_matrix_gaussian():
+    """P7 on the full CM-CC-CM-CC / CC-CM-CC-CM chain with random M (both forms): a
+    well-sampled Gaussian (N = 256) is mapped to the closed form to <= 5e-5; any wrong
+    sign, dropped term or transposed stage matrix gives an O(1) error."""
+    n = 256
+    dx = math.sqrt(2 * math.pi / n)
+    K = 1j * np.eye(2)
+    r, _ = synth.config_streams(7)
+    kinds = set()
+    for _ in range(4):
+        M = synth.random_symplectic(r)
+        G, plan = op.nsdlct(cf.gaussian(K, n, dx), M, dx)
+        ref = cf.gaussian_lct(M, K, n, dx)
+        kinds.add(plan["kind"])
+        assert me.rel_l2(me.align_sign(G, ref), ref) < 5e-5
+    assert kinds == {"I", "II"}
+
+
+def test_p7_fast_chirped_gaussian_lc():
+    """P7 for HA and LC (Eq. LC12 with its 1D CC, both forms, both axes) on a chirped
+    anisotropic Gaussian: whenever the plan's space-bandwidth objective J (Eq. HA24, the
+    paper's own aliasing proxy) is <= 1000, the output matches the
+    closed form to 1e-4."""
+    n = 256
+    dx = math.sqrt(2 * math.pi / n)
+    K = np.array([[0.3 + 1.2j, 0.2 + 0.1j], [0.2 + 0.1j, -0.2 + 0.9j]])
+    r, _ = synth.config_streams(8)
+    seen = set()
+    for _ in range(6):
+        M = synth.random_symplectic(r)
+        ref = cf.gaussian_lct(M, K, n, dx)
+        for variant in ("HA", "LC"):
+            G, plan = op.nsdlct(cf.gaussian(K, n, dx), M, dx, variant=variant)
+            if plan["J"] <= 1000:
+                seen.add((variant, plan["kind"], plan["axis"]))
+                assert me.rel_l2(me.align_sign(G, ref), ref) < 1e-4
+    assert {("LC", "I", "x"), ("LC", "II", "y"), ("HA", "II", None)} <= seen
+
+
+# ---------------------------------------------------------------- P8 the paper's worked examples
+_TRUTH = {}
+
+
+def _truth(inp, mat):
+    key = (inp, mat)
+    if key not in _TRUTH:
+        gi, t = GOLD[inp], GOLD["truth"]
+        gt = cf.hg2d(gi["orders"], t["n"], t["dx"])
+        _TRUTH[key] = od.direct(gt, paper_matrix(mat), t["dx"], dx_out=gi["dx"], n_out=gi["n"])
+    return _TRUTH[key]
+
+
+@pytest.mark.parametrize("ex", ["E1", "E2"])
+@pytest.mark.parametrize("variant", ["HA", "LC"])
+def test_p8_accuracy_examples(ex, variant):
+    """P8: NMSE_acc (Eq. Acc04) of HA/LC against the direct method on 1024^2 at dx = 0.078
+     reproduces the printed values within x1.5,
+    under the form-I-only policy of reading R8."""
+    e = GOLD[ex]
+    gi = GOLD[e["input"]]
+    g = cf.hg2d(gi["orders"], gi["n"], gi["dx"])
+    G, _ = op.nsdlct(g, paper_matrix(e["M"]), gi["dx"], variant=variant, policy="formI")
+    val = me.nmse_pm(G, _truth(e["input"], e["M"]))
+    assert e[variant] / 1.5 <= val <= e[variant] * 1.5, (ex, variant, val)
+
+
+@pytest.mark.parametrize("ex,variant", [("E4", "HA"), ("E5", "HA"), ("E5", "LC")])
+def test_p8_additivity_examples(ex, variant):
+    """P8: NMSE_add (Eq. Add16-22) reproduces PAPER.md:1266 / :1305
+    within x1.5 (form-I-only policy, reading R8)."""
+    e = GOLD[ex]
+    gi = GOLD[e["input"]]
+    g = cf.hg2d(gi["orders"], gi["n"], gi["dx"])
+    M1, M2 = paper_matrix(e["M1"]), paper_matrix(e["M2"])
+    kw = dict(variant=variant, policy="formI")
+    G1, _ = op.nsdlct(g, M1, gi["dx"], **kw)
+    G, _ = op.nsdlct(G1, M2, gi["dx"], **kw)
+    Gp, _ = op.nsdlct(g, M2 @ M1, gi["dx"], **kw)
+    val = me.nmse_pm(Gp, G)
+    assert e[variant] / 1.5 <= val <= e[variant] * 1.5, (ex, variant, val)
+
+
+def test_p8_reversibility_psnr():
+    """E7: 128x128 image, dx = 0.22, M = A2, forward then inverse:
+    'perfect reconstruction' (paper: ~279 dB). Any 128x128 input works (image-independent)."""
+    g = np.abs(synth.iid_cn(rng(7), (128, 128)))
+    M = paper_matrix("A2")
+    G, _ = op.nsdlct(g, M, 0.22)
+    back, _ = op.nsdlct(G, sy.inverse(M), 0.22)
+    assert me.psnr(back, g) > 270.0
+
+
+# ---------------------------------------------------------------- P9 B = 0 sub-cases
+def test_p9_b0_pure_chirp():
+    """P9: D = I, C != 0 -> Eq. Intro20 is the CM of Eq. BasicCM12 exactly."""
+    n = 32
+    dx = math.sqrt(2 * math.pi / n)
+    g = synth.iid_cn(rng(9), (n, n))
+    S = np.array([[0.7, -0.3], [-0.3, 1.1]])
+    M = synth.b0_matrix4(np.eye(2), S)
+    G, plan = op.nsdlct(g, M, dx)
+    assert plan["kind"] == "B0"
+    x = (np.arange(n) - n // 2) * dx
+    X, Y = np.meshgrid(x, x, indexing="ij")
+    ref = np.exp(0.5j * (0.7 * X * X - 0.6 * X * Y + 1.1 * Y * Y)) * g
+    assert me.rel_l2(G, ref) < 1e-15
+
+
+def test_p9_b0_parity_and_lattice():
+    """P9: D = -I -> G[p,q] = g[-p,-q] (sqrt(det D) = 1), row/col p = -N/2 lost off-grid;
+    D = (1,1;0,1) (unimodular) -> exact lattice shear, taps outside the grid read 0."""
+    n = 16
+    g = synth.iid_cn(rng(10), (n, n))
+    G, _ = op.nsdlct(g, synth.b0_matrix4(-np.eye(2), np.zeros((2, 2))))
+    ref = np.zeros_like(g)
+    ref[1:, 1:] = g[1:, 1:][::-1, ::-1]
+    assert np.abs(G - ref).max() < 1e-15
+    D = np.array([[1.0, 1.0], [0.0, 1.0]])
+    G, _ = op.nsdlct(g, synth.b0_matrix4(D, np.zeros((2, 2))))
+    ref = np.zeros_like(g)
+    for i in range(n):
+        for j in range(n):
+            p, q = i - n // 2, j - n // 2
+            a, b = p, p + q          # (p1, q1) = (d11 p + d21 q, d12 p + d22 q)
+            if -n // 2 <= a < n // 2 and -n // 2 <= b < n // 2:
+                ref[i, j] = g[a + n // 2, b + n // 2]
+    assert np.abs(G - ref).max() < 1e-15
+
+
+def test_p9_b0_general_smooth():
+    """P9: general D, smooth (well-sampled Gaussian) input -> bilinear resampling approximates
+    sqrt(det D) chi(CD^T) g(D^T z') of Eq. Intro20 to O(dx^2)."""
+    n = 128
+    dx = math.sqrt(2 * math.pi / n)
+    K = 1j * np.array([[0.5, 0.1], [0.1, 0.4]])
+    D = np.array([[1.2, 0.3], [-0.4, 0.9]])
+    S = np.array([[0.3, 0.2], [0.2, -0.5]])
+    M = synth.b0_matrix4(D, S)
+    G, _ = op.nsdlct(cf.gaussian(K, n, dx), M, dx)
+    ref = cf.gaussian_lct(M, K, n, dx)
+    assert me.rel_l2(me.align_sign(G, ref), ref) < 1e-2
+
+
+# ---------------------------------------------------------------- P10 planner, P11 semigroups
+def test_p10_planner_recomposition_and_optimality():
+    """P10: the stage matrices recompose to M (Eq. Bnonsym08 / CCCMCCCM12, <= 1e-9,
+    SPEC.md:40), are symmetric, and J(H*) <= J(0) when H = 0 is feasible."""
+    r, _ = synth.config_streams(40)
+    mats = [synth.random_symplectic(r) for _ in range(6)] + [paper_matrix(k) for k in ("A1", "A2", "A3", "A4")]
+    mats += [synth.gyrator_matrix4(a) for a in (0.4, 2.0, 2.9)]
+    for M in mats:
+        plan = pl.plan(M)
+        assert np.abs(pl.chain_matrix(plan["chain"]) - M).max() <= 1e-9
+        for opn in plan["chain"]:
+            assert np.abs(opn[1] - opn[1].T).max() == 0.0
+        Mf = M if plan["kind"] == "I" else sy.inverse(M)
+        J0 = pl.objective(Mf, np.zeros((2, 2)))
+        _, B, _, _ = sy.blocks(Mf)
+        if abs(B[0, 1] - B[1, 0]) < 1e-12:
+            assert plan["J"] <= J0 * (1 + 1e-12)
+
+
+def test_p10_planner_beats_dense_brute_force():
+    """P10: brute force over a dense 301^2 grid of the feasible plane never finds a
+    lower objective than the HA search (reading R5)."""
+    r, _ = synth.config_streams(41)
+    for _ in range(3):
+        M = synth.random_symplectic(r)
+        h, J = pl.ha_search(M)
+        h0, Nb = pl.feasible_param(M)
+        R = 4.0 * (1.0 + np.abs(M).max())
+        best = math.inf
+        for s in (2.0, R):
+            g = np.linspace(-s, s, 301)
+            T1, T2 = np.meshgrid(g, g, indexing="ij")
+            for t1, t2 in zip(T1.ravel()[::7], T2.ravel()[::7]):
+                best = min(best, pl.objective(M, pl.hmat(h0 + Nb @ np.array([t1, t2]))))
+        assert J <= best * (1 + 1e-9)
+
+
+def test_p10_feasible_plane():
+    """Every H on the parametrised plane keeps B' = B - AH symmetric."""
+    r, _ = synth.config_streams(42)
+    M = synth.random_symplectic(r)
+    A, B, _, _ = sy.blocks(M)
+    h0, Nb = pl.feasible_param(M)
+    for t in rng(1).normal(size=(20, 2)) * 3:
+        Bp = B - A @ pl.hmat(h0 + Nb @ t)
+        assert abs(Bp[0, 1] - Bp[1, 0]) < 1e-12
+
+
+def test_p10_no_decomp_case():
+    """Reading R5 / PAPER.md:681: A = aI with B nonsymmetric has no CM-CC-CM-CC
+    decomposition (B' = B - aH is never symmetric)."""
+    Z = np.zeros((2, 2))
+    Bm = np.array([[0.0, 1.0], [-1.0, 0.0]])   # rotation by -90 deg: A = 0, B nonsymmetric
+    M = np.block([[Z, Bm], [-Bm, Z]])          # = (0, R; R, 0) with R^T = -R -> symplectic
+    assert sy.is_valid(M)
+    with pytest.raises(pl.PlanError):
+        pl.plan(M)
+
+
+def test_p11_semigroups():
+    """P11: CM(Q1) CM(Q2) = CM(Q1+Q2); CC(B1) CC(B2) = CC(B1+B2); CC(0) = I
+    (Eq. BasicCM12, BasicCC20)."""
+    n = 32
+    dx = math.sqrt(2 * math.pi / n)
+    g = synth.iid_cn(rng(11), (n, n))
+    Q1 = np.array([[0.3, 0.1], [0.1, -0.2]])
+    Q2 = np.array([[-0.7, 0.4], [0.4, 0.5]])
+    assert me.rel_l2(op.cm(op.cm(g, Q1, dx), Q2, dx), op.cm(g, Q1 + Q2, dx)) < 1e-14
+    assert me.rel_l2(op.cc(op.cc(g, Q1, dx), Q2, dx), op.cc(g, Q1 + Q2, dx)) < 1e-13
+    assert me.rel_l2(op.cc(g, np.zeros((2, 2)), dx), g) < 1e-14
+
+
+def test_cc1d_equals_cc_with_rank1_b():
+    """The 1D CC of Eq. LC12 equals the 2D CC with B = (h,0;0,0) / (0,0;0,h)."""
+    n = 32
+    dx = math.sqrt(2 * math.pi / n)
+    g = synth.iid_cn(rng(12), (n, n))
+    assert me.rel_l2(op.cc1d(g, 0.8, "x", dx), op.cc(g, np.diag([0.8, 0.0]), dx)) < 1e-13
+    assert me.rel_l2(op.cc1d(g, -1.3, "y", dx), op.cc(g, np.diag([0.0, -1.3]), dx)) < 1e-13
+
+
+def test_dispatch_pairs_opposite_forms():
+    """Eq. Reversible08 with reading R7: s(M^{-1}) = -s(M)."""
+    r, _ = synth.config_streams(43)
+    for _ in range(20):
+        M = synth.random_symplectic(r)
+        assert pl.dispatch_key(sy.inverse(M)) == -pl.dispatch_key(M) != 0.0
+    for a in (0.5, 2.5):
+        G = synth.gyrator_matrix4(a)
+        assert pl.dispatch_key(sy.inverse(G)) == -pl.dispatch_key(G) != 0.0
