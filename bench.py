@@ -1,0 +1,325 @@
+"""Benchmark of the B200 NsDLCT (BASELINE.json metric: 2D NsLCT transforms/s and achieved
+HBM GB/s as a fraction of the roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Workload (default, config C4 of BASELINE.json): 4096 x 4096 complex64 HA-NsDLCT, batch 32
+images PER GPU (weak scaling: images are independent, no collective on the data path),
+random symplectic ABCD G(rng) of SURVEY.md §8(d), i.i.d. CN(0,1) input.  One step = one
+nslct_exec of the batch (all 5 fused passes).  Inputs are 4 GiB per GPU, far larger than
+the 126 MB L2, so no L2 flush is needed between steps.
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier + synchronize, CUDA
+events on the exec stream, max over ranks.  The dominant kernel's average launch time
+comes from the library's own per-pass CUDA events (nslct_pass_ms) recorded on the same
+stream inside the timed region.
+
+--impl reference: the fp64 CPU oracle (oracle/, the only "reference" this paper has) on
+the host cores, each step one 4096^2 image of the same workload; rank 0 only.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # id: (n, per-GPU batch, dtype, description)
+    2: (256, 64, "c64", "C2: 256x256 complex64, batch 64/GPU, random symplectic ABCD, iid CN(0,1)"),
+    3: (1024, 16, "c64", "C3: 1024x1024 complex64, batch 16/GPU, random symplectic ABCD, iid CN(0,1)"),
+    4: (4096, 32, "c64", "C4: 4096x4096 complex64, batch 32/GPU, random symplectic ABCD, iid CN(0,1)"),
+    5: (16384, 1, "c64", "C5: 16384x16384 complex64, 1 transform/GPU, random symplectic ABCD, iid CN(0,1)"),
+}
+METRIC = "2D NsLCT transforms/s (HBM roofline fraction reported in 'roofline')"
+UNIT = "transforms/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def max_over_ranks(x, world, device=None):
+    """Max of a float over all ranks (torch.distributed all_reduce MAX)."""
+    if world == 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, world, device=None):
+    if world == 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax = max(smax, float(r[2]))
+                for nm, v in zip(names, r[5:9]):
+                    if "Active" in v and "Not" not in v:
+                        reasons.add(nm)
+            except Exception:
+                continue
+        if not sm:
+            return None
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def traffic_from_profiles(cfg_id):
+    """ncu --set full DRAM bytes per launch of the dominant kernel, if a capture summary
+    for this workload is committed under profiles/ (see profiles/README.md)."""
+    p = os.path.join(ROOT, "profiles", "traffic_c%d.json" % cfg_id)
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["dram_bytes_per_launch"]), d.get("kernel")
+    except Exception:
+        return None, None
+
+
+def cpu_oracle_sample(x_img, M):
+    """Time the fp64 oracle (as it stands) on one image of the workload."""
+    import numpy as np
+    from oracle import operators
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    g = np.asarray(x_img, np.complex128)
+    t0 = time.perf_counter()
+    operators.nsdlct(g, M)
+    dt = time.perf_counter() - t0
+    return dt, cores
+
+
+def run_reference(args):
+    """Reference arm: the fp64 oracle on the host cores; one image per step."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+    import synth
+    n, batch, dtype, desc = CONFIGS[args.config]
+    mr, ir = synth.config_streams(args.config)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (n, n)).astype(np.complex64)
+    times = []
+    cores = None
+    for i in range(args.warmup + args.steps):
+        dt, cores = cpu_oracle_sample(x, M)
+        if i >= args.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    val = 1.0 / t
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64 (complex128)", "data": "synthetic",
+           "config": {"workload": desc, "n": n, "per_gpu_batch": batch,
+                      "step": "one %dx%d image through the fp64 oracle O_plan (dense-DFT zgemm)" % (n, n)},
+           "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": "1 image of %dx%d per step" % (n, n)},
+           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_1707_03688_b200 import nslct
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    n, batch, dtype, desc = CONFIGS[args.config]
+    mr, _ = synth.config_streams(args.config)
+    M = synth.random_symplectic(mr)                 # same matrix on every rank
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(synth.SEED_BASE + 1000 * args.config + rank)
+    x = torch.randn((batch, n, n), dtype=torch.complex64, device=dev, generator=gen)   # CN(0,1)
+    out = torch.empty_like(x)
+    plan = nslct.Plan(n, M, batch, dtype=dtype, profile=True, device=local)
+    info = plan.info()
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        plan.exec(x, out, stream)
+    torch.cuda.synchronize()
+    plan.pass_ms()                                  # reset the per-pass averages
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        plan.exec(x, out, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    pass_ms = plan.pass_ms()
+    ms = max_over_ranks(ms_local, world, dev)
+    total_units = sum_over_ranks(batch, world, dev)
+    value = total_units / (ms * 1e-3)
+
+    # dominant kernel roofline: algorithmic bytes per launch = batch * 2 * N^2 * S
+    S = 8 if dtype == "c64" else 16
+    ki = max(range(len(pass_ms)), key=lambda k: pass_ms[k])
+    bytes_launch = batch * 2.0 * n * n * S
+    peak, peak_src = peaks()
+    achieved = bytes_launch / (pass_ms[ki] * 1e-3) / 1e9
+    traffic, tr_kernel = traffic_from_profiles(args.config)
+    step_alg_bytes = info["n_passes"] * bytes_launch
+    names = ["K1 CM+FFT_y (transposed store)", "K2 FFT_x CM IFFT_x", "K3 IFFT_y CM FFT_y",
+             "K4 FFT_x CM IFFT_x", "K5 IFFT_y CM"] if info["n_passes"] == 5 else ["B0 gather"]
+
+    # end-to-end through the public C API with host buffers (H2D + exec + D2H per step)
+    e2e = None
+    if not args.no_e2e:
+        hin = torch.empty((batch, n, n), dtype=torch.complex64).pin_memory()
+        hin.copy_(x.cpu())
+        hout = torch.empty_like(hin).pin_memory()
+        plan.exec_host(hin, hout, stream)
+        plan.pass_ms()
+        nst = max(1, min(args.steps, args.e2e_steps))
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(nst):
+            plan.exec_host(hin, hout, stream)      # synchronises the stream each call
+        t_e2e = (time.perf_counter() - t0) / nst
+        barrier()
+        t_e2e = max_over_ranks(t_e2e, world, dev)
+        plan.pass_ms()
+        e2e = {"value": total_units / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(hin.numel() * 8),
+               "d2h_bytes_per_step": int(hout.numel() * 8), "steps": nst,
+               "how": "nslct_exec_host: pinned host in -> device, 5 passes, device -> pinned host out, stream sync"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        img0 = x[0].cpu().numpy()
+        dt, cores = cpu_oracle_sample(img0, M)
+        cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": "1 of the %d %dx%d images of one step (image 0), fp64 dense-DFT O_plan" % (batch, n, n)}
+
+    plan.close()
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": desc, "n": n, "per_gpu_batch": batch, "global_batch": int(total_units),
+                       "plan_kind": info["kind"], "parallelism": "dp%d (independent images, no collective)" % world,
+                       "l2": "inputs 4 GiB/GPU >> 126 MB L2; no flush", "hbm_alg_bytes_per_step": step_alg_bytes},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": names[ki],
+                         "alg_bytes_per_launch": bytes_launch, "launch_ms": pass_ms[ki],
+                         "peak_source": peak_src, "traffic_kernel": tr_kernel,
+                         "step_frac_of_peak": step_alg_bytes / (ms * 1e-3) / 1e9 / peak,
+                         "step_frac_of_8TBs": step_alg_bytes / (ms * 1e-3) / 1e9 / 8000.0,
+                         "pass_ms": pass_ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": info["n_passes"] * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(res))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,148 @@
+/*
+ * nslct.h -- C ABI of the B200-native 2D nonseparable discrete linear canonical
+ * transform (2D NsDLCT) of arxiv 1707.03688 ("PAPER.md").
+ *
+ * The problem (Eq. Intro08): given N x N complex
+ * samples g[m,n] = g(m dx, n dx) and a valid ABCD matrix (Eq. Intro04, PAPER.md:27-58;
+ * validity Eq. Intro12), compute N x N samples G[p,q] ~ G(p dx, q dx)
+ * of its 2D NsLCT.  For det B != 0 the library evaluates the paper's fast HA-NsDLCT
+ *     O = CM((D'-I)B'^-1) CC(B') CM(B'^-1(A-I)) CC(H)          (Eq. HA28)
+ * or its CC-CM-CC-CM mirror (Eq. CCCMCCCM40), chosen by the
+ * reversible dispatch of Eq. Reversible08 (reading R7),
+ * where CC(B) = F^-1 CM(-B) F (Eq. BasicCC20) and F is the 2D DFT of
+ * Eq. BasicDFT16 with F^-1 its exact inverse (reading R3).  For B = 0 it
+ * evaluates Eq. Intro20 as chirp x bilinear affine resampling
+ * (Eq. BasicAffine12/16).
+ *
+ * Conventions (readings R1/R2):
+ *   - centered indices m, n, p, q in [-N/2, N/2-1], stored at array index m + N/2;
+ *   - data layout [batch][N][N], row index = m (x), column index = n (y, contiguous);
+ *   - input and output on the same grid dx (Delta_u = Delta_x);
+ *     the frequency grid of the CC middle chirp has spacing 2 pi / (N dx);
+ *   - complex numbers interleaved (re, im): NSLCT_C64 = 2 x float, NSLCT_C128 = 2 x double;
+ *   - the output carries no extra normalisation: the transform is unitary.
+ *
+ * Errors: every call returns an nslct_status and never aborts; a thread-local message
+ * is available from nslct_last_error().  The inverse transform is nslct_plan() on
+ * M^-1 = (D^T, -B^T; -C^T, A^T) (Eq. CCCMCCCM20); with the reversible dispatch,
+ * exec(plan(M^-1)) o exec(plan(M)) is the identity to rounding.
+ */
+#ifndef NSLCT_H
+#define NSLCT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NSLCT_ABI_VERSION 1
+
+typedef enum { NSLCT_C64 = 0, NSLCT_C128 = 1 } nslct_dtype;
+
+typedef enum {
+  NSLCT_OK = 0,
+  NSLCT_E_ARG = 1,             /* null/misaligned pointer, bad batch/dtype/option            */
+  NSLCT_E_NOT_SYMPLECTIC = 2,  /* an Eq. Intro12 residual exceeds 1e-10                       */
+  NSLCT_E_NO_DECOMP = 3,       /* no feasible H with |det B'| > 1e-8 max(1,|B'|^2) (reading R5) */
+  NSLCT_E_UNSUPPORTED_N = 4,   /* N must be a power of two, 32 <= N <= 16384                  */
+  NSLCT_E_CUDA = 5,            /* a CUDA launch/copy/allocation call failed (see last_error)  */
+  NSLCT_E_NCCL = 6,            /* reserved for the slab-sharded mode                          */
+  NSLCT_E_OOM = 7              /* device allocation of the plan's scratch failed              */
+} nslct_status;
+
+typedef struct nslct_plan_s* nslct_plan_t;
+
+/* plan variants */
+enum { NSLCT_VARIANT_HA = 0,       /* H by the HA objective of Eq. HA24, search of reading R5     */
+       NSLCT_VARIANT_LC = 1,       /* H = (h,0;0,0) or (0,0;0,h) of Eq. LC08/LC10, HA fallback     */
+       NSLCT_VARIANT_FIXED_H = 2   /* H given in nslct_opts.h_fixed (form I: H of M; form II:
+                                      H~ = the form-I H of M^-1), e.g. to reproduce another plan */
+};
+/* dispatch policies */
+enum { NSLCT_DISPATCH_REVERSIBLE = 0,  /* Eq. Reversible08 + odd tie key (reading R7) */
+       NSLCT_DISPATCH_FORM_I = 1        /* always CM-CC-CM-CC (reading R8)            */
+};
+
+typedef struct {
+  double dx;          /* sample spacing dx = dy = du = dv; <= 0 selects sqrt(2 pi / N)  */
+  int variant;        /* NSLCT_VARIANT_*                                                */
+  int dispatch;       /* NSLCT_DISPATCH_*                                               */
+  double h_fixed[3];  /* (h11, h22, h12) for NSLCT_VARIANT_FIXED_H                      */
+  int device;         /* CUDA device ordinal for the plan's buffers; -1 = current       */
+  int profile;        /* 1: record per-pass CUDA events in nslct_exec (nslct_pass_ms)   */
+  int reserved[6];
+} nslct_opts;
+
+/* Fill *opts with the defaults (dx = sqrt(2 pi/N), HA, reversible, current device). */
+void nslct_opts_default(nslct_opts* opts);
+
+/* Build a plan for `batch` transforms of size n x n with ABCD matrix abcd (row-major
+ * 4x4: [[a11 a12 b11 b12],[a21 a22 b21 b22],[c11 c12 d11 d12],[c21 c22 d21 d22]],
+ * PAPER.md:46-51).  Host-side planning (validation, dispatch, H search) plus device
+ * allocation of twiddle tables and one scratch buffer of batch*n*n complex elements on
+ * the selected device.  The plan owns everything it allocates; free with nslct_destroy. */
+nslct_status nslct_plan(nslct_plan_t* plan, int64_t n, const double abcd[16], int64_t batch,
+                        nslct_dtype dtype);
+nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16], int64_t batch,
+                           nslct_dtype dtype, const nslct_opts* opts);
+
+/* Enqueue the transform of `batch` images on `cuda_stream` (a cudaStream_t; NULL = the
+ * legacy default stream).  in/out: DEVICE pointers to [batch][n][n] interleaved complex,
+ * 16-byte aligned, owned by the caller; in == out is allowed.  Asynchronous and
+ * stream-ordered: no host synchronisation, no allocation.  At most one exec per plan in
+ * flight (the plan's scratch is shared).  Errors: E_ARG (null/misaligned), E_CUDA. */
+nslct_status nslct_exec(nslct_plan_t plan, const void* in, void* out, void* cuda_stream);
+
+/* Same transform from HOST memory: copies host_in -> device, runs nslct_exec, copies the
+ * result back to host_out, all on cuda_stream, and synchronises that stream before it
+ * returns.  host buffers [batch][n][n] complex (pinned memory gives full copy speed).
+ * Device staging buffers are allocated on the first call and owned by the plan. */
+nslct_status nslct_exec_host(nslct_plan_t plan, const void* host_in, void* host_out,
+                             void* cuda_stream);
+
+typedef struct {
+  int kind;                    /* 0 = B=0 (Eq. Intro20), 1 = form I (Eq. HA28), 2 = form II  */
+  int variant;                 /* variant actually used (LC falls back to HA: PAPER.md:840)  */
+  int lc_axis;                 /* 0 none, 1 = H=(h,0;0,0) (x), 2 = H=(0,0;0,h) (y)            */
+  int n_passes;                /* device passes per transform (5 for HA, 1 for B=0)           */
+  double H[3], Bp[3], P2[3], P4[3];  /* form-I plan of M (form I) or of M^-1 (form II):
+                                        (q11, q22, q12) of H, B', P2=B'^-1(A-I), P4=(D'-I)B'^-1 */
+  double Q[5][3];              /* the executed chirps, application order:
+                                  CM_space(Q0) F CM_freq(Q1) F^-1 CM_space(Q2) F CM_freq(Q3)
+                                  F^-1 CM_space(Q4); (q11, q22, q12)                        */
+  double dx;                   /* sample spacing used                                         */
+  double objective;            /* J(H) of Eq. HA24                                            */
+  double sym_residual;         /* max Eq. Intro12 residual of the input matrix                */
+  double recomposition_residual; /* |product of stage matrices - M|_max                        */
+  double dispatch_key;         /* s(M) of reading R7                                          */
+} nslct_plan_desc;
+
+nslct_status nslct_plan_info(nslct_plan_t plan, nslct_plan_desc* out);
+
+/* Host-only dry run of nslct_plan_ex: validation, dispatch and H search only, no CUDA call
+ * and no allocation; fills *out as nslct_plan_info would.  n only selects the default dx.
+ * Same error codes as nslct_plan_ex (except E_CUDA / E_OOM, which cannot occur). */
+nslct_status nslct_plan_describe(int64_t n, const double abcd[16], const nslct_opts* opts,
+                                 nslct_plan_desc* out);
+
+/* Per-pass device times (ms), averaged over every nslct_exec of a plan built with
+ * opts.profile = 1 since the previous call (events recorded on the exec stream between
+ * passes).  Synchronises on those events, then resets the average.  ms must hold
+ * n_passes floats; *n_written receives n_passes. */
+nslct_status nslct_pass_ms(nslct_plan_t plan, float* ms, int capacity, int* n_written);
+
+/* Free the plan and everything it owns (device-synchronises its buffers). NULL is a no-op. */
+nslct_status nslct_destroy(nslct_plan_t plan);
+
+/* Thread-local text of the last error on this thread ("" if none). */
+const char* nslct_last_error(void);
+
+/* NSLCT_ABI_VERSION of the loaded library. */
+int nslct_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NSLCT_H */

@@ -1,0 +1,436 @@
+// Device kernels of the B200 NsDLCT (sm_100a).  Included by nslct.cu only.
+//
+// The HA chain (Eq. HA28; form II Eq. CCCMCCCM40) is executed as
+//     G = CM_r(Q4) S W^-1 CM_w(Q3) W CM_r(Q2) W^-1 CM_w(Q1) W S CM_r(Q0) g
+// where W is the plain (uncentered) 2D DFT along array indices, W^-1 = W*/N^2, and
+// S = (-1)^(i+j) is the checkerboard that turns W into the centered DFT of Eq. BasicDFT16
+// (e^{-j2pi(k-N/2)(i-N/2)/N} = (-1)^(k+i) e^{-j2pi ki/N} for N % 4 == 0).  Inner
+// checkerboards cancel pairwise (S CM S = CM), so only the outer two survive and are
+// folded into the Q0 / Q4 chirps as half-turns.  The 8 axis passes of the chain are
+// merged into 5 HBM round trips:
+//   K1: CM_r(Q0)+S, W_y                 row-major in   -> transposed out
+//   K2: W_x, CM_w(Q1)/N, W_x^-1         lines along x  -> transposed out
+//   K3: W_y^-1, CM_r(Q2)/N, W_y         lines along y  -> transposed out
+//   K4: W_x, CM_w(Q3)/N, W_x^-1         lines along x  -> transposed out
+//   K5: W_y^-1, CM_r(Q4)/N + S          lines along y  -> row-major out (in place)
+// Every pass reads whole contiguous lines (the previous pass wrote them transposed),
+// so every global load is coalesced; the transposed store is staged through shared
+// memory so that consecutive threads write consecutive lines of the output.
+//
+// Chirp phases (the CM of Eq. BasicCM12): exp(j/2 d^2 (q11 p^2 + 2 q12 p q + q22 q^2))
+// = exp(2 pi j t) with t a quadratic polynomial in (line, element) whose coefficients
+// are 64-bit fixed-point fractions of a turn; t is evaluated EXACTLY mod 1 with wrapping
+// uint64 arithmetic (second differences along the thread's elements), then converted to
+// an angle in [-pi, pi).  This keeps the phase error at the 2^-32 (c64) / 2^-53 (c128)
+// level at any N, where a naive fp32 phase would be off by 1e-3 at N = 8192.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nslct {
+
+template <typename T>
+struct __align__(2 * sizeof(T)) cpx {
+  T x, y;
+};
+
+template <typename T>
+__device__ __forceinline__ cpx<T> cmul(cpx<T> a, cpx<T> b) {
+  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+}
+template <typename T>
+__device__ __forceinline__ cpx<T> cadd(cpx<T> a, cpx<T> b) {
+  return {a.x + b.x, a.y + b.y};
+}
+template <typename T>
+__device__ __forceinline__ cpx<T> csub(cpx<T> a, cpx<T> b) {
+  return {a.x - b.x, a.y - b.y};
+}
+template <typename T>
+__device__ __forceinline__ cpx<T> cconj(cpx<T> a) {
+  return {a.x, -a.y};
+}
+// multiply by -j
+template <typename T>
+__device__ __forceinline__ cpx<T> mul_mj(cpx<T> a) {
+  return {a.y, -a.x};
+}
+
+// ---------------------------------------------------------------------------------
+// Small DFTs in registers (forward, e^{-2 pi i n k / R}), natural order in and out.
+// ---------------------------------------------------------------------------------
+// W_16^q for constant q, specialised so that trivial factors cost nothing.
+template <int Q, typename T>
+__device__ __forceinline__ cpx<T> w16(cpx<T> a) {
+  constexpr int q = Q & 15;
+  constexpr double C1 = 0.92387953251128675613;  // cos(pi/8)
+  constexpr double S1 = 0.38268343236508977173;  // sin(pi/8)
+  constexpr double R2 = 0.70710678118654752440;  // sqrt(1/2)
+  if constexpr (q == 0) {
+    return a;
+  } else if constexpr (q == 4) {
+    return mul_mj(a);
+  } else if constexpr (q == 8) {
+    return {-a.x, -a.y};
+  } else if constexpr (q == 12) {
+    return {-a.y, a.x};
+  } else if constexpr (q == 2) {  // (1 - j)/sqrt2
+    return {T(R2) * (a.x + a.y), T(R2) * (a.y - a.x)};
+  } else if constexpr (q == 6) {  // (-1 - j)/sqrt2
+    return {T(R2) * (a.y - a.x), T(-R2) * (a.x + a.y)};
+  } else if constexpr (q == 10) {  // (-1 + j)/sqrt2
+    return {T(-R2) * (a.x + a.y), T(R2) * (a.x - a.y)};
+  } else if constexpr (q == 14) {  // (1 + j)/sqrt2
+    return {T(R2) * (a.x - a.y), T(R2) * (a.x + a.y)};
+  } else {
+    // generic: cos(2 pi q/16) - j sin(2 pi q/16)
+    constexpr double c = (q == 1 || q == 15) ? C1 : (q == 3 || q == 13) ? S1
+                         : (q == 5 || q == 11) ? -S1 : -C1;  // q = 7, 9
+    constexpr double s = (q == 1 || q == 7) ? S1 : (q == 3 || q == 5) ? C1
+                         : (q == 9 || q == 15) ? -S1 : -C1;  // q = 11, 13
+    return {T(c) * a.x + T(s) * a.y, T(c) * a.y - T(s) * a.x};
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void dft2(cpx<T>& a, cpx<T>& b) {
+  cpx<T> t = a;
+  a = cadd(t, b);
+  b = csub(t, b);
+}
+
+template <typename T>
+__device__ __forceinline__ void dft4(cpx<T>& a0, cpx<T>& a1, cpx<T>& a2, cpx<T>& a3) {
+  cpx<T> t0 = cadd(a0, a2), t1 = csub(a0, a2);
+  cpx<T> t2 = cadd(a1, a3), t3 = mul_mj(csub(a1, a3));
+  a0 = cadd(t0, t2);
+  a2 = csub(t0, t2);
+  a1 = cadd(t1, t3);
+  a3 = csub(t1, t3);
+}
+
+// u[R] -> DFT_R(u) in place.  R in {2, 4, 8, 16}.
+template <int R, typename T>
+__device__ __forceinline__ void dft(cpx<T>* u) {
+  if constexpr (R == 2) {
+    dft2(u[0], u[1]);
+  } else if constexpr (R == 4) {
+    dft4(u[0], u[1], u[2], u[3]);
+  } else if constexpr (R == 8) {
+    // n = n1 + 2 n2, k = k2 + 4 k1
+    cpx<T> y0[4] = {u[0], u[2], u[4], u[6]};
+    cpx<T> y1[4] = {u[1], u[3], u[5], u[7]};
+    dft4(y0[0], y0[1], y0[2], y0[3]);
+    dft4(y1[0], y1[1], y1[2], y1[3]);
+    y1[1] = w16<2>(y1[1]);  // W8^1
+    y1[2] = w16<4>(y1[2]);  // W8^2
+    y1[3] = w16<6>(y1[3]);  // W8^3
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      u[k2] = cadd(y0[k2], y1[k2]);
+      u[k2 + 4] = csub(y0[k2], y1[k2]);
+    }
+  } else {
+    static_assert(R == 16, "radix");
+    // n = n1 + 4 n2, k = k2 + 4 k1
+    cpx<T> y[4][4];
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) {
+      y[n1][0] = u[n1];
+      y[n1][1] = u[n1 + 4];
+      y[n1][2] = u[n1 + 8];
+      y[n1][3] = u[n1 + 12];
+      dft4(y[n1][0], y[n1][1], y[n1][2], y[n1][3]);
+    }
+    y[1][1] = w16<1>(y[1][1]);
+    y[1][2] = w16<2>(y[1][2]);
+    y[1][3] = w16<3>(y[1][3]);
+    y[2][1] = w16<2>(y[2][1]);
+    y[2][2] = w16<4>(y[2][2]);
+    y[2][3] = w16<6>(y[2][3]);
+    y[3][1] = w16<3>(y[3][1]);
+    y[3][2] = w16<6>(y[3][2]);
+    y[3][3] = w16<9>(y[3][3]);
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      dft4(y[0][k2], y[1][k2], y[2][k2], y[3][k2]);
+      u[k2] = y[0][k2];
+      u[k2 + 4] = y[1][k2];
+      u[k2 + 8] = y[2][k2];
+      u[k2 + 12] = y[3][k2];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Line FFT of length N = 2^LOG2N, E = 16 elements per thread, TL = N/16 threads per line.
+// Register slot e of thread j holds element j + TL*e, before and after (Stockham
+// autosort, decimation in time; radix-16 stages, last stage radix 2^(LOG2N mod 4)).
+// buf: this line's shared-memory buffer, padded index P(i) = i + (i >> 4).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+
+template <typename T, int LOG2N, int STAGE, int NS>
+__device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], cpx<T>* buf, int j,
+                                          const cpx<T>* __restrict__ tw) {
+  constexpr int N = 1 << LOG2N;
+  constexpr int TL = N / 16;
+  constexpr int NFULL = LOG2N / 4;
+  constexpr int R = (STAGE < NFULL) ? 16 : (1 << (LOG2N % 4));
+  constexpr int NB = 16 / R;
+  constexpr bool LAST = (STAGE == NS - 1);
+  constexpr int Ns = (STAGE < NFULL) ? (1 << (4 * STAGE)) : (1 << (4 * NFULL));
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int jp = j + b * TL;
+    cpx<T> u[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) u[r] = v[b + r * NB];
+    if constexpr (Ns > 1) {
+      const int k0 = (jp % Ns) * (N / (Ns * R));
+#pragma unroll
+      for (int r = 1; r < R; ++r) u[r] = cmul(u[r], tw[k0 * r]);
+    }
+    dft<R>(u);
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[b + r * NB] = u[r];
+    if constexpr (!LAST) {
+      const int idxD = (jp / Ns) * Ns * R + (jp % Ns);
+#pragma unroll
+      for (int r = 0; r < R; ++r) buf[pad16(idxD + r * Ns)] = u[r];
+    }
+  }
+  if constexpr (!LAST) {
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = buf[pad16(j + TL * e)];
+    __syncthreads();
+  }
+}
+
+template <typename T, int LOG2N, int STAGE, int NS>
+struct FftStages {
+  __device__ __forceinline__ static void run(cpx<T> (&v)[16], cpx<T>* buf, int j,
+                                             const cpx<T>* __restrict__ tw) {
+    fft_stage<T, LOG2N, STAGE, NS>(v, buf, j, tw);
+    FftStages<T, LOG2N, STAGE + 1, NS>::run(v, buf, j, tw);
+  }
+};
+template <typename T, int LOG2N, int NS>
+struct FftStages<T, LOG2N, NS, NS> {
+  __device__ __forceinline__ static void run(cpx<T> (&)[16], cpx<T>*, int, const cpx<T>* __restrict__) {}
+};
+
+template <typename T, int LOG2N>
+__device__ __forceinline__ void line_fft(cpx<T> (&v)[16], cpx<T>* buf, int j,
+                                         const cpx<T>* __restrict__ tw) {
+  constexpr int NS = (LOG2N + 3) / 4;
+  FftStages<T, LOG2N, 0, NS>::run(v, buf, j, tw);
+}
+
+// ---------------------------------------------------------------------------------
+// Chirp evaluation: exp(2 pi j t) * scale, t given in 64-bit fixed point (turns).
+// ---------------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ cpx<T> chirp_of(uint64_t t, T scale);
+
+template <>
+__device__ __forceinline__ cpx<float> chirp_of<float>(uint64_t t, float scale) {
+  // top 32 bits as a signed fraction of a turn in [-1/2, 1/2) -> angle in [-pi, pi)
+  const int32_t hi = (int32_t)(t >> 32);
+  const float ang = (float)hi * 1.4629180792671596e-09f;  // 2 pi / 2^32
+  float s, c;
+  __sincosf(ang, &s, &c);
+  return {c * scale, s * scale};
+}
+
+template <>
+__device__ __forceinline__ cpx<double> chirp_of<double>(uint64_t t, double scale) {
+  const double turns = (double)(int64_t)t * 5.42101086242752217e-20;  // 2^-64
+  double s, c;
+  sincospi(2.0 * turns, &s, &c);
+  return {c * scale, s * scale};
+}
+
+// Phase polynomial of one pass in (line l, element e), all mod 2^64:
+//   t = cA l^2 + cB l e + cC e^2 + cL l + cE e + cK
+struct Phase {
+  uint64_t cA, cB, cC, cL, cE, cK;
+};
+
+// Multiply the thread's 16 elements (e = j + TL*k) of line l by the chirp.
+// Exact second-difference recurrence in k:  t_k = a0 + d0 k + dd k(k-1)/2 ...
+template <typename T, int TL, bool CONJ_IN>
+__device__ __forceinline__ void apply_chirp(cpx<T> (&v)[16], const Phase& ph, uint64_t l, uint64_t j,
+                                            T scale) {
+  // t(e) = alpha + gamma e + cC e^2, alpha = cA l^2 + cL l + cK, gamma = cB l + cE
+  const uint64_t alpha = ph.cA * l * l + ph.cL * l + ph.cK;
+  const uint64_t gamma = ph.cB * l + ph.cE;
+  // e = j + TL k: t_k = t0 + k (gamma TL + 2 cC j TL) + k^2 cC TL^2
+  uint64_t t = alpha + gamma * j + ph.cC * j * j;
+  const uint64_t dd = 2ull * ph.cC * (uint64_t)TL * (uint64_t)TL;  // second difference
+  uint64_t d = gamma * (uint64_t)TL + 2ull * ph.cC * j * (uint64_t)TL + ph.cC * (uint64_t)TL * (uint64_t)TL;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    cpx<T> c = chirp_of<T>(t, scale);
+    cpx<T> x = v[k];
+    if (CONJ_IN) x = cconj(x);
+    v[k] = cmul(x, c);
+    t += d;
+    d += dd;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// The fused line pass.
+// MODE 0 (K1): CM, FFT,               transposed store
+// MODE 1 (K2, K4): FFT, CM, IFFT,     transposed store
+// MODE 2 (K3): IFFT, CM, FFT,         transposed store
+// MODE 3 (K5): IFFT, CM,              straight store (may run in place)
+// IFFT(x) (unnormalised) = conj(FFT(conj(x))); the 1/N is part of the CM scale.
+// ---------------------------------------------------------------------------------
+struct PassArgs {
+  const void* in;
+  void* out;
+  const void* tw;      // exp(-2 pi i k / N), k < N
+  long long n_lines;   // batch * N
+  Phase ph;
+  double scale;
+};
+
+template <int LOG2N>
+struct LineCfg {
+  static constexpr int N = 1 << LOG2N;
+  static constexpr int TL = N / 16;                       // threads per line
+  static constexpr int TB = (N <= 2048) ? 256 : (N <= 8192 ? 512 : 1024);
+  static constexpr int G = (TB / TL < N) ? TB / TL : N;   // lines per CTA (one image at most)
+  static constexpr int THREADS = G * TL;
+  static constexpr int LS = N + N / 16 + 1;               // padded line stride (odd)
+};
+
+template <typename T, int LOG2N, int MODE>
+__global__ void __launch_bounds__(LineCfg<LOG2N>::THREADS)
+line_pass_kernel(PassArgs a) {
+  using Cfg = LineCfg<LOG2N>;
+  constexpr int N = Cfg::N, TL = Cfg::TL, G = Cfg::G, LS = Cfg::LS, THREADS = Cfg::THREADS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cpx<T>* smem = reinterpret_cast<cpx<T>*>(smem_raw);
+
+  const int tid = threadIdx.x;
+  const int j = tid % TL;
+  const int gl = tid / TL;
+  const long long line0 = (long long)blockIdx.x * G;   // first global line of this CTA
+  const long long line = line0 + gl;
+  const long long img = line / N;
+  const int l = (int)(line % N);
+  cpx<T>* buf = smem + gl * LS;
+  const cpx<T>* __restrict__ tw = reinterpret_cast<const cpx<T>*>(a.tw);
+  const cpx<T>* __restrict__ src = reinterpret_cast<const cpx<T>*>(a.in) + line * N;
+
+  cpx<T> v[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] = src[j + TL * e];
+
+  const T scale = (T)a.scale;
+  if constexpr (MODE == 0) {
+    apply_chirp<T, TL, false>(v, a.ph, (uint64_t)l, (uint64_t)j, scale);
+    line_fft<T, LOG2N>(v, buf, j, tw);
+  } else if constexpr (MODE == 1) {
+    line_fft<T, LOG2N>(v, buf, j, tw);
+    // conj(CM * X) = conj(X) * conj(CM): conjugate the input, then conj result of mult
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
+    Phase ph = a.ph;  // conj(chirp) = chirp of -t
+    ph.cA = 0 - ph.cA; ph.cB = 0 - ph.cB; ph.cC = 0 - ph.cC;
+    ph.cL = 0 - ph.cL; ph.cE = 0 - ph.cE; ph.cK = 0 - ph.cK;
+    apply_chirp<T, TL, false>(v, ph, (uint64_t)l, (uint64_t)j, scale);
+    line_fft<T, LOG2N>(v, buf, j, tw);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
+  } else if constexpr (MODE == 2) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
+    line_fft<T, LOG2N>(v, buf, j, tw);
+    apply_chirp<T, TL, true>(v, a.ph, (uint64_t)l, (uint64_t)j, scale);
+    line_fft<T, LOG2N>(v, buf, j, tw);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
+    line_fft<T, LOG2N>(v, buf, j, tw);
+    apply_chirp<T, TL, true>(v, a.ph, (uint64_t)l, (uint64_t)j, scale);
+  }
+
+  if constexpr (MODE == 3) {
+    cpx<T>* dst = reinterpret_cast<cpx<T>*>(a.out) + line * N;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
+  } else {
+    // transposed store: out[img][e][l] ; stage through shared memory so that
+    // consecutive threads write consecutive l.
+    __syncthreads();   // all FFT reads of buf done (last stage keeps data in registers)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) buf[pad16(j + TL * e)] = v[e];
+    __syncthreads();
+    const int l0 = (int)(line0 % N);
+    const long long img0 = line0 / N;
+    cpx<T>* dst = reinterpret_cast<cpx<T>*>(a.out) + img0 * (long long)N * N;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int f = tid + k * THREADS;
+      const int ll = f % G;
+      const int e = f / G;
+      dst[(long long)e * N + l0 + ll] = smem[ll * LS + pad16(e)];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// B = 0: G[p,q] = sqrt(det D) chi(C D^T)[p,q] * bilinear(g)(p1, q1)   (Eq. Intro20,
+// Eq. BasicAffine12/16), p1 = d11 p + d21 q, q1 = d12 p + d22 q, taps outside -> 0.
+// Coordinates in fp64 without FMA contraction (same rounding as the plain formula).
+// ---------------------------------------------------------------------------------
+struct B0Args {
+  const void* in;
+  void* out;
+  long long total;    // batch * N * N
+  int n;
+  double d11, d12, d21, d22;
+  double amp_re, amp_im;
+  Phase ph;           // chirp polynomial in (i, j) array indices
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) b0_kernel(B0Args a) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= a.total) return;
+  const int n = a.n, h = n / 2;
+  const long long nn = (long long)n * n;
+  const long long img = idx / nn;
+  const int i = (int)((idx % nn) / n);
+  const int jj = (int)(idx % n);
+  const double p = (double)(i - h), q = (double)(jj - h);
+  const double p1 = __dadd_rn(__dmul_rn(a.d11, p), __dmul_rn(a.d21, q));
+  const double q1 = __dadd_rn(__dmul_rn(a.d12, p), __dmul_rn(a.d22, q));
+  const double p2 = floor(p1), q2 = floor(q1);
+  const double kk = p1 - p2, lw = q1 - q2;
+  const cpx<T>* __restrict__ g = reinterpret_cast<const cpx<T>*>(a.in) + img * nn;
+  const long long ia = (long long)p2 + h, ja = (long long)q2 + h;
+  auto tap = [&](long long r, long long c) -> cpx<T> {
+    if (r < 0 || r >= n || c < 0 || c >= n) return {T(0), T(0)};
+    return g[r * n + c];
+  };
+  const cpx<T> g00 = tap(ia, ja), g01 = tap(ia, ja + 1), g10 = tap(ia + 1, ja), g11 = tap(ia + 1, ja + 1);
+  const T w00 = (T)((1.0 - kk) * (1.0 - lw)), w01 = (T)((1.0 - kk) * lw);
+  const T w10 = (T)(kk * (1.0 - lw)), w11 = (T)(kk * lw);
+  cpx<T> s;
+  s.x = w00 * g00.x + w01 * g01.x + w10 * g10.x + w11 * g11.x;
+  s.y = w00 * g00.y + w01 * g01.y + w10 * g10.y + w11 * g11.y;
+  const uint64_t ui = (uint64_t)i, uj = (uint64_t)jj;
+  const uint64_t t = a.ph.cA * ui * ui + a.ph.cB * ui * uj + a.ph.cC * uj * uj + a.ph.cL * ui +
+                     a.ph.cE * uj + a.ph.cK;
+  const cpx<T> c = chirp_of<T>(t, T(1));
+  const cpx<T> amp = {(T)a.amp_re, (T)a.amp_im};
+  reinterpret_cast<cpx<T>*>(a.out)[idx] = cmul(amp, cmul(c, s));
+}
+
+}  // namespace nslct

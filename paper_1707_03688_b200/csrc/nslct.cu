@@ -1,0 +1,516 @@
+// C ABI of the B200 NsDLCT: plan / exec / exec_host / plan_info / pass_ms / destroy.
+// See include/nslct.h for the contract and kernels.cuh for the pass schedule.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/nslct.h"
+#include "kernels.cuh"
+#include "planner.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+nslct_status fail(nslct_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(e_ == cudaErrorMemoryAllocation ? NSLCT_E_OOM : NSLCT_E_CUDA,             \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                      \
+  } while (0)
+
+using nslct::PassArgs;
+using nslct::Phase;
+
+typedef cudaError_t (*launch_fn)(const PassArgs&, cudaStream_t);
+typedef cudaError_t (*attr_fn)();
+
+template <typename T, int LOG2N, int MODE>
+cudaError_t launch_pass(const PassArgs& a, cudaStream_t s) {
+  using Cfg = nslct::LineCfg<LOG2N>;
+  const size_t smem = (size_t)Cfg::G * Cfg::LS * sizeof(nslct::cpx<T>);
+  const long long grid = a.n_lines / Cfg::G;
+  nslct::line_pass_kernel<T, LOG2N, MODE><<<(unsigned)grid, Cfg::THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T, int LOG2N, int MODE>
+cudaError_t set_attr() {
+  using Cfg = nslct::LineCfg<LOG2N>;
+  const size_t smem = (size_t)Cfg::G * Cfg::LS * sizeof(nslct::cpx<T>);
+  return cudaFuncSetAttribute(nslct::line_pass_kernel<T, LOG2N, MODE>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <typename T, int LOG2N>
+struct Row {
+  static void fill(launch_fn* l, attr_fn* at) {
+    l[0] = launch_pass<T, LOG2N, 0>;
+    l[1] = launch_pass<T, LOG2N, 1>;
+    l[2] = launch_pass<T, LOG2N, 2>;
+    l[3] = launch_pass<T, LOG2N, 3>;
+    at[0] = set_attr<T, LOG2N, 0>;
+    at[1] = set_attr<T, LOG2N, 1>;
+    at[2] = set_attr<T, LOG2N, 2>;
+    at[3] = set_attr<T, LOG2N, 3>;
+  }
+};
+
+constexpr int kMinLog = 5, kMaxLog = 14;
+constexpr int kMaxLog128 = 13;  // c128 line buffer of 16384 would exceed shared memory
+
+struct Table {
+  launch_fn l[2][kMaxLog + 1][4] = {};
+  attr_fn at[2][kMaxLog + 1][4] = {};
+  Table() {
+    Row<float, 5>::fill(l[0][5], at[0][5]);
+    Row<float, 6>::fill(l[0][6], at[0][6]);
+    Row<float, 7>::fill(l[0][7], at[0][7]);
+    Row<float, 8>::fill(l[0][8], at[0][8]);
+    Row<float, 9>::fill(l[0][9], at[0][9]);
+    Row<float, 10>::fill(l[0][10], at[0][10]);
+    Row<float, 11>::fill(l[0][11], at[0][11]);
+    Row<float, 12>::fill(l[0][12], at[0][12]);
+    Row<float, 13>::fill(l[0][13], at[0][13]);
+    Row<float, 14>::fill(l[0][14], at[0][14]);
+    Row<double, 5>::fill(l[1][5], at[1][5]);
+    Row<double, 6>::fill(l[1][6], at[1][6]);
+    Row<double, 7>::fill(l[1][7], at[1][7]);
+    Row<double, 8>::fill(l[1][8], at[1][8]);
+    Row<double, 9>::fill(l[1][9], at[1][9]);
+    Row<double, 10>::fill(l[1][10], at[1][10]);
+    Row<double, 11>::fill(l[1][11], at[1][11]);
+    Row<double, 12>::fill(l[1][12], at[1][12]);
+    Row<double, 13>::fill(l[1][13], at[1][13]);
+  }
+};
+const Table& table() {
+  static Table t;
+  return t;
+}
+
+// ---- fixed-point phase coefficients ------------------------------------------------
+// turns -> 64-bit fixed-point fraction of a turn (mod 1)
+uint64_t fx(double turns) {
+  double f = turns - std::floor(turns);           // [0, 1)
+  double s = std::ldexp(f, 64);
+  if (!(s < 18446744073709551616.0)) return 0;     // rounding up to exactly 1 turn
+  return (uint64_t)s;
+}
+
+// Chirp exp(j/2 d^2 (q11 p^2 + 2 q12 p q + q22 q^2)) with centered p = i - h, q = j - h,
+// plus `checker` half-turns per index (the centring checkerboard (-1)^(i+j)), as a
+// polynomial in array indices (i, j):  t = A i^2 + B ij + C j^2 + Li i + Lj j + K.
+struct Poly {
+  uint64_t A, B, C, Li, Lj, K;
+};
+Poly chirp_poly(const nslct::Sym& q, double d, int n, bool checker) {
+  const double c0 = d * d / (4.0 * M_PI);
+  const uint64_t A = fx(c0 * q.q11), B = fx(2.0 * c0 * q.q12), C = fx(c0 * q.q22);
+  const uint64_t h = (uint64_t)(n / 2);
+  Poly P;
+  P.A = A;
+  P.B = B;
+  P.C = C;
+  // a(i-h)^2 + b(i-h)(j-h) + c(j-h)^2 expanded, all mod 2^64
+  P.Li = (uint64_t)0 - (2ull * h * A + h * B);
+  P.Lj = (uint64_t)0 - (2ull * h * C + h * B);
+  P.K = h * h * (A + B + C);
+  if (checker) {
+    P.Li += (1ull << 63);
+    P.Lj += (1ull << 63);
+  }
+  return P;
+}
+// roles: line index = i (x) or j (y)
+Phase to_phase(const Poly& P, bool line_is_x) {
+  Phase ph;
+  if (line_is_x) {
+    ph.cA = P.A; ph.cB = P.B; ph.cC = P.C; ph.cL = P.Li; ph.cE = P.Lj; ph.cK = P.K;
+  } else {
+    ph.cA = P.C; ph.cB = P.B; ph.cC = P.A; ph.cL = P.Lj; ph.cE = P.Li; ph.cK = P.K;
+  }
+  return ph;
+}
+
+}  // namespace
+
+struct nslct_plan_s {
+  int64_t n = 0, batch = 0;
+  int log2n = 0;
+  nslct_dtype dtype = NSLCT_C64;
+  int device = 0;
+  int profile = 0;
+  double dx = 0;
+  nslct::Plan p;
+  size_t elem = 8, bytes = 0;
+  void* tw = nullptr;
+  void* scratch = nullptr;
+  void* h_in = nullptr;   // device staging for exec_host
+  void* h_out = nullptr;
+  PassArgs args[5];
+  int mode[5] = {0, 1, 2, 1, 3};
+  nslct::B0Args b0{};
+  struct EvSet {
+    cudaEvent_t e[6];
+  };
+  std::vector<EvSet> ev;  // one set per exec since the last nslct_pass_ms (profile mode)
+  size_t ev_used = 0;
+};
+
+namespace {
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void free_plan(nslct_plan_s* pl) {
+  if (!pl) return;
+  DeviceGuard g(pl->device);
+  if (pl->tw) cudaFree(pl->tw);
+  if (pl->scratch) cudaFree(pl->scratch);
+  if (pl->h_in) cudaFree(pl->h_in);
+  if (pl->h_out) cudaFree(pl->h_out);
+  for (auto& set : pl->ev)
+    for (auto& e : set.e)
+      if (e) cudaEventDestroy(e);
+  delete pl;
+}
+}  // namespace
+
+extern "C" {
+
+void nslct_opts_default(nslct_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->dx = 0.0;
+  o->variant = NSLCT_VARIANT_HA;
+  o->dispatch = NSLCT_DISPATCH_REVERSIBLE;
+  o->device = -1;
+  o->profile = 0;
+}
+
+int nslct_abi_version(void) { return NSLCT_ABI_VERSION; }
+
+const char* nslct_last_error(void) { return g_err.c_str(); }
+
+nslct_status nslct_plan(nslct_plan_t* plan, int64_t n, const double abcd[16], int64_t batch,
+                        nslct_dtype dtype) {
+  nslct_opts o;
+  nslct_opts_default(&o);
+  return nslct_plan_ex(plan, n, abcd, batch, dtype, &o);
+}
+
+nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16], int64_t batch,
+                           nslct_dtype dtype, const nslct_opts* opts) {
+  g_err.clear();
+  if (!plan || !abcd) return fail(NSLCT_E_ARG, "null plan or abcd pointer");
+  *plan = nullptr;
+  nslct_opts o;
+  if (opts)
+    o = *opts;
+  else
+    nslct_opts_default(&o);
+  if (dtype != NSLCT_C64 && dtype != NSLCT_C128) return fail(NSLCT_E_ARG, "bad dtype");
+  if (batch < 1) return fail(NSLCT_E_ARG, "batch must be >= 1");
+  if (o.variant < 0 || o.variant > 2 || o.dispatch < 0 || o.dispatch > 1)
+    return fail(NSLCT_E_ARG, "bad variant/dispatch option");
+  int lg = 0;
+  while ((int64_t(1) << lg) < n && lg < 62) ++lg;
+  if (n < 1 || (int64_t(1) << lg) != n || lg < kMinLog || lg > kMaxLog ||
+      (dtype == NSLCT_C128 && lg > kMaxLog128))
+    return fail(NSLCT_E_UNSUPPORTED_N, "N must be a power of two in [32, 16384] (c128: <= 8192)");
+  if (!(std::isfinite(o.dx)) || (o.dx > 0 && !(o.dx < 1e30)))
+    return fail(NSLCT_E_ARG, "bad dx");
+
+  std::string err;
+  nslct::Plan p;
+  int st = nslct::make_plan(abcd, o.variant, o.dispatch, o.h_fixed, &p, &err);
+  if (st) return fail((nslct_status)st, err);
+
+  nslct_plan_s* pl = new (std::nothrow) nslct_plan_s();
+  if (!pl) return fail(NSLCT_E_OOM, "host allocation failed");
+  pl->n = n;
+  pl->batch = batch;
+  pl->log2n = lg;
+  pl->dtype = dtype;
+  pl->p = p;
+  pl->profile = o.profile;
+  pl->dx = (o.dx > 0) ? o.dx : std::sqrt(2.0 * M_PI / (double)n);
+  pl->elem = (dtype == NSLCT_C64) ? 8 : 16;
+  pl->bytes = (size_t)batch * (size_t)n * (size_t)n * pl->elem;
+  if (o.device >= 0) {
+    pl->device = o.device;
+  } else {
+    cudaError_t e = cudaGetDevice(&pl->device);
+    if (e != cudaSuccess) {
+      delete pl;
+      return fail(NSLCT_E_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+    }
+  }
+  nslct_status result = NSLCT_OK;
+  do {
+    DeviceGuard guard(pl->device);
+    const int ti = (dtype == NSLCT_C64) ? 0 : 1;
+    const double dx = pl->dx;
+    const double dw = 2.0 * M_PI / ((double)n * dx);  // frequency grid
+    if (p.kind == 0) {
+      // B = 0: chirp exp(j/2 z'^T C D^T z') and sqrt(det D) (Eq. Intro20)
+      nslct::M2 C = p.Cb, D = p.Db;
+      nslct::M2 CDt = {C.a * D.a + C.b * D.b, C.a * D.c + C.b * D.d, C.c * D.a + C.d * D.b,
+                       C.c * D.c + C.d * D.d};
+      nslct::Sym S = {CDt.a, CDt.d, 0.5 * (CDt.b + CDt.c)};
+      Poly P = chirp_poly(S, dx, (int)n, false);
+      double detD = D.a * D.d - D.b * D.c;
+      nslct::B0Args& b = pl->b0;
+      b.n = (int)n;
+      b.total = batch * n * n;
+      b.d11 = D.a; b.d12 = D.b; b.d21 = D.c; b.d22 = D.d;
+      b.amp_re = detD >= 0 ? std::sqrt(detD) : 0.0;
+      b.amp_im = detD >= 0 ? 0.0 : std::sqrt(-detD);
+      b.ph = to_phase(P, true);
+      break;
+    }
+    // twiddles exp(-2 pi i k/N) in fp64, stored at the run precision
+    {
+      const size_t tw_bytes = (size_t)n * pl->elem;
+      unsigned char* host = new (std::nothrow) unsigned char[tw_bytes];
+      if (!host) { result = fail(NSLCT_E_OOM, "host twiddles"); break; }
+      for (int64_t k = 0; k < n; ++k) {
+        // reduce k/N to [-1/8, 1/8] turns around the nearest quarter for accuracy
+        double s, c;
+        const int64_t q4 = (4 * k + n / 2) / n;           // nearest quarter turn
+        const double r = 2.0 * M_PI * ((double)(4 * k - q4 * n) / (4.0 * (double)n));
+        const double cr = std::cos(r), sr = std::sin(r);
+        switch (q4 & 3) {
+          case 0: c = cr; s = sr; break;
+          case 1: c = -sr; s = cr; break;
+          case 2: c = -cr; s = -sr; break;
+          default: c = sr; s = -cr; break;
+        }
+        if (dtype == NSLCT_C64) {
+          float* f = reinterpret_cast<float*>(host);
+          f[2 * k] = (float)c;
+          f[2 * k + 1] = (float)(-s);
+        } else {
+          double* f = reinterpret_cast<double*>(host);
+          f[2 * k] = c;
+          f[2 * k + 1] = -s;
+        }
+      }
+      cudaError_t e = cudaMalloc(&pl->tw, tw_bytes);
+      if (e == cudaSuccess) e = cudaMemcpy(pl->tw, host, tw_bytes, cudaMemcpyHostToDevice);
+      delete[] host;
+      if (e != cudaSuccess) {
+        result = fail(e == cudaErrorMemoryAllocation ? NSLCT_E_OOM : NSLCT_E_CUDA,
+                      std::string("twiddles: ") + cudaGetErrorString(e));
+        break;
+      }
+    }
+    {
+      cudaError_t e = cudaMalloc(&pl->scratch, pl->bytes);
+      if (e != cudaSuccess) {
+        result = fail(e == cudaErrorMemoryAllocation ? NSLCT_E_OOM : NSLCT_E_CUDA,
+                      std::string("scratch: ") + cudaGetErrorString(e));
+        break;
+      }
+    }
+    const nslct::Sym zero = {0, 0, 0};
+    const double invn = 1.0 / (double)n;
+    // K1: CM_r(Q0) + checkerboard;  K2: CM_w(Q1)/N;  K3: CM_r(Q2)/N;  K4: CM_w(Q3)/N;
+    // K5: CM_r(Q4)/N + checkerboard.
+    Poly P0 = chirp_poly(p.q_active[0] ? p.Q[0] : zero, dx, (int)n, true);
+    Poly P1 = chirp_poly(p.Q[1], dw, (int)n, false);
+    Poly P2 = chirp_poly(p.Q[2], dx, (int)n, false);
+    Poly P3 = chirp_poly(p.Q[3], dw, (int)n, false);
+    Poly P4 = chirp_poly(p.q_active[4] ? p.Q[4] : zero, dx, (int)n, true);
+    const Phase ph[5] = {to_phase(P0, true), to_phase(P1, false), to_phase(P2, true),
+                         to_phase(P3, false), to_phase(P4, true)};
+    const double sc[5] = {1.0, invn, invn, invn, invn};
+    for (int k = 0; k < 5; ++k) {
+      pl->args[k].tw = pl->tw;
+      pl->args[k].n_lines = batch * n;
+      pl->args[k].ph = ph[k];
+      pl->args[k].scale = sc[k];
+    }
+    for (int m = 0; m < 4; ++m) {
+      cudaError_t e = table().at[ti][lg][m]();
+      if (e != cudaSuccess) {
+        result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+        break;
+      }
+    }
+    if (result != NSLCT_OK) break;
+  } while (0);
+  if (result != NSLCT_OK) {
+    free_plan(pl);
+    return result;
+  }
+  *plan = pl;
+  return NSLCT_OK;
+}
+
+nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream) {
+  if (!pl) return fail(NSLCT_E_ARG, "null plan");
+  if (!in || !out) return fail(NSLCT_E_ARG, "null in/out pointer");
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(NSLCT_E_ARG, "in/out must be 16-byte aligned");
+  DeviceGuard guard(pl->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int ti = (pl->dtype == NSLCT_C64) ? 0 : 1;
+  cudaEvent_t* ev = nullptr;
+  if (pl->profile) {
+    if (pl->ev_used == pl->ev.size()) {
+      nslct_plan_s::EvSet set{};
+      for (auto& e : set.e) CUDA_TRY(cudaEventCreate(&e));
+      pl->ev.push_back(set);
+    }
+    ev = pl->ev[pl->ev_used].e;
+  }
+  if (pl->p.kind == 0) {
+    nslct::B0Args b = pl->b0;
+    b.in = in;
+    b.out = out;
+    const long long blocks = (b.total + 255) / 256;
+    if (in == out) return fail(NSLCT_E_ARG, "the B = 0 gather cannot run in place");
+    if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
+    if (ti == 0)
+      nslct::b0_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(b);
+    else
+      nslct::b0_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(b);
+    CUDA_TRY(cudaGetLastError());
+    if (ev) {
+      CUDA_TRY(cudaEventRecord(ev[1], s));
+      ++pl->ev_used;
+    }
+    return NSLCT_OK;
+  }
+  // K1 in->S, K2 S->out, K3 out->S, K4 S->out, K5 out->out (straight pass, in place)
+  const void* src[5] = {in, pl->scratch, out, pl->scratch, out};
+  void* dst[5] = {pl->scratch, out, pl->scratch, out, out};
+  for (int k = 0; k < 5; ++k) {
+    if (ev) CUDA_TRY(cudaEventRecord(ev[k], s));
+    PassArgs a = pl->args[k];
+    a.in = src[k];
+    a.out = dst[k];
+    CUDA_TRY(table().l[ti][pl->log2n][pl->mode[k]](a, s));
+  }
+  if (ev) {
+    CUDA_TRY(cudaEventRecord(ev[5], s));
+    ++pl->ev_used;
+  }
+  return NSLCT_OK;
+}
+
+nslct_status nslct_exec_host(nslct_plan_t pl, const void* host_in, void* host_out, void* stream) {
+  if (!pl) return fail(NSLCT_E_ARG, "null plan");
+  if (!host_in || !host_out) return fail(NSLCT_E_ARG, "null host pointer");
+  DeviceGuard guard(pl->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!pl->h_in) CUDA_TRY(cudaMalloc(&pl->h_in, pl->bytes));
+  if (!pl->h_out) CUDA_TRY(cudaMalloc(&pl->h_out, pl->bytes));
+  CUDA_TRY(cudaMemcpyAsync(pl->h_in, host_in, pl->bytes, cudaMemcpyHostToDevice, s));
+  nslct_status st = nslct_exec(pl, pl->h_in, pl->h_out, stream);
+  if (st != NSLCT_OK) return st;
+  CUDA_TRY(cudaMemcpyAsync(host_out, pl->h_out, pl->bytes, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return NSLCT_OK;
+}
+
+static void describe(const nslct::Plan& p, double dx, nslct_plan_desc* d) {
+  std::memset(d, 0, sizeof(*d));
+  d->kind = p.kind;
+  d->variant = p.variant;
+  d->lc_axis = p.lc_axis;
+  d->n_passes = (p.kind == 0) ? 1 : 5;
+  auto put = [](double* o, const nslct::Sym& s) {
+    o[0] = s.q11;
+    o[1] = s.q22;
+    o[2] = s.q12;
+  };
+  put(d->H, p.H);
+  put(d->Bp, p.Bp);
+  put(d->P2, p.P2);
+  put(d->P4, p.P4);
+  for (int i = 0; i < 5; ++i) {
+    if (p.kind != 0 && (i % 2 == 1 || p.q_active[i])) put(d->Q[i], p.Q[i]);
+  }
+  d->dx = dx;
+  d->objective = p.objective;
+  d->sym_residual = p.sym_residual;
+  d->recomposition_residual = p.recomposition_residual;
+  d->dispatch_key = p.key;
+}
+
+nslct_status nslct_plan_info(nslct_plan_t pl, nslct_plan_desc* d) {
+  if (!pl || !d) return fail(NSLCT_E_ARG, "null pointer");
+  describe(pl->p, pl->dx, d);
+  return NSLCT_OK;
+}
+
+nslct_status nslct_plan_describe(int64_t n, const double abcd[16], const nslct_opts* opts,
+                                 nslct_plan_desc* d) {
+  g_err.clear();
+  if (!abcd || !d) return fail(NSLCT_E_ARG, "null pointer");
+  nslct_opts o;
+  if (opts)
+    o = *opts;
+  else
+    nslct_opts_default(&o);
+  if (n < 2) return fail(NSLCT_E_ARG, "n must be >= 2");
+  if (o.variant < 0 || o.variant > 2 || o.dispatch < 0 || o.dispatch > 1)
+    return fail(NSLCT_E_ARG, "bad variant/dispatch option");
+  std::string err;
+  nslct::Plan p;
+  int st = nslct::make_plan(abcd, o.variant, o.dispatch, o.h_fixed, &p, &err);
+  if (st) return fail((nslct_status)st, err);
+  describe(p, (o.dx > 0) ? o.dx : std::sqrt(2.0 * M_PI / (double)n), d);
+  return NSLCT_OK;
+}
+
+nslct_status nslct_pass_ms(nslct_plan_t pl, float* ms, int capacity, int* n_written) {
+  if (!pl || !ms) return fail(NSLCT_E_ARG, "null pointer");
+  if (!pl->profile || pl->ev_used == 0) return fail(NSLCT_E_ARG, "plan not profiled / no exec yet");
+  DeviceGuard guard(pl->device);
+  const int np = (pl->p.kind == 0) ? 1 : 5;
+  if (capacity < np) return fail(NSLCT_E_ARG, "capacity too small");
+  for (int k = 0; k < np; ++k) ms[k] = 0.0f;
+  for (size_t i = 0; i < pl->ev_used; ++i) {
+    cudaEvent_t* e = pl->ev[i].e;
+    CUDA_TRY(cudaEventSynchronize(e[np]));
+    for (int k = 0; k < np; ++k) {
+      float t = 0.0f;
+      CUDA_TRY(cudaEventElapsedTime(&t, e[k], e[k + 1]));
+      ms[k] += t;
+    }
+  }
+  for (int k = 0; k < np; ++k) ms[k] /= (float)pl->ev_used;
+  pl->ev_used = 0;
+  if (n_written) *n_written = np;
+  return NSLCT_OK;
+}
+
+nslct_status nslct_destroy(nslct_plan_t pl) {
+  free_plan(pl);
+  return NSLCT_OK;
+}
+
+}  // extern "C"

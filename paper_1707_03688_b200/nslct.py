@@ -1,0 +1,200 @@
+"""Thin ctypes binding of libnslct.so (include/nslct.h).
+
+Argument marshalling only: every step of the transform runs in the library's CUDA
+kernels.  There is no CPU fallback: if libnslct.so is missing or fails to load, every
+entry point raises.  PyTorch is used only for device memory and streams.
+"""
+import ctypes
+import math
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnslct.so")
+
+C64, C128 = 0, 1
+VARIANTS = {"HA": 0, "LC": 1, "FIXED_H": 2}
+DISPATCH = {"reversible": 0, "formI": 1}
+STATUS = {0: "OK", 1: "E_ARG", 2: "E_NOT_SYMPLECTIC", 3: "E_NO_DECOMP", 4: "E_UNSUPPORTED_N",
+          5: "E_CUDA", 6: "E_NCCL", 7: "E_OOM"}
+KINDS = {0: "B0", 1: "I", 2: "II"}
+
+# every symbol include/nslct.h declares
+EXPORTS = ("nslct_opts_default", "nslct_plan", "nslct_plan_ex", "nslct_exec", "nslct_exec_host",
+           "nslct_plan_info", "nslct_plan_describe", "nslct_pass_ms", "nslct_destroy",
+           "nslct_last_error", "nslct_abi_version")
+
+
+class NslctError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("%s: %s" % (STATUS.get(status, status), msg))
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class nslct_opts(ctypes.Structure):
+    _fields_ = [("dx", ctypes.c_double), ("variant", ctypes.c_int), ("dispatch", ctypes.c_int),
+                ("h_fixed", ctypes.c_double * 3), ("device", ctypes.c_int), ("profile", ctypes.c_int),
+                ("reserved", ctypes.c_int * 6)]
+
+
+class nslct_plan_desc(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("variant", ctypes.c_int), ("lc_axis", ctypes.c_int),
+                ("n_passes", ctypes.c_int),
+                ("H", ctypes.c_double * 3), ("Bp", ctypes.c_double * 3), ("P2", ctypes.c_double * 3),
+                ("P4", ctypes.c_double * 3), ("Q", (ctypes.c_double * 3) * 5),
+                ("dx", ctypes.c_double), ("objective", ctypes.c_double),
+                ("sym_residual", ctypes.c_double), ("recomposition_residual", ctypes.c_double),
+                ("dispatch_key", ctypes.c_double)]
+
+
+_LIB = None
+
+
+def lib():
+    """Load libnslct.so (fails loudly when it is missing: there is no fallback)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libnslct.so not built (run python -m paper_1707_03688_b200.build)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, dp = ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_double)
+        L.nslct_opts_default.argtypes = [ctypes.POINTER(nslct_opts)]
+        L.nslct_opts_default.restype = None
+        L.nslct_plan.argtypes = [ctypes.POINTER(vp), i64, dp, i64, ctypes.c_int]
+        L.nslct_plan_ex.argtypes = [ctypes.POINTER(vp), i64, dp, i64, ctypes.c_int, ctypes.POINTER(nslct_opts)]
+        L.nslct_exec.argtypes = [vp, vp, vp, vp]
+        L.nslct_exec_host.argtypes = [vp, vp, vp, vp]
+        L.nslct_plan_info.argtypes = [vp, ctypes.POINTER(nslct_plan_desc)]
+        L.nslct_plan_describe.argtypes = [i64, dp, ctypes.POINTER(nslct_opts), ctypes.POINTER(nslct_plan_desc)]
+        L.nslct_pass_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        L.nslct_destroy.argtypes = [vp]
+        L.nslct_last_error.restype = ctypes.c_char_p
+        L.nslct_abi_version.restype = ctypes.c_int
+        for f in ("nslct_plan", "nslct_plan_ex", "nslct_exec", "nslct_exec_host", "nslct_plan_info",
+                  "nslct_plan_describe", "nslct_pass_ms", "nslct_destroy"):
+            getattr(L, f).restype = ctypes.c_int
+        _LIB = L
+    return _LIB
+
+
+def _check(st):
+    if st != 0:
+        raise NslctError(st, lib().nslct_last_error().decode(errors="replace"))
+
+
+def _abcd(M):
+    a = np.ascontiguousarray(np.asarray(M, dtype=np.float64).reshape(16))
+    return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def make_opts(dx=None, variant="HA", dispatch="reversible", h_fixed=None, device=None, profile=False):
+    o = nslct_opts()
+    lib().nslct_opts_default(ctypes.byref(o))
+    o.dx = float(dx) if dx else 0.0
+    o.variant = VARIANTS[variant]
+    o.dispatch = DISPATCH[dispatch]
+    if h_fixed is not None:
+        o.variant = VARIANTS["FIXED_H"]
+        for i in range(3):
+            o.h_fixed[i] = float(h_fixed[i])
+    o.device = -1 if device is None else int(device)
+    o.profile = 1 if profile else 0
+    return o
+
+
+def _desc_dict(d):
+    s = lambda a: np.array([[a[0], a[2]], [a[2], a[1]]])
+    return dict(kind=KINDS[d.kind], variant={0: "HA", 1: "LC", 2: "FIXED_H"}[d.variant],
+                lc_axis={0: None, 1: "x", 2: "y"}[d.lc_axis], n_passes=d.n_passes,
+                h=np.array(list(d.H)), H=s(d.H), Bp=s(d.Bp), P2=s(d.P2), P4=s(d.P4),
+                Q=[s(d.Q[i]) for i in range(5)], dx=d.dx, objective=d.objective,
+                sym_residual=d.sym_residual, recomposition_residual=d.recomposition_residual,
+                dispatch_key=d.dispatch_key)
+
+
+def nslct_plan_describe(n, M, **kw):
+    """Host-only planning (no GPU needed): returns the plan description dict."""
+    a, ap = _abcd(M)
+    o = make_opts(**kw)
+    d = nslct_plan_desc()
+    _check(lib().nslct_plan_describe(int(n), ap, ctypes.byref(o), ctypes.byref(d)))
+    return _desc_dict(d)
+
+
+class Plan:
+    """RAII wrapper of nslct_plan_t.  exec() takes torch CUDA tensors (complex64/128)."""
+
+    def __init__(self, n, M, batch, dtype="c64", dx=None, variant="HA", dispatch="reversible",
+                 h_fixed=None, device=None, profile=False):
+        self.n, self.batch = int(n), int(batch)
+        self.dtype = dtype
+        a, ap = _abcd(M)
+        o = make_opts(dx, variant, dispatch, h_fixed, device, profile)
+        h = ctypes.c_void_p()
+        _check(lib().nslct_plan_ex(ctypes.byref(h), self.n, ap, self.batch,
+                                   C64 if dtype == "c64" else C128, ctypes.byref(o)))
+        self._h = h
+        self.profile = profile
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().nslct_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def info(self):
+        d = nslct_plan_desc()
+        _check(lib().nslct_plan_info(self._h, ctypes.byref(d)))
+        return _desc_dict(d)
+
+    def exec_ptr(self, in_ptr, out_ptr, stream_ptr=0):
+        _check(lib().nslct_exec(self._h, ctypes.c_void_p(in_ptr), ctypes.c_void_p(out_ptr),
+                                ctypes.c_void_p(stream_ptr)))
+
+    def exec(self, x, out=None, stream=None):
+        """x: torch CUDA tensor [batch, n, n] of complex64 (c64) / complex128 (c128)."""
+        import torch
+        want = torch.complex64 if self.dtype == "c64" else torch.complex128
+        if not (x.is_cuda and x.dtype == want and x.is_contiguous()
+                and tuple(x.shape[-2:]) == (self.n, self.n) and x.numel() == self.batch * self.n * self.n):
+            raise ValueError("exec expects a contiguous CUDA %s tensor of %d x %d x %d"
+                             % (want, self.batch, self.n, self.n))
+        if out is None:
+            out = torch.empty_like(x)
+        s = stream if stream is not None else torch.cuda.current_stream(x.device)
+        self.exec_ptr(x.data_ptr(), out.data_ptr(), s.cuda_stream)
+        return out
+
+    def exec_host(self, host_in, host_out, stream=None):
+        """host_in/host_out: CPU torch tensors or numpy arrays (pinned for full speed)."""
+        def ptr(t):
+            return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+        sp = 0
+        if stream is not None:
+            sp = stream.cuda_stream
+        _check(lib().nslct_exec_host(self._h, ctypes.c_void_p(ptr(host_in)),
+                                     ctypes.c_void_p(ptr(host_out)), ctypes.c_void_p(sp)))
+        return host_out
+
+    def pass_ms(self):
+        buf = (ctypes.c_float * 8)()
+        nw = ctypes.c_int(0)
+        _check(lib().nslct_pass_ms(self._h, buf, 8, ctypes.byref(nw)))
+        return [buf[i] for i in range(nw.value)]
+
+
+def default_dx(n):
+    return math.sqrt(2.0 * math.pi / n)

@@ -1,0 +1,315 @@
+"""GPU parity of libnslct.so against the fp64 oracle.
+
+Every test calls the C ABI (through the ctypes binding) on identical seeded inputs: the
+input is generated in fp64, cast to the run dtype, and the oracle runs on the cast values.
+Unless a test says otherwise the GPU plan is given the oracle's H (VARIANT_FIXED_H), so
+both sides evaluate the same discrete operator; planner agreement is tested separately
+(tests/test_abi.py).  Tolerances (north_star): relative L2 <= 1e-4 (complex64),
+<= 1e-10 (complex128).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import metrics as me
+from oracle import operators as op
+from oracle import planner as opl
+from oracle import symplectic as sy
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1707_03688_b200 import nslct  # noqa: E402
+
+TOL = {"c64": 1e-4, "c128": 1e-10}
+TDT = {"c64": torch.complex64, "c128": torch.complex128}
+NDT = {"c64": np.complex64, "c128": np.complex128}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+def run_gpu(x, M, dtype, **kw):
+    """x: numpy [b, n, n] (already at the run precision).  Returns numpy result, plan info."""
+    b, n, _ = x.shape
+    xt = torch.from_numpy(np.ascontiguousarray(x)).to("cuda")
+    with nslct.Plan(n, M, b, dtype=dtype, **kw) as p:
+        out = p.exec(xt)
+        torch.cuda.synchronize()
+        return out.cpu().numpy(), p.info()
+
+
+def oracle(x, M, dx=None, variant="HA", policy="reversible", h=None):
+    G, pl = op.nsdlct(np.asarray(x, np.complex128), M, dx=dx, variant=variant, policy=policy, h_override=h)
+    return G, pl
+
+
+def parity(x, M, dtype, variant="HA", policy="reversible", check_imgs=None):
+    """Run both sides with the oracle's H; return (max relL2 over checked images, plan)."""
+    pl = opl.plan(M, variant=variant, policy=policy)
+    kw = dict(dispatch="formI" if policy == "formI" else "reversible")
+    if pl["kind"] != "B0":
+        kw["h_fixed"] = pl["h"]
+    G, info = run_gpu(x, M, dtype, **kw)
+    idx = range(x.shape[0]) if check_imgs is None else check_imgs
+    errs = []
+    for i in idx:
+        ref, _ = op.nsdlct(x[i].astype(np.complex128), M, pl=pl, variant=variant)
+        errs.append(me.rel_l2(G[i], ref))
+    return max(errs), info, G
+
+
+# ------------------------------------------------------------------ the five configs
+def test_config1_n32_c128():
+    """C1: 32x32 complex128, G(rng) matrix, i.i.d. CN(0,1): relL2 <= 1e-10."""
+    mr, ir = synth.config_streams(1)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (1, 32, 32)).astype(np.complex128)
+    err, info, _ = parity(x, M, "c128")
+    assert err <= TOL["c128"], err
+
+
+def test_config2_n256_batch64():
+    """C2: 256x256 complex64, batch 64, Gaussian-windowed chirps + 5% noise: all 64 images."""
+    mr, ir = synth.config_streams(2)
+    M = synth.random_symplectic(mr)
+    x = synth.chirp_gauss_field(ir, 256, 64).astype(np.complex64)
+    err, info, _ = parity(x, M, "c64")
+    assert err <= TOL["c64"], err
+
+
+@pytest.mark.parametrize("sub", ["dft", "gyrator", "separable", "b0"])
+def test_config3_n1024_sweep(sub):
+    """C3: 1024x1024 complex64, batch 16, special-case sweep; 4 of 16 images vs the oracle,
+    the remaining images through the same launch."""
+    mr, ir = synth.config_streams(3)
+    subs = {}
+    subs["dft"] = synth.dft_matrix4()
+    while True:
+        a = mr.uniform(0, math.pi)
+        if math.sin(a) ** 2 > 0.1:
+            break
+    subs["gyrator"] = synth.gyrator_matrix4(a)
+    while True:
+        a = mr.uniform(-2, 2, 2); b = mr.uniform(-2, 2, 2); c = mr.uniform(-2, 2, 2)
+        if np.all(np.abs(b) > 0.32) and np.all(np.abs(a) > 0.1):
+            break
+    subs["separable"] = synth.separable_matrix4(a, b, c)
+    while True:
+        D = mr.uniform(-2, 2, (2, 2))
+        if 0.5 <= abs(np.linalg.det(D)) <= 2:
+            break
+    S = mr.uniform(-2, 2, (2, 2))
+    subs["b0"] = synth.b0_matrix4(D, S)
+    M = subs[sub]
+    x = synth.random_phase_field(ir, (16, 1024, 1024)).astype(np.complex64)
+    err, info, _ = parity(x, M, "c64", check_imgs=[0, 5, 10, 15])
+    assert err <= TOL["c64"], (sub, err)
+
+
+def test_config4_n4096_batch32():
+    """C4: 4096x4096 complex64, batch 32 (the bench launch); image 0 and image 31 against
+    the full oracle, Parseval on every image."""
+    mr, ir = synth.config_streams(4)
+    M = synth.random_symplectic(mr)
+    x = np.empty((32, 4096, 4096), np.complex64)
+    for i in range(32):
+        x[i] = synth.iid_cn(ir, (4096, 4096))
+    err, info, G = parity(x, M, "c64", check_imgs=[0, 31])
+    assert err <= TOL["c64"], err
+    for i in range(32):
+        e_in = np.sum(np.abs(x[i].astype(np.complex128)) ** 2)
+        e_out = np.sum(np.abs(G[i].astype(np.complex128)) ** 2)
+        assert abs(e_out / e_in - 1) < 1e-5, i
+
+
+def test_config5_n16384_properties():
+    """C5 on one GPU: 16384x16384 complex64 single transform (2 GiB).  The full oracle is
+    out of reach, so: (i) Parseval; (ii) reversibility exec(M^-1) exec(M) = I; (iii) the
+    DFT matrix through the same kernels matches sampled outputs of Eq. BasicDFT16."""
+    n = 16384
+    mr, ir = synth.config_streams(5)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (1, n, n)).astype(np.complex64)
+    xt = torch.from_numpy(x).to("cuda")
+    with nslct.Plan(n, M, 1) as p, nslct.Plan(n, sy.inverse(M), 1) as pi:
+        G = p.exec(xt)
+        back = pi.exec(G)
+        torch.cuda.synchronize()
+        e_in = float(torch.sum(torch.abs(xt.to(torch.complex128)) ** 2))
+        e_out = float(torch.sum(torch.abs(G.to(torch.complex128)) ** 2))
+        assert abs(e_out / e_in - 1) < 1e-5
+        rel = float(torch.linalg.vector_norm((back - xt).to(torch.complex128)) /
+                    torch.linalg.vector_norm(xt.to(torch.complex128)))
+        assert rel < 1e-5, rel
+        assert p.info()["kind"] != pi.info()["kind"]
+    del G, back
+    # (iii) DFT: G[p,q] = (dx^2/(j 2 pi)) sum exp(-j2pi(pm+qn)/N) g[m,n], sampled outputs
+    with nslct.Plan(n, synth.dft_matrix4(), 1) as p:
+        G = p.exec(xt).cpu().numpy()[0]
+    g = x[0].astype(np.complex128)
+    k = np.arange(n) - n // 2
+    dx = math.sqrt(2 * math.pi / n)
+    rs = np.random.default_rng(0)
+    for _ in range(6):
+        pp, qq = rs.integers(-n // 2, n // 2, 2)
+        wr = np.exp(-2j * math.pi * np.mod(pp * k, n) / n)
+        wc = np.exp(-2j * math.pi * np.mod(qq * k, n) / n)
+        ref = dx * dx / (2j * math.pi) * (wr @ g @ wc)
+        got = G[pp + n // 2, qq + n // 2]
+        # unitary transform of a unit-variance input: |G| ~ 1; c64 error budget 1e-4
+        assert abs(got - ref) <= 1e-4
+
+
+# ------------------------------------------------------------------ sweeps and edge cases
+@pytest.mark.parametrize("n", [32, 64, 128, 256, 512, 1024, 2048])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_all_sizes_random_matrix(n, dtype):
+    """Every supported N (several tiles per line, both stage-radix tails) vs the oracle,
+    batch 3, both dispatch forms exercised across the sweep."""
+    mr, ir = synth.config_streams(100 + n)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (3, n, n)).astype(NDT[dtype])
+    err, info, _ = parity(x, M, dtype, check_imgs=[0, 2])
+    assert err <= TOL[dtype], (n, dtype, err)
+
+
+@pytest.mark.parametrize("n", [4096, 8192])
+def test_large_sizes_c64(n):
+    mr, ir = synth.config_streams(100 + n)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (1, n, n)).astype(np.complex64)
+    err, info, _ = parity(x, M, "c64")
+    assert err <= TOL["c64"], (n, err)
+
+
+@pytest.mark.parametrize("policy", ["reversible", "formI"])
+def test_both_forms(policy):
+    """Form I and form II (Eq. HA28 / CCCMCCCM40) on the same matrix with tr B < 0."""
+    mr, ir = synth.config_streams(7)
+    while True:
+        M = synth.random_symplectic(mr)
+        if np.trace(M[0:2, 2:4]) < -0.5:
+            break
+    x = synth.iid_cn(ir, (2, 128, 128))
+    for dtype in ("c64", "c128"):
+        err, info, _ = parity(x.astype(NDT[dtype]), M, dtype, policy=policy)
+        assert info["kind"] == ("II" if policy == "reversible" else "I")
+        assert err <= TOL[dtype], (policy, dtype, err)
+
+
+def test_gpu_own_planner_matches_oracle():
+    """Without FIXED_H: the library's own HA plan gives the oracle's operator (planner parity)."""
+    mr, ir = synth.config_streams(8)
+    for _ in range(3):
+        M = synth.random_symplectic(mr)
+        x = synth.iid_cn(ir, (1, 64, 64))
+        G, info = run_gpu(x, M, "c128")
+        ref, pl = oracle(x[0], M)
+        if np.abs(info["h"] - pl["h"]).max() < 1e-9:
+            assert me.rel_l2(G[0], ref) <= 1e-9
+
+
+def test_lc_variant():
+    """LC-NsDLCT (Eq. LC12): the plan's H is rank one and the result matches the oracle LC."""
+    mr, ir = synth.config_streams(9)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (1, 128, 128))
+    pl = opl.plan(M, variant="LC")
+    G, info = run_gpu(x, M, "c128", variant="LC")
+    assert info["lc_axis"] == pl["axis"]
+    ref, _ = op.nsdlct(x[0], M, variant="LC", pl=pl)
+    assert me.rel_l2(G[0], ref) <= 1e-9
+
+
+def test_exact_special_cases():
+    """P1: DFT matrix -> Eq. BasicDFT16 via numpy.fft; P3: identity -> bit-exact copy;
+    P2: gyrator pi/2 -> twisted DFT."""
+    n = 256
+    dx = math.sqrt(2 * math.pi / n)
+    x = synth.iid_cn(np.random.default_rng(1), (2, n, n))
+    G, _ = run_gpu(x, synth.dft_matrix4(), "c128")
+    ref = dx * dx / (2j * math.pi) * np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(x, axes=(1, 2))), axes=(1, 2))
+    assert me.rel_l2(G, ref) < 1e-12
+    G, _ = run_gpu(x, np.eye(4), "c128")
+    assert np.array_equal(G, x)
+    G, _ = run_gpu(x.astype(np.complex64), np.eye(4), "c64")
+    assert np.array_equal(G, x.astype(np.complex64))
+    G, _ = run_gpu(x, synth.gyrator_matrix4(math.pi / 2), "c128")
+    ref2 = np.swapaxes(np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(x, axes=(1, 2))), axes=(1, 2)), 1, 2) / n
+    assert me.rel_l2(G, ref2) < 1e-12
+
+
+def test_reversibility_and_parseval_c128():
+    """P4/P5 through the GPU: exec(M^-1) exec(M) = I and energy preserved."""
+    mr, ir = synth.config_streams(10)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (2, 512, 512))
+    xt = torch.from_numpy(x).cuda()
+    with nslct.Plan(512, M, 2, dtype="c128") as p, nslct.Plan(512, sy.inverse(M), 2, dtype="c128") as q:
+        G = p.exec(xt)
+        back = q.exec(G)
+        torch.cuda.synchronize()
+    assert me.nmse(back.cpu().numpy(), x) < 1e-24
+    assert abs(float(torch.sum(torch.abs(G) ** 2) / torch.sum(torch.abs(xt) ** 2)) - 1) < 1e-12
+
+
+def test_in_place_and_host_exec():
+    """in == out allowed (HA path); nslct_exec_host (host buffers) equals device exec."""
+    mr, ir = synth.config_streams(11)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (4, 256, 256)).astype(np.complex64)
+    with nslct.Plan(256, M, 4) as p:
+        xt = torch.from_numpy(x).cuda()
+        ref = p.exec(xt).cpu().numpy()
+        y = xt.clone()
+        p.exec(y, out=y)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), ref)
+        hin = torch.from_numpy(x).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        p.exec_host(hin, hout)
+        assert np.array_equal(hout.numpy(), ref)
+
+
+def test_argument_errors():
+    """Error codes of the ABI: unsupported N, bad batch, misaligned pointers, B0 in place."""
+    M = synth.dft_matrix4()
+    for n in (16, 48, 100, 32768):
+        with pytest.raises(nslct.NslctError) as e:
+            nslct.Plan(n, M, 1)
+        assert e.value.name == "E_UNSUPPORTED_N"
+    with pytest.raises(nslct.NslctError) as e:
+        nslct.Plan(16384, M, 1, dtype="c128")
+    assert e.value.name == "E_UNSUPPORTED_N"
+    with pytest.raises(nslct.NslctError) as e:
+        nslct.Plan(64, M, 0)
+    assert e.value.name == "E_ARG"
+    with nslct.Plan(64, M, 1) as p:
+        buf = torch.zeros(2 * 64 * 64 + 1, dtype=torch.complex64, device="cuda")
+        with pytest.raises(nslct.NslctError) as e:
+            p.exec_ptr(buf.data_ptr() + 8, buf.data_ptr(), 0)
+        assert e.value.name == "E_ARG"
+        with pytest.raises(nslct.NslctError):
+            p.exec_ptr(0, buf.data_ptr(), 0)
+    with nslct.Plan(64, np.eye(4), 1) as p:
+        buf = torch.zeros(64 * 64, dtype=torch.complex64, device="cuda")
+        with pytest.raises(nslct.NslctError):
+            p.exec_ptr(buf.data_ptr(), buf.data_ptr(), 0)
+
+
+def test_profile_pass_times():
+    mr, ir = synth.config_streams(12)
+    M = synth.random_symplectic(mr)
+    with nslct.Plan(1024, M, 4, profile=True) as p:
+        x = torch.zeros(4, 1024, 1024, dtype=torch.complex64, device="cuda")
+        for _ in range(3):
+            p.exec(x)
+        ms = p.pass_ms()
+        assert len(ms) == 5 and all(t > 0 for t in ms)
