@@ -162,6 +162,29 @@ __device__ __forceinline__ void dft(cpx<T>* u) {
   }
 }
 
+// w[r] = w1^r for r = 1..R-1 (w[0] unused), products of depth <= 4.
+template <int R, typename T>
+__device__ __forceinline__ void twiddle_powers(cpx<T> w1, cpx<T> (&w)[R]) {
+  w[1] = w1;
+  if constexpr (R >= 4) {
+    w[2] = cmul(w1, w1);
+    w[3] = cmul(w[2], w1);
+  }
+  if constexpr (R == 2) {
+    return;
+  } else if constexpr (R >= 8) {
+    w[4] = cmul(w[2], w[2]);
+    w[5] = cmul(w[4], w1);
+    w[6] = cmul(w[4], w[2]);
+    w[7] = cmul(w[4], w[3]);
+  }
+  if constexpr (R == 16) {
+    w[8] = cmul(w[4], w[4]);
+#pragma unroll
+    for (int r = 9; r < 16; ++r) w[r] = cmul(w[8], w[r - 8]);
+  }
+}
+
 // ---------------------------------------------------------------------------------
 // Line FFT of length N = 2^LOG2N, E = 16 elements per thread, TL = N/16 threads per line.
 // Register slot e of thread j holds element j + TL*e, before and after (Stockham
@@ -170,9 +193,20 @@ __device__ __forceinline__ void dft(cpx<T>* u) {
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
 
-template <typename T, int LOG2N, int STAGE, int NS>
+// Exchange-buffer layouts.  PadLayout: padded index (buffer N + N/16 per line).
+// SwzLayout: unpadded, XOR-swizzled 16-element groups (the TMA staging buffer doubles as
+// the exchange buffer); c = per-line constant so G lines read together hit distinct banks.
+struct PadLayout {
+  __device__ __forceinline__ int operator()(int i) const { return pad16(i); }
+};
+struct SwzLayout {
+  int c;
+  __device__ __forceinline__ int operator()(int i) const { return i ^ (((i >> 4) + c) & 15); }
+};
+
+template <typename T, int LOG2N, int STAGE, int NS, class L>
 __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], cpx<T>* buf, int j,
-                                          const cpx<T>* __restrict__ tw) {
+                                          const cpx<T>* __restrict__ tw, L lay) {
   constexpr int N = 1 << LOG2N;
   constexpr int TL = N / 16;
   constexpr int NFULL = LOG2N / 4;
@@ -187,9 +221,13 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], cpx<T>* buf, int j,
 #pragma unroll
     for (int r = 0; r < R; ++r) u[r] = v[b + r * NB];
     if constexpr (Ns > 1) {
+      // twiddles w^r, w = exp(-2 pi i k0/N): one (L1-resident) table load per butterfly,
+      // powers by products of depth <= 4 (error ~4 ulp), instead of R-1 strided loads.
       const int k0 = (jp % Ns) * (N / (Ns * R));
+      cpx<T> w[R];
+      twiddle_powers<R>(tw[k0], w);
 #pragma unroll
-      for (int r = 1; r < R; ++r) u[r] = cmul(u[r], tw[k0 * r]);
+      for (int r = 1; r < R; ++r) u[r] = cmul(u[r], w[r]);
     }
     dft<R>(u);
 #pragma unroll
@@ -197,35 +235,35 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], cpx<T>* buf, int j,
     if constexpr (!LAST) {
       const int idxD = (jp / Ns) * Ns * R + (jp % Ns);
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[pad16(idxD + r * Ns)] = u[r];
+      for (int r = 0; r < R; ++r) buf[lay(idxD + r * Ns)] = u[r];
     }
   }
   if constexpr (!LAST) {
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = buf[pad16(j + TL * e)];
+    for (int e = 0; e < 16; ++e) v[e] = buf[lay(j + TL * e)];
     __syncthreads();
   }
 }
 
-template <typename T, int LOG2N, int STAGE, int NS>
+template <typename T, int LOG2N, int STAGE, int NS, class L>
 struct FftStages {
   __device__ __forceinline__ static void run(cpx<T> (&v)[16], cpx<T>* buf, int j,
-                                             const cpx<T>* __restrict__ tw) {
-    fft_stage<T, LOG2N, STAGE, NS>(v, buf, j, tw);
-    FftStages<T, LOG2N, STAGE + 1, NS>::run(v, buf, j, tw);
+                                             const cpx<T>* __restrict__ tw, L lay) {
+    fft_stage<T, LOG2N, STAGE, NS, L>(v, buf, j, tw, lay);
+    FftStages<T, LOG2N, STAGE + 1, NS, L>::run(v, buf, j, tw, lay);
   }
 };
-template <typename T, int LOG2N, int NS>
-struct FftStages<T, LOG2N, NS, NS> {
-  __device__ __forceinline__ static void run(cpx<T> (&)[16], cpx<T>*, int, const cpx<T>* __restrict__) {}
+template <typename T, int LOG2N, int NS, class L>
+struct FftStages<T, LOG2N, NS, NS, L> {
+  __device__ __forceinline__ static void run(cpx<T> (&)[16], cpx<T>*, int, const cpx<T>* __restrict__, L) {}
 };
 
-template <typename T, int LOG2N>
+template <typename T, int LOG2N, class L = PadLayout>
 __device__ __forceinline__ void line_fft(cpx<T> (&v)[16], cpx<T>* buf, int j,
-                                         const cpx<T>* __restrict__ tw) {
+                                         const cpx<T>* __restrict__ tw, L lay = L()) {
   constexpr int NS = (LOG2N + 3) / 4;
-  FftStages<T, LOG2N, 0, NS>::run(v, buf, j, tw);
+  FftStages<T, LOG2N, 0, NS, L>::run(v, buf, j, tw, lay);
 }
 
 // ---------------------------------------------------------------------------------
@@ -298,6 +336,41 @@ struct PassArgs {
   double scale;
 };
 
+// The per-line work of one pass (registers v hold elements j + TL*e of line l).
+template <typename T, int LOG2N, int MODE, class L>
+__device__ __forceinline__ void pass_body(cpx<T> (&v)[16], cpx<T>* buf, int j,
+                                          const cpx<T>* __restrict__ tw, const Phase& ph0,
+                                          uint64_t l, T scale, L lay) {
+  constexpr int TL = (1 << LOG2N) / 16;
+  if constexpr (MODE == 0) {
+    apply_chirp<T, TL, false>(v, ph0, l, (uint64_t)j, scale);
+    line_fft<T, LOG2N>(v, buf, j, tw, lay);
+  } else if constexpr (MODE == 1) {
+    line_fft<T, LOG2N>(v, buf, j, tw, lay);
+    // IFFT(CM X) = conj(FFT(conj(X) conj(CM))); conj(CM) is the chirp of -t
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
+    Phase ph = ph0;
+    ph.cA = 0 - ph.cA; ph.cB = 0 - ph.cB; ph.cC = 0 - ph.cC;
+    ph.cL = 0 - ph.cL; ph.cE = 0 - ph.cE; ph.cK = 0 - ph.cK;
+    apply_chirp<T, TL, false>(v, ph, l, (uint64_t)j, scale);
+    line_fft<T, LOG2N>(v, buf, j, tw, lay);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
+  } else if constexpr (MODE == 2) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
+    line_fft<T, LOG2N>(v, buf, j, tw, lay);
+    apply_chirp<T, TL, true>(v, ph0, l, (uint64_t)j, scale);
+    line_fft<T, LOG2N>(v, buf, j, tw, lay);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
+    line_fft<T, LOG2N>(v, buf, j, tw, lay);
+    apply_chirp<T, TL, true>(v, ph0, l, (uint64_t)j, scale);
+  }
+}
+
 template <int LOG2N>
 struct LineCfg {
   static constexpr int N = 1 << LOG2N;
@@ -305,7 +378,9 @@ struct LineCfg {
   static constexpr int TB = (N <= 2048) ? 256 : (N <= 8192 ? 512 : 1024);
   static constexpr int G = (TB / TL < N) ? TB / TL : N;   // lines per CTA (one image at most)
   static constexpr int THREADS = G * TL;
-  static constexpr int LS = N + N / 16 + 1;               // padded line stride (odd)
+  // padded line stride: LS = 16/G (mod 16) spreads the G lines read together by the
+  // transposed store over distinct banks (G <= 16), LS odd otherwise.
+  static constexpr int LS = N + N / 16 + ((G >= 16) ? 1 : 16 / G);
 };
 
 template <typename T, int LOG2N, int MODE>
@@ -331,34 +406,7 @@ line_pass_kernel(PassArgs a) {
 #pragma unroll
   for (int e = 0; e < 16; ++e) v[e] = src[j + TL * e];
 
-  const T scale = (T)a.scale;
-  if constexpr (MODE == 0) {
-    apply_chirp<T, TL, false>(v, a.ph, (uint64_t)l, (uint64_t)j, scale);
-    line_fft<T, LOG2N>(v, buf, j, tw);
-  } else if constexpr (MODE == 1) {
-    line_fft<T, LOG2N>(v, buf, j, tw);
-    // conj(CM * X) = conj(X) * conj(CM): conjugate the input, then conj result of mult
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
-    Phase ph = a.ph;  // conj(chirp) = chirp of -t
-    ph.cA = 0 - ph.cA; ph.cB = 0 - ph.cB; ph.cC = 0 - ph.cC;
-    ph.cL = 0 - ph.cL; ph.cE = 0 - ph.cE; ph.cK = 0 - ph.cK;
-    apply_chirp<T, TL, false>(v, ph, (uint64_t)l, (uint64_t)j, scale);
-    line_fft<T, LOG2N>(v, buf, j, tw);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
-  } else if constexpr (MODE == 2) {
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
-    line_fft<T, LOG2N>(v, buf, j, tw);
-    apply_chirp<T, TL, true>(v, a.ph, (uint64_t)l, (uint64_t)j, scale);
-    line_fft<T, LOG2N>(v, buf, j, tw);
-  } else {
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
-    line_fft<T, LOG2N>(v, buf, j, tw);
-    apply_chirp<T, TL, true>(v, a.ph, (uint64_t)l, (uint64_t)j, scale);
-  }
+  pass_body<T, LOG2N, MODE>(v, buf, j, tw, a.ph, (uint64_t)l, (T)a.scale, PadLayout());
 
   if constexpr (MODE == 3) {
     cpx<T>* dst = reinterpret_cast<cpx<T>*>(a.out) + line * N;
@@ -381,6 +429,145 @@ line_pass_kernel(PassArgs a) {
       const int e = f / G;
       dst[(long long)e * N + l0 + ll] = smem[ll * LS + pad16(e)];
     }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Persistent, TMA-pipelined variant of the line pass (sm_100a).  One CTA per SM loops over
+// groups of G contiguous lines.  Each group is brought into shared memory by ONE bulk
+// async copy (cp.async.bulk, completion on an mbarrier) issued one iteration ahead, so HBM
+// reads overlap the FFT/chirp work of the previous group.  The staging buffer of the
+// current group is then reused, XOR-swizzled, as its FFT exchange buffer; two buffers
+// alternate.  Stores are issued from registers (straight) or through the swizzled
+// buffer (transposed) and drain while the next group computes.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int LOG2N>
+struct PipeCfg {
+  static constexpr int N = 1 << LOG2N;
+  static constexpr int TL = N / 16;
+  static constexpr int THREADS = 512;
+  static constexpr int G = THREADS / TL;                    // lines per group (>= 1)
+  static constexpr int GROUP_ELEMS = G * N;                 // = 16 * THREADS = 8192
+  static constexpr int SWZ_STEP = (G >= 16) ? 1 : 16 / G;   // per-line swizzle offset
+};
+
+template <typename T, int LOG2N, int MODE>
+__global__ void __launch_bounds__(512, 1)
+line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counter) {
+  using Cfg = PipeCfg<LOG2N>;
+  constexpr int N = Cfg::N, TL = Cfg::TL, G = Cfg::G, THREADS = Cfg::THREADS;
+  constexpr int GE = Cfg::GROUP_ELEMS;
+  constexpr uint32_t GROUP_BYTES = GE * sizeof(cpx<T>);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cpx<T>* stage = reinterpret_cast<cpx<T>*>(smem_raw);                       // 2 x GE
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 2 * GROUP_BYTES);  // 2 mbarriers
+  long long* s_next = reinterpret_cast<long long*>(bar + 2);                // 2 slots
+
+  const int tid = threadIdx.x;
+  const int j = tid % TL;
+  const int gl = tid / TL;
+  const SwzLayout lay{gl * Cfg::SWZ_STEP};
+  const cpx<T>* __restrict__ tw = reinterpret_cast<const cpx<T>*>(a.tw);
+  const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in);
+  cpx<T>* __restrict__ out = reinterpret_cast<cpx<T>*>(a.out);
+
+  // Groups are claimed in order from a global counter (not round-robin) so the groups
+  // in flight across the GPU stay a contiguous window: the 8*G-byte pieces of the
+  // transposed stores of neighbouring groups then meet in L2 and leave as full lines.
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    const long long g0 = (long long)atomicAdd(counter, 1ull);
+    if (g0 < n_groups) {
+      mbar_expect_tx(&bar[0], GROUP_BYTES);
+      bulk_g2s(stage, in + g0 * GE, GROUP_BYTES, &bar[0]);
+    }
+    s_next[1] = g0;
+  }
+  __syncthreads();
+  long long g = s_next[1];
+  for (int k = 0; g < n_groups; ++k) {
+    const int b = k & 1;
+    cpx<T>* sb = stage + b * GE;
+    if (tid == 0) {   // claim and prefetch the next group into the other buffer
+      const long long gn = (long long)atomicAdd(counter, 1ull);
+      if (gn < n_groups) {
+        fence_proxy_async_smem();        // its previous generic-proxy use is complete (barrier)
+        mbar_expect_tx(&bar[b ^ 1], GROUP_BYTES);
+        bulk_g2s(stage + (b ^ 1) * GE, in + gn * GE, GROUP_BYTES, &bar[b ^ 1]);
+      }
+      s_next[b] = gn;
+    }
+    mbar_wait(&bar[b], (uint32_t)((k >> 1) & 1));
+
+    const long long line0 = g * G;
+    const int l = (int)((line0 + gl) % N);
+    cpx<T>* buf = sb + gl * N;
+    cpx<T> v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = buf[j + TL * e];
+    __syncthreads();   // every thread has its inputs; the buffer becomes the exchange space
+
+    pass_body<T, LOG2N, MODE>(v, buf, j, tw, a.ph, (uint64_t)l, (T)a.scale, lay);
+
+    if constexpr (MODE == 3) {
+      cpx<T>* dst = out + (line0 + gl) * N;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
+    } else {
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) buf[lay(j + TL * e)] = v[e];
+      __syncthreads();
+      const int l0 = (int)(line0 % N);
+      cpx<T>* dst = out + (line0 / N) * (long long)N * N + l0;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const int f = tid + kk * THREADS;
+        const int ll = f % G;
+        const int e = f / G;
+        const SwzLayout lr{ll * Cfg::SWZ_STEP};
+        dst[(long long)e * N + ll] = sb[ll * N + lr(e)];
+      }
+    }
+    __syncthreads();   // buffer b is free for the prefetch issued in iteration k+1
+    g = s_next[b];
   }
 }
 

@@ -4,6 +4,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -53,6 +54,41 @@ cudaError_t set_attr() {
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
+// persistent TMA-pipelined variant: grid = #SMs (one CTA per SM)
+constexpr size_t kPipeExtra = 64;   // 2 mbarriers + 2 claimed-group slots
+template <typename T, int LOG2N, int MODE>
+cudaError_t launch_pipe(const PassArgs& a, cudaStream_t s, int grid, unsigned long long* counter) {
+  using Cfg = nslct::PipeCfg<LOG2N>;
+  const size_t smem = 2 * (size_t)Cfg::GROUP_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
+  const long long n_groups = a.n_lines / Cfg::G;
+  const long long g = n_groups < grid ? n_groups : grid;
+  nslct::line_pass_pipe_kernel<T, LOG2N, MODE><<<(unsigned)g, Cfg::THREADS, smem, s>>>(a, n_groups, counter);
+  return cudaGetLastError();
+}
+template <typename T, int LOG2N, int MODE>
+cudaError_t set_attr_pipe() {
+  using Cfg = nslct::PipeCfg<LOG2N>;
+  const size_t smem = 2 * (size_t)Cfg::GROUP_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
+  return cudaFuncSetAttribute(nslct::line_pass_pipe_kernel<T, LOG2N, MODE>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+typedef cudaError_t (*pipe_fn)(const PassArgs&, cudaStream_t, int, unsigned long long*);
+
+template <typename T, int LOG2N>
+struct PipeRow {
+  static void fill(pipe_fn* l, attr_fn* at) {
+    l[0] = launch_pipe<T, LOG2N, 0>;
+    l[1] = launch_pipe<T, LOG2N, 1>;
+    l[2] = launch_pipe<T, LOG2N, 2>;
+    l[3] = launch_pipe<T, LOG2N, 3>;
+    at[0] = set_attr_pipe<T, LOG2N, 0>;
+    at[1] = set_attr_pipe<T, LOG2N, 1>;
+    at[2] = set_attr_pipe<T, LOG2N, 2>;
+    at[3] = set_attr_pipe<T, LOG2N, 3>;
+  }
+};
+constexpr int kPipeMinLog = 10, kPipeMaxLog = 13;
+
 template <typename T, int LOG2N>
 struct Row {
   static void fill(launch_fn* l, attr_fn* at) {
@@ -73,7 +109,13 @@ constexpr int kMaxLog128 = 13;  // c128 line buffer of 16384 would exceed shared
 struct Table {
   launch_fn l[2][kMaxLog + 1][4] = {};
   attr_fn at[2][kMaxLog + 1][4] = {};
+  pipe_fn lp[kMaxLog + 1][4] = {};   // c64 only
+  attr_fn atp[kMaxLog + 1][4] = {};
   Table() {
+    PipeRow<float, 10>::fill(lp[10], atp[10]);
+    PipeRow<float, 11>::fill(lp[11], atp[11]);
+    PipeRow<float, 12>::fill(lp[12], atp[12]);
+    PipeRow<float, 13>::fill(lp[13], atp[13]);
     Row<float, 5>::fill(l[0][5], at[0][5]);
     Row<float, 6>::fill(l[0][6], at[0][6]);
     Row<float, 7>::fill(l[0][7], at[0][7]);
@@ -101,12 +143,14 @@ const Table& table() {
 }
 
 // ---- fixed-point phase coefficients ------------------------------------------------
-// turns -> 64-bit fixed-point fraction of a turn (mod 1)
+// turns -> 64-bit fixed-point fraction of a turn (mod 1).  x - nearbyint(x) is exact in
+// fp64 and keeps the full relative precision of a small |x| (reducing a small negative
+// x to 1 - |x| first would round it to 2^-53 turns, ~1e-10 turns after scaling by i^2).
 uint64_t fx(double turns) {
-  double f = turns - std::floor(turns);           // [0, 1)
-  double s = std::ldexp(f, 64);
-  if (!(s < 18446744073709551616.0)) return 0;     // rounding up to exactly 1 turn
-  return (uint64_t)s;
+  const double f = turns - std::nearbyint(turns);   // [-1/2, 1/2], exact
+  double v = std::ldexp(f, 64);                      // [-2^63, 2^63], exact
+  if (v >= 9223372036854775808.0) v -= 18446744073709551616.0;
+  return (uint64_t)(int64_t)v;
 }
 
 // Chirp exp(j/2 d^2 (q11 p^2 + 2 q12 p q + q22 q^2)) with centered p = i - h, q = j - h,
@@ -161,6 +205,9 @@ struct nslct_plan_s {
   void* h_out = nullptr;
   PassArgs args[5];
   int mode[5] = {0, 1, 2, 1, 3};
+  bool pipe = false;   // persistent TMA-pipelined kernels
+  unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
+  int num_sms = 148;
   nslct::B0Args b0{};
   struct EvSet {
     cudaEvent_t e[6];
@@ -187,6 +234,7 @@ void free_plan(nslct_plan_s* pl) {
   DeviceGuard g(pl->device);
   if (pl->tw) cudaFree(pl->tw);
   if (pl->scratch) cudaFree(pl->scratch);
+  if (pl->counters) cudaFree(pl->counters);
   if (pl->h_in) cudaFree(pl->h_in);
   if (pl->h_out) cudaFree(pl->h_out);
   for (auto& set : pl->ev)
@@ -351,6 +399,28 @@ nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16],
       pl->args[k].ph = ph[k];
       pl->args[k].scale = sc[k];
     }
+    {
+      int sms = 0;
+      if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device) == cudaSuccess && sms > 0)
+        pl->num_sms = sms;
+      const char* np = std::getenv("NSLCT_NO_PIPE");
+      pl->pipe = (ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
+    }
+    if (pl->pipe) {
+      cudaError_t e = cudaMalloc(&pl->counters, 8 * sizeof(unsigned long long));
+      if (e != cudaSuccess) {
+        result = fail(NSLCT_E_OOM, std::string("counters: ") + cudaGetErrorString(e));
+        break;
+      }
+    }
+    for (int m = 0; m < 4 && pl->pipe; ++m) {
+      cudaError_t e = table().atp[lg][m]();
+      if (e != cudaSuccess) {
+        result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(pipe): ") + cudaGetErrorString(e));
+        break;
+      }
+    }
+    if (result != NSLCT_OK) break;
     for (int m = 0; m < 4; ++m) {
       cudaError_t e = table().at[ti][lg][m]();
       if (e != cudaSuccess) {
@@ -403,6 +473,7 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
     }
     return NSLCT_OK;
   }
+  if (pl->pipe) CUDA_TRY(cudaMemsetAsync(pl->counters, 0, 5 * sizeof(unsigned long long), s));
   // K1 in->S, K2 S->out, K3 out->S, K4 S->out, K5 out->out (straight pass, in place)
   const void* src[5] = {in, pl->scratch, out, pl->scratch, out};
   void* dst[5] = {pl->scratch, out, pl->scratch, out, out};
@@ -411,7 +482,10 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
     PassArgs a = pl->args[k];
     a.in = src[k];
     a.out = dst[k];
-    CUDA_TRY(table().l[ti][pl->log2n][pl->mode[k]](a, s));
+    if (pl->pipe)
+      CUDA_TRY(table().lp[pl->log2n][pl->mode[k]](a, s, pl->num_sms, pl->counters + k));
+    else
+      CUDA_TRY(table().l[ti][pl->log2n][pl->mode[k]](a, s));
   }
   if (ev) {
     CUDA_TRY(cudaEventRecord(ev[5], s));

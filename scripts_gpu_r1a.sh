@@ -1,0 +1,7 @@
+#!/bin/bash
+# first GPU call: smoke, parity tests, short bench
+cd $GRAFT_REPO_ROOT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 600 -k "not config4 and not config5 and not large" > gpurun_out/pytest_small.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_small.log
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "rc=$?" >> gpurun_out/bench.log
