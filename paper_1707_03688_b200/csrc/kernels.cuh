@@ -162,26 +162,46 @@ __device__ __forceinline__ void dft(cpx<T>* u) {
   }
 }
 
-// w[r] = w1^r for r = 1..R-1 (w[0] unused), products of depth <= 4.
+// u[r] *= w1^r, r = 1..R-1, generating the powers on the fly (product depth <= 5, so
+// the error stays a few ulp) with few live registers: the upper half is first scaled by
+// w1^(R/2), then u[r] and u[r + R/2] share w1^r.
 template <int R, typename T>
-__device__ __forceinline__ void twiddle_powers(cpx<T> w1, cpx<T> (&w)[R]) {
-  w[1] = w1;
-  if constexpr (R >= 4) {
-    w[2] = cmul(w1, w1);
-    w[3] = cmul(w[2], w1);
-  }
+__device__ __forceinline__ void apply_twiddles(cpx<T>* u, cpx<T> w1) {
   if constexpr (R == 2) {
-    return;
-  } else if constexpr (R >= 8) {
-    w[4] = cmul(w[2], w[2]);
-    w[5] = cmul(w[4], w1);
-    w[6] = cmul(w[4], w[2]);
-    w[7] = cmul(w[4], w[3]);
-  }
-  if constexpr (R == 16) {
-    w[8] = cmul(w[4], w[4]);
+    u[1] = cmul(u[1], w1);
+  } else if constexpr (R == 4) {
+    const cpx<T> w2 = cmul(w1, w1);
+    u[1] = cmul(u[1], w1);
+    u[2] = cmul(u[2], w2);
+    u[3] = cmul(u[3], cmul(w2, w1));
+  } else {
+    constexpr int H = R / 2;
+    const cpx<T> w2 = cmul(w1, w1);
+    const cpx<T> w4 = cmul(w2, w2);
+    cpx<T> wh = w4;
+    if constexpr (R == 16) wh = cmul(w4, w4);
 #pragma unroll
-    for (int r = 9; r < 16; ++r) w[r] = cmul(w[8], w[r - 8]);
+    for (int r = H; r < R; ++r) u[r] = cmul(u[r], wh);
+    u[1] = cmul(u[1], w1);
+    u[H + 1] = cmul(u[H + 1], w1);
+    u[2] = cmul(u[2], w2);
+    u[H + 2] = cmul(u[H + 2], w2);
+    const cpx<T> w3 = cmul(w2, w1);
+    u[3] = cmul(u[3], w3);
+    u[H + 3] = cmul(u[H + 3], w3);
+    if constexpr (R == 16) {
+      u[4] = cmul(u[4], w4);
+      u[12] = cmul(u[12], w4);
+      const cpx<T> w5 = cmul(w4, w1);
+      u[5] = cmul(u[5], w5);
+      u[13] = cmul(u[13], w5);
+      const cpx<T> w6 = cmul(w4, w2);
+      u[6] = cmul(u[6], w6);
+      u[14] = cmul(u[14], w6);
+      const cpx<T> w7 = cmul(w4, w3);
+      u[7] = cmul(u[7], w7);
+      u[15] = cmul(u[15], w7);
+    }
   }
 }
 
@@ -193,20 +213,37 @@ __device__ __forceinline__ void twiddle_powers(cpx<T> w1, cpx<T> (&w)[R]) {
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
 
-// Exchange-buffer layouts.  PadLayout: padded index (buffer N + N/16 per line).
-// SwzLayout: unpadded, XOR-swizzled 16-element groups (the TMA staging buffer doubles as
-// the exchange buffer); c = per-line constant so G lines read together hit distinct banks.
-struct PadLayout {
-  __device__ __forceinline__ int operator()(int i) const { return pad16(i); }
+// Exchange policies (how a stage hands its outputs to the next stage through shared
+// memory).  X is the compile-time index of the exchange within the pass.
+//  ExPad: one padded buffer (index i + i/16, N + N/16 per line); write, barrier, read,
+//         barrier.
+//  ExSwz: two unpadded buffers used alternately (exchange X uses buffer X & 1) with an
+//         XOR swizzle of each 16-element group: write, barrier, read -- the next write
+//         goes to the other buffer, so the trailing barrier is not needed.  c is a
+//         per-line constant so the G lines read together by the transposed store hit
+//         distinct banks.  Buffer 0 is the TMA staging buffer of the current group.
+template <typename T>
+struct ExPad {
+  static constexpr bool kDouble = false;
+  cpx<T>* buf;
+  template <int X>
+  __device__ __forceinline__ cpx<T>* b() const { return buf; }
+  __device__ __forceinline__ int idx(int i) const { return pad16(i); }
 };
-struct SwzLayout {
+template <typename T>
+struct ExSwz {
+  static constexpr bool kDouble = true;
+  cpx<T>* buf0;
+  cpx<T>* buf1;
   int c;
-  __device__ __forceinline__ int operator()(int i) const { return i ^ (((i >> 4) + c) & 15); }
+  template <int X>
+  __device__ __forceinline__ cpx<T>* b() const { return (X & 1) ? buf1 : buf0; }
+  __device__ __forceinline__ int idx(int i) const { return i ^ (((i >> 4) + c) & 15); }
 };
 
-template <typename T, int LOG2N, int STAGE, int NS, class L>
-__device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], cpx<T>* buf, int j,
-                                          const cpx<T>* __restrict__ tw, L lay) {
+template <typename T, int LOG2N, int STAGE, int NS, int X, class E>
+__device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const cpx<T>* __restrict__ tw,
+                                          const E& ex) {
   constexpr int N = 1 << LOG2N;
   constexpr int TL = N / 16;
   constexpr int NFULL = LOG2N / 4;
@@ -214,6 +251,7 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], cpx<T>* buf, int j,
   constexpr int NB = 16 / R;
   constexpr bool LAST = (STAGE == NS - 1);
   constexpr int Ns = (STAGE < NFULL) ? (1 << (4 * STAGE)) : (1 << (4 * NFULL));
+  cpx<T>* buf = ex.template b<X>();
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int jp = j + b * TL;
@@ -224,10 +262,7 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], cpx<T>* buf, int j,
       // twiddles w^r, w = exp(-2 pi i k0/N): one (L1-resident) table load per butterfly,
       // powers by products of depth <= 4 (error ~4 ulp), instead of R-1 strided loads.
       const int k0 = (jp % Ns) * (N / (Ns * R));
-      cpx<T> w[R];
-      twiddle_powers<R>(tw[k0], w);
-#pragma unroll
-      for (int r = 1; r < R; ++r) u[r] = cmul(u[r], w[r]);
+      apply_twiddles<R>(u, tw[k0]);
     }
     dft<R>(u);
 #pragma unroll
@@ -235,35 +270,41 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], cpx<T>* buf, int j,
     if constexpr (!LAST) {
       const int idxD = (jp / Ns) * Ns * R + (jp % Ns);
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[lay(idxD + r * Ns)] = u[r];
+      for (int r = 0; r < R; ++r) buf[ex.idx(idxD + r * Ns)] = u[r];
     }
   }
   if constexpr (!LAST) {
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = buf[lay(j + TL * e)];
-    __syncthreads();
+    for (int e = 0; e < 16; ++e) v[e] = buf[ex.idx(j + TL * e)];
+    if constexpr (!E::kDouble) __syncthreads();
   }
 }
 
-template <typename T, int LOG2N, int STAGE, int NS, class L>
+template <typename T, int LOG2N, int STAGE, int NS, int X0, class E>
 struct FftStages {
-  __device__ __forceinline__ static void run(cpx<T> (&v)[16], cpx<T>* buf, int j,
-                                             const cpx<T>* __restrict__ tw, L lay) {
-    fft_stage<T, LOG2N, STAGE, NS, L>(v, buf, j, tw, lay);
-    FftStages<T, LOG2N, STAGE + 1, NS, L>::run(v, buf, j, tw, lay);
+  __device__ __forceinline__ static void run(cpx<T> (&v)[16], int j, const cpx<T>* __restrict__ tw,
+                                             const E& ex) {
+    fft_stage<T, LOG2N, STAGE, NS, X0 + STAGE, E>(v, j, tw, ex);
+    FftStages<T, LOG2N, STAGE + 1, NS, X0, E>::run(v, j, tw, ex);
   }
 };
-template <typename T, int LOG2N, int NS, class L>
-struct FftStages<T, LOG2N, NS, NS, L> {
-  __device__ __forceinline__ static void run(cpx<T> (&)[16], cpx<T>*, int, const cpx<T>* __restrict__, L) {}
+template <typename T, int LOG2N, int NS, int X0, class E>
+struct FftStages<T, LOG2N, NS, NS, X0, E> {
+  __device__ __forceinline__ static void run(cpx<T> (&)[16], int, const cpx<T>* __restrict__, const E&) {}
 };
 
-template <typename T, int LOG2N, class L = PadLayout>
-__device__ __forceinline__ void line_fft(cpx<T> (&v)[16], cpx<T>* buf, int j,
-                                         const cpx<T>* __restrict__ tw, L lay = L()) {
-  constexpr int NS = (LOG2N + 3) / 4;
-  FftStages<T, LOG2N, 0, NS, L>::run(v, buf, j, tw, lay);
+template <int LOG2N>
+struct FftInfo {
+  static constexpr int NS = (LOG2N + 3) / 4;   // stages
+  static constexpr int NX = NS - 1;            // exchanges per FFT
+};
+
+// FFT of the thread's line; X0 = index of its first exchange within the pass.
+template <typename T, int LOG2N, int X0, class E>
+__device__ __forceinline__ void line_fft(cpx<T> (&v)[16], int j, const cpx<T>* __restrict__ tw,
+                                         const E& ex) {
+  FftStages<T, LOG2N, 0, FftInfo<LOG2N>::NS, X0, E>::run(v, j, tw, ex);
 }
 
 // ---------------------------------------------------------------------------------
@@ -337,16 +378,22 @@ struct PassArgs {
 };
 
 // The per-line work of one pass (registers v hold elements j + TL*e of line l).
-template <typename T, int LOG2N, int MODE, class L>
-__device__ __forceinline__ void pass_body(cpx<T> (&v)[16], cpx<T>* buf, int j,
-                                          const cpx<T>* __restrict__ tw, const Phase& ph0,
-                                          uint64_t l, T scale, L lay) {
+// Exchanges used: MODE 0, 3: NX;  MODE 1, 2: 2 NX.
+template <int LOG2N, int MODE>
+struct PassInfo {
+  static constexpr int NX = FftInfo<LOG2N>::NX * ((MODE == 1 || MODE == 2) ? 2 : 1);
+};
+
+template <typename T, int LOG2N, int MODE, class E>
+__device__ __forceinline__ void pass_body(cpx<T> (&v)[16], int j, const cpx<T>* __restrict__ tw,
+                                          const Phase& ph0, uint64_t l, T scale, const E& ex) {
   constexpr int TL = (1 << LOG2N) / 16;
+  constexpr int NX = FftInfo<LOG2N>::NX;
   if constexpr (MODE == 0) {
     apply_chirp<T, TL, false>(v, ph0, l, (uint64_t)j, scale);
-    line_fft<T, LOG2N>(v, buf, j, tw, lay);
+    line_fft<T, LOG2N, 0>(v, j, tw, ex);
   } else if constexpr (MODE == 1) {
-    line_fft<T, LOG2N>(v, buf, j, tw, lay);
+    line_fft<T, LOG2N, 0>(v, j, tw, ex);
     // IFFT(CM X) = conj(FFT(conj(X) conj(CM))); conj(CM) is the chirp of -t
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
@@ -354,19 +401,19 @@ __device__ __forceinline__ void pass_body(cpx<T> (&v)[16], cpx<T>* buf, int j,
     ph.cA = 0 - ph.cA; ph.cB = 0 - ph.cB; ph.cC = 0 - ph.cC;
     ph.cL = 0 - ph.cL; ph.cE = 0 - ph.cE; ph.cK = 0 - ph.cK;
     apply_chirp<T, TL, false>(v, ph, l, (uint64_t)j, scale);
-    line_fft<T, LOG2N>(v, buf, j, tw, lay);
+    line_fft<T, LOG2N, NX>(v, j, tw, ex);
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
   } else if constexpr (MODE == 2) {
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
-    line_fft<T, LOG2N>(v, buf, j, tw, lay);
+    line_fft<T, LOG2N, 0>(v, j, tw, ex);
     apply_chirp<T, TL, true>(v, ph0, l, (uint64_t)j, scale);
-    line_fft<T, LOG2N>(v, buf, j, tw, lay);
+    line_fft<T, LOG2N, NX>(v, j, tw, ex);
   } else {
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
-    line_fft<T, LOG2N>(v, buf, j, tw, lay);
+    line_fft<T, LOG2N, 0>(v, j, tw, ex);
     apply_chirp<T, TL, true>(v, ph0, l, (uint64_t)j, scale);
   }
 }
@@ -406,7 +453,7 @@ line_pass_kernel(PassArgs a) {
 #pragma unroll
   for (int e = 0; e < 16; ++e) v[e] = src[j + TL * e];
 
-  pass_body<T, LOG2N, MODE>(v, buf, j, tw, a.ph, (uint64_t)l, (T)a.scale, PadLayout());
+  pass_body<T, LOG2N, MODE>(v, j, tw, a.ph, (uint64_t)l, (T)a.scale, ExPad<T>{buf});
 
   if constexpr (MODE == 3) {
     cpx<T>* dst = reinterpret_cast<cpx<T>*>(a.out) + line * N;
@@ -484,7 +531,16 @@ struct PipeCfg {
   static constexpr int G = THREADS / TL;                    // lines per group (>= 1)
   static constexpr int GROUP_ELEMS = G * N;                 // = 16 * THREADS = 8192
   static constexpr int SWZ_STEP = (G >= 16) ? 1 : 16 / G;   // per-line swizzle offset
+  static constexpr int NBUF = 3;                            // 2 staging + 1 exchange
+  static constexpr int IL = 2;   // interleave of the intermediate layout (see below)
+  static_assert(G % IL == 0, "pipe kernels need an even number of lines per group");
 };
+// Intermediate layout between pipe passes ("pair-interleaved transposed"): element mu of
+// line lambda (lines as the NEXT pass reads them) lives at
+//     (lambda / IL) * IL*N + mu * IL + lambda % IL.
+// A consumer group of G lines is still one contiguous block (one bulk copy), and a
+// producer holding G lines writes G*IL-element contiguous segments (>= 32 B: full L2
+// sectors; 16-byte half-sector writes measured ~5x slower, tools/micro_bench.cu).
 
 template <typename T, int LOG2N, int MODE>
 __global__ void __launch_bounds__(512, 1)
@@ -494,14 +550,14 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
   constexpr int GE = Cfg::GROUP_ELEMS;
   constexpr uint32_t GROUP_BYTES = GE * sizeof(cpx<T>);
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  cpx<T>* stage = reinterpret_cast<cpx<T>*>(smem_raw);                       // 2 x GE
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 2 * GROUP_BYTES);  // 2 mbarriers
+  cpx<T>* stage = reinterpret_cast<cpx<T>*>(smem_raw);                       // buffers 0, 1
+  cpx<T>* xbuf = stage + 2 * GE;                                            // buffer 2
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 3 * GROUP_BYTES);  // 2 mbarriers
   long long* s_next = reinterpret_cast<long long*>(bar + 2);                // 2 slots
 
   const int tid = threadIdx.x;
   const int j = tid % TL;
   const int gl = tid / TL;
-  const SwzLayout lay{gl * Cfg::SWZ_STEP};
   const cpx<T>* __restrict__ tw = reinterpret_cast<const cpx<T>*>(a.tw);
   const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in);
   cpx<T>* __restrict__ out = reinterpret_cast<cpx<T>*>(a.out);
@@ -525,49 +581,60 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
   for (int k = 0; g < n_groups; ++k) {
     const int b = k & 1;
     cpx<T>* sb = stage + b * GE;
-    if (tid == 0) {   // claim and prefetch the next group into the other buffer
+    mbar_wait(&bar[b], (uint32_t)((k >> 1) & 1));
+
+    const long long line0 = g * G;
+    const int l = (int)((line0 + gl) % N);
+    cpx<T> v[16];
+    if constexpr (MODE == 0) {   // the user's row-major input: lines are contiguous
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = sb[gl * N + j + TL * e];
+    } else {                     // pair-interleaved intermediate
+      const cpx<T>* src = sb + (gl / Cfg::IL) * (Cfg::IL * N) + (gl % Cfg::IL);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = src[(j + TL * e) * Cfg::IL];
+    }
+    // Everyone has its inputs, and everyone has finished iteration k-1: buffer b^1 (used
+    // by iteration k-1) may now be refilled and buffer b becomes exchange space.
+    __syncthreads();
+    if (tid == 0) {   // claim and prefetch the next group
       const long long gn = (long long)atomicAdd(counter, 1ull);
       if (gn < n_groups) {
-        fence_proxy_async_smem();        // its previous generic-proxy use is complete (barrier)
+        fence_proxy_async_smem();      // order the generic-proxy uses of buffer b^1 before TMA
         mbar_expect_tx(&bar[b ^ 1], GROUP_BYTES);
         bulk_g2s(stage + (b ^ 1) * GE, in + gn * GE, GROUP_BYTES, &bar[b ^ 1]);
       }
       s_next[b] = gn;
     }
-    mbar_wait(&bar[b], (uint32_t)((k >> 1) & 1));
 
-    const long long line0 = g * G;
-    const int l = (int)((line0 + gl) % N);
-    cpx<T>* buf = sb + gl * N;
-    cpx<T> v[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = buf[j + TL * e];
-    __syncthreads();   // every thread has its inputs; the buffer becomes the exchange space
-
-    pass_body<T, LOG2N, MODE>(v, buf, j, tw, a.ph, (uint64_t)l, (T)a.scale, lay);
+    const ExSwz<T> ex{sb + gl * N, xbuf + gl * N, gl * Cfg::SWZ_STEP};
+    pass_body<T, LOG2N, MODE>(v, j, tw, a.ph, (uint64_t)l, (T)a.scale, ex);
 
     if constexpr (MODE == 3) {
       cpx<T>* dst = out + (line0 + gl) * N;
 #pragma unroll
       for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
     } else {
-      __syncthreads();
+      constexpr int XT = PassInfo<LOG2N, MODE>::NX;   // exchange index of the store
+      cpx<T>* tb = (XT & 1) ? xbuf : sb;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) buf[lay(j + TL * e)] = v[e];
+      for (int e = 0; e < 16; ++e) tb[gl * N + ex.idx(j + TL * e)] = v[e];
       __syncthreads();
+      // pair-interleaved transposed store: segment ep holds elements e = IL*ep .. IL*ep+IL-1
+      // of this group's G lines: G*IL contiguous elements at ep*IL*N + l0*IL.
+      constexpr int SEG = G * Cfg::IL;
       const int l0 = (int)(line0 % N);
-      cpx<T>* dst = out + (line0 / N) * (long long)N * N + l0;
+      cpx<T>* dst = out + (line0 / N) * (long long)N * N + (long long)l0 * Cfg::IL;
 #pragma unroll
       for (int kk = 0; kk < 16; ++kk) {
         const int f = tid + kk * THREADS;
-        const int ll = f % G;
-        const int e = f / G;
-        const SwzLayout lr{ll * Cfg::SWZ_STEP};
-        dst[(long long)e * N + ll] = sb[ll * N + lr(e)];
+        const int ep = f / SEG, sub = f % SEG;
+        const int ll = sub / Cfg::IL, e = ep * Cfg::IL + sub % Cfg::IL;
+        const int c = ll * Cfg::SWZ_STEP;
+        dst[(long long)ep * (Cfg::IL * N) + sub] = tb[ll * N + (e ^ (((e >> 4) + c) & 15))];
       }
     }
-    __syncthreads();   // buffer b is free for the prefetch issued in iteration k+1
-    g = s_next[b];
+    g = s_next[b];   // written by thread 0 before at least one later barrier
   }
 }
 

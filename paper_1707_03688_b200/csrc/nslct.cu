@@ -59,7 +59,7 @@ constexpr size_t kPipeExtra = 64;   // 2 mbarriers + 2 claimed-group slots
 template <typename T, int LOG2N, int MODE>
 cudaError_t launch_pipe(const PassArgs& a, cudaStream_t s, int grid, unsigned long long* counter) {
   using Cfg = nslct::PipeCfg<LOG2N>;
-  const size_t smem = 2 * (size_t)Cfg::GROUP_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
+  const size_t smem = (size_t)Cfg::NBUF * Cfg::GROUP_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
   const long long n_groups = a.n_lines / Cfg::G;
   const long long g = n_groups < grid ? n_groups : grid;
   nslct::line_pass_pipe_kernel<T, LOG2N, MODE><<<(unsigned)g, Cfg::THREADS, smem, s>>>(a, n_groups, counter);
@@ -68,7 +68,7 @@ cudaError_t launch_pipe(const PassArgs& a, cudaStream_t s, int grid, unsigned lo
 template <typename T, int LOG2N, int MODE>
 cudaError_t set_attr_pipe() {
   using Cfg = nslct::PipeCfg<LOG2N>;
-  const size_t smem = 2 * (size_t)Cfg::GROUP_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
+  const size_t smem = (size_t)Cfg::NBUF * Cfg::GROUP_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
   return cudaFuncSetAttribute(nslct::line_pass_pipe_kernel<T, LOG2N, MODE>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
@@ -87,7 +87,7 @@ struct PipeRow {
     at[3] = set_attr_pipe<T, LOG2N, 3>;
   }
 };
-constexpr int kPipeMinLog = 10, kPipeMaxLog = 13;
+constexpr int kPipeMinLog = 10, kPipeMaxLog = 12;  // needs an even number of lines per group
 
 template <typename T, int LOG2N>
 struct Row {
@@ -115,7 +115,6 @@ struct Table {
     PipeRow<float, 10>::fill(lp[10], atp[10]);
     PipeRow<float, 11>::fill(lp[11], atp[11]);
     PipeRow<float, 12>::fill(lp[12], atp[12]);
-    PipeRow<float, 13>::fill(lp[13], atp[13]);
     Row<float, 5>::fill(l[0][5], at[0][5]);
     Row<float, 6>::fill(l[0][6], at[0][6]);
     Row<float, 7>::fill(l[0][7], at[0][7]);
