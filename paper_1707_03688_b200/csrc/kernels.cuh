@@ -225,14 +225,26 @@ __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
 template <typename T>
 struct ExPad {
   static constexpr bool kDouble = false;
+  static constexpr bool kPadded = true;
   cpx<T>* buf;
   template <int X>
   __device__ __forceinline__ cpx<T>* b() const { return buf; }
   __device__ __forceinline__ int idx(int i) const { return pad16(i); }
 };
 template <typename T>
+struct ExPad2 {   // two padded buffers used alternately: write, barrier, read
+  static constexpr bool kDouble = true;
+  static constexpr bool kPadded = true;
+  cpx<T>* buf0;
+  cpx<T>* buf1;
+  template <int X>
+  __device__ __forceinline__ cpx<T>* b() const { return (X & 1) ? buf1 : buf0; }
+  __device__ __forceinline__ int idx(int i) const { return pad16(i); }
+};
+template <typename T>
 struct ExSwz {
   static constexpr bool kDouble = true;
+  static constexpr bool kPadded = false;
   cpx<T>* buf0;
   cpx<T>* buf1;
   int c;
@@ -252,6 +264,12 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const cpx<T>* 
   constexpr bool LAST = (STAGE == NS - 1);
   constexpr int Ns = (STAGE < NFULL) ? (1 << (4 * STAGE)) : (1 << (4 * NFULL));
   cpx<T>* buf = ex.template b<X>();
+  // Padded layouts: pad16(i + k) = pad16(i) + k + k/16 whenever k is a multiple of 16,
+  // or i is a multiple of 16 and k < 16 -- so one base per butterfly/thread plus
+  // compile-time offsets (the compiler cannot prove j < TL by itself).
+  constexpr bool FAST = E::kPadded && (TL % 16 == 0);
+  constexpr int WSTEP = (Ns >= 16) ? Ns + Ns / 16 : Ns;
+  constexpr int RSTEP = TL + TL / 16;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int jp = j + b * TL;
@@ -260,7 +278,7 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const cpx<T>* 
     for (int r = 0; r < R; ++r) u[r] = v[b + r * NB];
     if constexpr (Ns > 1) {
       // twiddles w^r, w = exp(-2 pi i k0/N): one (L1-resident) table load per butterfly,
-      // powers by products of depth <= 4 (error ~4 ulp), instead of R-1 strided loads.
+      // powers by products of depth <= 5 (error a few ulp), instead of R-1 strided loads.
       const int k0 = (jp % Ns) * (N / (Ns * R));
       apply_twiddles<R>(u, tw[k0]);
     }
@@ -269,14 +287,26 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const cpx<T>* 
     for (int r = 0; r < R; ++r) v[b + r * NB] = u[r];
     if constexpr (!LAST) {
       const int idxD = (jp / Ns) * Ns * R + (jp % Ns);
+      if constexpr (FAST) {
+        cpx<T>* wb = buf + pad16(idxD);
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[ex.idx(idxD + r * Ns)] = u[r];
+        for (int r = 0; r < R; ++r) wb[r * WSTEP] = u[r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[ex.idx(idxD + r * Ns)] = u[r];
+      }
     }
   }
   if constexpr (!LAST) {
     __syncthreads();
+    if constexpr (FAST) {
+      const cpx<T>* rb = buf + pad16(j);
 #pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = buf[ex.idx(j + TL * e)];
+      for (int e = 0; e < 16; ++e) v[e] = rb[e * RSTEP];
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = buf[ex.idx(j + TL * e)];
+    }
     if constexpr (!E::kDouble) __syncthreads();
   }
 }
@@ -533,6 +563,10 @@ struct PipeCfg {
   static constexpr int SWZ_STEP = (G >= 16) ? 1 : 16 / G;   // per-line swizzle offset
   static constexpr int NBUF = 3;                            // 2 staging + 1 exchange
   static constexpr int IL = 2;   // interleave of the intermediate layout (see below)
+  // padded line stride of the exchange layout (index i + i/16): LS = 16/G (mod 16) so
+  // the G lines read together by the transposed store hit distinct banks
+  static constexpr int LS = N + N / 16 + ((G >= 16) ? 1 : 16 / G);
+  static constexpr int BUF_ELEMS = ((G * LS + 15) / 16) * 16;   // >= G*N (TMA staging)
   static_assert(G % IL == 0, "pipe kernels need an even number of lines per group");
 };
 // Intermediate layout between pipe passes ("pair-interleaved transposed"): element mu of
@@ -548,16 +582,21 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
   using Cfg = PipeCfg<LOG2N>;
   constexpr int N = Cfg::N, TL = Cfg::TL, G = Cfg::G, THREADS = Cfg::THREADS;
   constexpr int GE = Cfg::GROUP_ELEMS;
+  constexpr int BE = Cfg::BUF_ELEMS, LS = Cfg::LS;
   constexpr uint32_t GROUP_BYTES = GE * sizeof(cpx<T>);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   cpx<T>* stage = reinterpret_cast<cpx<T>*>(smem_raw);                       // buffers 0, 1
-  cpx<T>* xbuf = stage + 2 * GE;                                            // buffer 2
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 3 * GROUP_BYTES);  // 2 mbarriers
+  cpx<T>* xbuf = stage + 2 * BE;                                            // buffer 2
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 3 * BE * sizeof(cpx<T>));  // 2 mbarriers
   long long* s_next = reinterpret_cast<long long*>(bar + 2);                // 2 slots
 
+  // Lines of a group are interleaved across lanes (line gl = tid % G): the lanes holding
+  // elements (i, i+1) of all G lines then form one contiguous G*IL-element segment of the
+  // pair-interleaved output, so the transposed store goes straight from registers, and
+  // the interleaved input is read without bank conflicts.
   const int tid = threadIdx.x;
-  const int j = tid % TL;
-  const int gl = tid / TL;
+  const int gl = tid % G;
+  const int j = tid / G;
   const cpx<T>* __restrict__ tw = reinterpret_cast<const cpx<T>*>(a.tw);
   const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in);
   cpx<T>* __restrict__ out = reinterpret_cast<cpx<T>*>(a.out);
@@ -572,7 +611,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     const long long g0 = (long long)atomicAdd(counter, 1ull);
     if (g0 < n_groups) {
       mbar_expect_tx(&bar[0], GROUP_BYTES);
-      bulk_g2s(stage, in + g0 * GE, GROUP_BYTES, &bar[0]);
+      bulk_g2s(stage, in + g0 * GE, GROUP_BYTES, &bar[0]);   // staging is contiguous
     }
     s_next[1] = g0;
   }
@@ -580,7 +619,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
   long long g = s_next[1];
   for (int k = 0; g < n_groups; ++k) {
     const int b = k & 1;
-    cpx<T>* sb = stage + b * GE;
+    cpx<T>* sb = stage + b * BE;
     mbar_wait(&bar[b], (uint32_t)((k >> 1) & 1));
 
     const long long line0 = g * G;
@@ -602,37 +641,26 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
       if (gn < n_groups) {
         fence_proxy_async_smem();      // order the generic-proxy uses of buffer b^1 before TMA
         mbar_expect_tx(&bar[b ^ 1], GROUP_BYTES);
-        bulk_g2s(stage + (b ^ 1) * GE, in + gn * GE, GROUP_BYTES, &bar[b ^ 1]);
+        bulk_g2s(stage + (b ^ 1) * BE, in + gn * GE, GROUP_BYTES, &bar[b ^ 1]);
       }
       s_next[b] = gn;
     }
 
-    const ExSwz<T> ex{sb + gl * N, xbuf + gl * N, gl * Cfg::SWZ_STEP};
+    const ExPad2<T> ex{sb + gl * LS, xbuf + gl * LS};
     pass_body<T, LOG2N, MODE>(v, j, tw, a.ph, (uint64_t)l, (T)a.scale, ex);
 
     if constexpr (MODE == 3) {
-      cpx<T>* dst = out + (line0 + gl) * N;
+      cpx<T>* dst = out + (line0 + gl) * N + j;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
+      for (int e = 0; e < 16; ++e) dst[TL * e] = v[e];
     } else {
-      constexpr int XT = PassInfo<LOG2N, MODE>::NX;   // exchange index of the store
-      cpx<T>* tb = (XT & 1) ? xbuf : sb;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) tb[gl * N + ex.idx(j + TL * e)] = v[e];
-      __syncthreads();
-      // pair-interleaved transposed store: segment ep holds elements e = IL*ep .. IL*ep+IL-1
-      // of this group's G lines: G*IL contiguous elements at ep*IL*N + l0*IL.
-      constexpr int SEG = G * Cfg::IL;
+      // pair-interleaved transposed store: element i = j + TL*e of line l0 + gl goes to
+      // (i / IL) * IL*N + (l0 + gl) * IL + i % IL of the output image.
       const int l0 = (int)(line0 % N);
-      cpx<T>* dst = out + (line0 / N) * (long long)N * N + (long long)l0 * Cfg::IL;
+      cpx<T>* dst = out + (line0 / N) * (long long)N * N + (long long)(j / Cfg::IL) * (Cfg::IL * N) +
+                    (l0 + gl) * Cfg::IL + (j % Cfg::IL);
 #pragma unroll
-      for (int kk = 0; kk < 16; ++kk) {
-        const int f = tid + kk * THREADS;
-        const int ep = f / SEG, sub = f % SEG;
-        const int ll = sub / Cfg::IL, e = ep * Cfg::IL + sub % Cfg::IL;
-        const int c = ll * Cfg::SWZ_STEP;
-        dst[(long long)ep * (Cfg::IL * N) + sub] = tb[ll * N + (e ^ (((e >> 4) + c) & 15))];
-      }
+      for (int e = 0; e < 16; ++e) dst[(long long)e * (TL / Cfg::IL) * (Cfg::IL * N)] = v[e];
     }
     g = s_next[b];   // written by thread 0 before at least one later barrier
   }

@@ -59,7 +59,7 @@ constexpr size_t kPipeExtra = 64;   // 2 mbarriers + 2 claimed-group slots
 template <typename T, int LOG2N, int MODE>
 cudaError_t launch_pipe(const PassArgs& a, cudaStream_t s, int grid, unsigned long long* counter) {
   using Cfg = nslct::PipeCfg<LOG2N>;
-  const size_t smem = (size_t)Cfg::NBUF * Cfg::GROUP_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
+  const size_t smem = (size_t)Cfg::NBUF * Cfg::BUF_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
   const long long n_groups = a.n_lines / Cfg::G;
   const long long g = n_groups < grid ? n_groups : grid;
   nslct::line_pass_pipe_kernel<T, LOG2N, MODE><<<(unsigned)g, Cfg::THREADS, smem, s>>>(a, n_groups, counter);
@@ -68,7 +68,7 @@ cudaError_t launch_pipe(const PassArgs& a, cudaStream_t s, int grid, unsigned lo
 template <typename T, int LOG2N, int MODE>
 cudaError_t set_attr_pipe() {
   using Cfg = nslct::PipeCfg<LOG2N>;
-  const size_t smem = (size_t)Cfg::NBUF * Cfg::GROUP_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
+  const size_t smem = (size_t)Cfg::NBUF * Cfg::BUF_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
   return cudaFuncSetAttribute(nslct::line_pass_pipe_kernel<T, LOG2N, MODE>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
