@@ -205,6 +205,43 @@ __device__ __forceinline__ void apply_twiddles(cpx<T>* u, cpx<T> w1) {
   }
 }
 
+// Per-thread twiddle bases of one line FFT: stage s >= 1, butterfly b uses
+// w = exp(-2 pi i k0/N) with k0 = (jp % Ns) * N/(Ns R), jp = j + b*TL.  They depend only
+// on the thread, not on the data, so a persistent kernel loads them once.
+template <int LOG2N>
+struct FftShape {
+  static constexpr int N = 1 << LOG2N;
+  static constexpr int TL = N / 16;
+  static constexpr int NFULL = LOG2N / 4;
+  static constexpr int NS = (LOG2N + 3) / 4;
+  template <int S>
+  __host__ __device__ static constexpr int R() { return (S < NFULL) ? 16 : (1 << (LOG2N % 4)); }
+  template <int S>
+  __host__ __device__ static constexpr int Ns() { return (S < NFULL) ? (1 << (4 * S)) : (1 << (4 * NFULL)); }
+};
+
+template <typename T, int LOG2N>
+struct TwSet {
+  using Sh = FftShape<LOG2N>;
+  static constexpr int NBMAX = 16 / Sh::template R<Sh::NS - 1>() > 1 ? 16 / Sh::template R<Sh::NS - 1>() : 1;
+  cpx<T> w[Sh::NS][NBMAX];
+  __device__ __forceinline__ void load(const cpx<T>* __restrict__ tw, int j) {
+    load_stage<1>(tw, j);
+  }
+  template <int S>
+  __device__ __forceinline__ void load_stage(const cpx<T>* __restrict__ tw, int j) {
+    if constexpr (S < Sh::NS) {
+      constexpr int R = Sh::template R<S>(), Ns = Sh::template Ns<S>(), NB = 16 / R;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int jp = j + b * Sh::TL;
+        w[S][b] = tw[(jp % Ns) * (Sh::N / (Ns * R))];
+      }
+      load_stage<S + 1>(tw, j);
+    }
+  }
+};
+
 // ---------------------------------------------------------------------------------
 // Line FFT of length N = 2^LOG2N, E = 16 elements per thread, TL = N/16 threads per line.
 // Register slot e of thread j holds element j + TL*e, before and after (Stockham
@@ -254,7 +291,7 @@ struct ExSwz {
 };
 
 template <typename T, int LOG2N, int STAGE, int NS, int X, class E>
-__device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const cpx<T>* __restrict__ tw,
+__device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TwSet<T, LOG2N>& tw,
                                           const E& ex) {
   constexpr int N = 1 << LOG2N;
   constexpr int TL = N / 16;
@@ -279,8 +316,7 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const cpx<T>* 
     if constexpr (Ns > 1) {
       // twiddles w^r, w = exp(-2 pi i k0/N): one (L1-resident) table load per butterfly,
       // powers by products of depth <= 5 (error a few ulp), instead of R-1 strided loads.
-      const int k0 = (jp % Ns) * (N / (Ns * R));
-      apply_twiddles<R>(u, tw[k0]);
+      apply_twiddles<R>(u, tw.w[STAGE][b]);
     }
     dft<R>(u);
 #pragma unroll
@@ -313,7 +349,7 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const cpx<T>* 
 
 template <typename T, int LOG2N, int STAGE, int NS, int X0, class E>
 struct FftStages {
-  __device__ __forceinline__ static void run(cpx<T> (&v)[16], int j, const cpx<T>* __restrict__ tw,
+  __device__ __forceinline__ static void run(cpx<T> (&v)[16], int j, const TwSet<T, LOG2N>& tw,
                                              const E& ex) {
     fft_stage<T, LOG2N, STAGE, NS, X0 + STAGE, E>(v, j, tw, ex);
     FftStages<T, LOG2N, STAGE + 1, NS, X0, E>::run(v, j, tw, ex);
@@ -321,7 +357,7 @@ struct FftStages {
 };
 template <typename T, int LOG2N, int NS, int X0, class E>
 struct FftStages<T, LOG2N, NS, NS, X0, E> {
-  __device__ __forceinline__ static void run(cpx<T> (&)[16], int, const cpx<T>* __restrict__, const E&) {}
+  __device__ __forceinline__ static void run(cpx<T> (&)[16], int, const TwSet<T, LOG2N>&, const E&) {}
 };
 
 template <int LOG2N>
@@ -332,7 +368,7 @@ struct FftInfo {
 
 // FFT of the thread's line; X0 = index of its first exchange within the pass.
 template <typename T, int LOG2N, int X0, class E>
-__device__ __forceinline__ void line_fft(cpx<T> (&v)[16], int j, const cpx<T>* __restrict__ tw,
+__device__ __forceinline__ void line_fft(cpx<T> (&v)[16], int j, const TwSet<T, LOG2N>& tw,
                                          const E& ex) {
   FftStages<T, LOG2N, 0, FftInfo<LOG2N>::NS, X0, E>::run(v, j, tw, ex);
 }
@@ -344,7 +380,7 @@ template <typename T>
 __device__ __forceinline__ cpx<T> chirp_of(uint64_t t, T scale);
 
 template <>
-__device__ __forceinline__ cpx<float> chirp_of<float>(uint64_t t, float scale) {
+__device__ __forceinline__ cpx<float> chirp_of<float>(uint64_t t, float scale) {   // scale==1 folds
   // top 32 bits as a signed fraction of a turn in [-1/2, 1/2) -> angle in [-pi, pi)
   const int32_t hi = (int32_t)(t >> 32);
   const float ang = (float)hi * 1.4629180792671596e-09f;  // 2 pi / 2^32
@@ -369,9 +405,22 @@ struct Phase {
 
 // Multiply the thread's 16 elements (e = j + TL*k) of line l by the chirp.
 // Exact second-difference recurrence in k:  t_k = a0 + d0 k + dd k(k-1)/2 ...
-template <typename T, int TL, bool CONJ_IN>
+template <typename T, int TL, bool CONJ_IN, bool SCALE>
 __device__ __forceinline__ void apply_chirp(cpx<T> (&v)[16], const Phase& ph, uint64_t l, uint64_t j,
-                                            T scale) {
+                                            T scale, bool sign_only) {
+  if (sign_only) {
+    // Q = 0: only the centring checkerboard (-1)^(l+e); e = j + TL k with TL even, so the
+    // sign is the same for all 16 elements of the thread.
+    T s = (((l + j) & 1) ? T(-1) : T(1));
+    if (SCALE) s *= scale;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      cpx<T> x = v[k];
+      if (CONJ_IN) x = cconj(x);
+      v[k] = {x.x * s, x.y * s};
+    }
+    return;
+  }
   // t(e) = alpha + gamma e + cC e^2, alpha = cA l^2 + cL l + cK, gamma = cB l + cE
   const uint64_t alpha = ph.cA * l * l + ph.cL * l + ph.cK;
   const uint64_t gamma = ph.cB * l + ph.cE;
@@ -381,7 +430,7 @@ __device__ __forceinline__ void apply_chirp(cpx<T> (&v)[16], const Phase& ph, ui
   uint64_t d = gamma * (uint64_t)TL + 2ull * ph.cC * j * (uint64_t)TL + ph.cC * (uint64_t)TL * (uint64_t)TL;
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
-    cpx<T> c = chirp_of<T>(t, scale);
+    cpx<T> c = chirp_of<T>(t, SCALE ? scale : T(1));
     cpx<T> x = v[k];
     if (CONJ_IN) x = cconj(x);
     v[k] = cmul(x, c);
@@ -405,6 +454,7 @@ struct PassArgs {
   long long n_lines;   // batch * N
   Phase ph;
   double scale;
+  int sign_only;       // the chirp is only the centring checkerboard (Q0/Q4 absent)
 };
 
 // The per-line work of one pass (registers v hold elements j + TL*e of line l).
@@ -415,12 +465,14 @@ struct PassInfo {
 };
 
 template <typename T, int LOG2N, int MODE, class E>
-__device__ __forceinline__ void pass_body(cpx<T> (&v)[16], int j, const cpx<T>* __restrict__ tw,
-                                          const Phase& ph0, uint64_t l, T scale, const E& ex) {
+__device__ __forceinline__ void pass_body(cpx<T> (&v)[16], int j, const TwSet<T, LOG2N>& tw,
+                                          const Phase& ph0, uint64_t l, T scale, bool sign_only,
+                                          const E& ex) {
+  // The inverse FFTs are left unnormalised; the whole 1/N^4 is applied in MODE 3 (K5).
   constexpr int TL = (1 << LOG2N) / 16;
   constexpr int NX = FftInfo<LOG2N>::NX;
   if constexpr (MODE == 0) {
-    apply_chirp<T, TL, false>(v, ph0, l, (uint64_t)j, scale);
+    apply_chirp<T, TL, false, false>(v, ph0, l, (uint64_t)j, scale, sign_only);
     line_fft<T, LOG2N, 0>(v, j, tw, ex);
   } else if constexpr (MODE == 1) {
     line_fft<T, LOG2N, 0>(v, j, tw, ex);
@@ -430,7 +482,7 @@ __device__ __forceinline__ void pass_body(cpx<T> (&v)[16], int j, const cpx<T>* 
     Phase ph = ph0;
     ph.cA = 0 - ph.cA; ph.cB = 0 - ph.cB; ph.cC = 0 - ph.cC;
     ph.cL = 0 - ph.cL; ph.cE = 0 - ph.cE; ph.cK = 0 - ph.cK;
-    apply_chirp<T, TL, false>(v, ph, l, (uint64_t)j, scale);
+    apply_chirp<T, TL, false, false>(v, ph, l, (uint64_t)j, scale, false);
     line_fft<T, LOG2N, NX>(v, j, tw, ex);
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
@@ -438,13 +490,13 @@ __device__ __forceinline__ void pass_body(cpx<T> (&v)[16], int j, const cpx<T>* 
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
     line_fft<T, LOG2N, 0>(v, j, tw, ex);
-    apply_chirp<T, TL, true>(v, ph0, l, (uint64_t)j, scale);
+    apply_chirp<T, TL, true, false>(v, ph0, l, (uint64_t)j, scale, false);
     line_fft<T, LOG2N, NX>(v, j, tw, ex);
   } else {
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
     line_fft<T, LOG2N, 0>(v, j, tw, ex);
-    apply_chirp<T, TL, true>(v, ph0, l, (uint64_t)j, scale);
+    apply_chirp<T, TL, true, true>(v, ph0, l, (uint64_t)j, scale, sign_only);
   }
 }
 
@@ -483,7 +535,9 @@ line_pass_kernel(PassArgs a) {
 #pragma unroll
   for (int e = 0; e < 16; ++e) v[e] = src[j + TL * e];
 
-  pass_body<T, LOG2N, MODE>(v, j, tw, a.ph, (uint64_t)l, (T)a.scale, ExPad<T>{buf});
+  TwSet<T, LOG2N> tws;
+  tws.load(tw, j);
+  pass_body<T, LOG2N, MODE>(v, j, tws, a.ph, (uint64_t)l, (T)a.scale, a.sign_only != 0, ExPad<T>{buf});
 
   if constexpr (MODE == 3) {
     cpx<T>* dst = reinterpret_cast<cpx<T>*>(a.out) + line * N;
@@ -576,6 +630,22 @@ struct PipeCfg {
 // producer holding G lines writes G*IL-element contiguous segments (>= 32 B: full L2
 // sectors; 16-byte half-sector writes measured ~5x slower, tools/micro_bench.cu).
 
+// One group into a staging buffer.  MODE 0 reads the user's row-major lines and lands
+// line ll at ll*LS (LS = 16/G mod 16: the lanes of the G lines hit different banks);
+// other modes read one contiguous pair-interleaved block.
+template <typename T, int LOG2N, int MODE>
+__device__ __forceinline__ void load_group(cpx<T>* dst, const cpx<T>* src, uint64_t* bar) {
+  using Cfg = PipeCfg<LOG2N>;
+  constexpr uint32_t LINE_BYTES = Cfg::N * sizeof(cpx<T>);
+  mbar_expect_tx(bar, Cfg::G * LINE_BYTES);
+  if constexpr (MODE == 0) {
+#pragma unroll
+    for (int ll = 0; ll < Cfg::G; ++ll) bulk_g2s(dst + ll * Cfg::LS, src + ll * Cfg::N, LINE_BYTES, bar);
+  } else {
+    bulk_g2s(dst, src, Cfg::G * LINE_BYTES, bar);
+  }
+}
+
 template <typename T, int LOG2N, int MODE>
 __global__ void __launch_bounds__(512, 1)
 line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counter) {
@@ -601,6 +671,9 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
   const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in);
   cpx<T>* __restrict__ out = reinterpret_cast<cpx<T>*>(a.out);
 
+  TwSet<T, LOG2N> tws;   // this thread's twiddle bases, the same for every group
+  tws.load(tw, j);
+
   // Groups are claimed in order from a global counter (not round-robin) so the groups
   // in flight across the GPU stay a contiguous window: the 8*G-byte pieces of the
   // transposed stores of neighbouring groups then meet in L2 and leave as full lines.
@@ -609,10 +682,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     mbar_init(&bar[1], 1);
     fence_mbar_init();
     const long long g0 = (long long)atomicAdd(counter, 1ull);
-    if (g0 < n_groups) {
-      mbar_expect_tx(&bar[0], GROUP_BYTES);
-      bulk_g2s(stage, in + g0 * GE, GROUP_BYTES, &bar[0]);   // staging is contiguous
-    }
+    if (g0 < n_groups) load_group<T, LOG2N, MODE>(stage, in + g0 * GE, &bar[0]);
     s_next[1] = g0;
   }
   __syncthreads();
@@ -625,9 +695,9 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     const long long line0 = g * G;
     const int l = (int)((line0 + gl) % N);
     cpx<T> v[16];
-    if constexpr (MODE == 0) {   // the user's row-major input: lines are contiguous
+    if constexpr (MODE == 0) {   // the user's row-major input, lines staged LS apart
 #pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = sb[gl * N + j + TL * e];
+      for (int e = 0; e < 16; ++e) v[e] = sb[gl * LS + j + TL * e];
     } else {                     // pair-interleaved intermediate
       const cpx<T>* src = sb + (gl / Cfg::IL) * (Cfg::IL * N) + (gl % Cfg::IL);
 #pragma unroll
@@ -640,14 +710,13 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
       const long long gn = (long long)atomicAdd(counter, 1ull);
       if (gn < n_groups) {
         fence_proxy_async_smem();      // order the generic-proxy uses of buffer b^1 before TMA
-        mbar_expect_tx(&bar[b ^ 1], GROUP_BYTES);
-        bulk_g2s(stage + (b ^ 1) * BE, in + gn * GE, GROUP_BYTES, &bar[b ^ 1]);
+        load_group<T, LOG2N, MODE>(stage + (b ^ 1) * BE, in + gn * GE, &bar[b ^ 1]);
       }
       s_next[b] = gn;
     }
 
     const ExPad2<T> ex{sb + gl * LS, xbuf + gl * LS};
-    pass_body<T, LOG2N, MODE>(v, j, tw, a.ph, (uint64_t)l, (T)a.scale, ex);
+    pass_body<T, LOG2N, MODE>(v, j, tws, a.ph, (uint64_t)l, (T)a.scale, a.sign_only != 0, ex);
 
     if constexpr (MODE == 3) {
       cpx<T>* dst = out + (line0 + gl) * N + j;

@@ -391,12 +391,15 @@ nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16],
     Poly P4 = chirp_poly(p.q_active[4] ? p.Q[4] : zero, dx, (int)n, true);
     const Phase ph[5] = {to_phase(P0, true), to_phase(P1, false), to_phase(P2, true),
                          to_phase(P3, false), to_phase(P4, true)};
-    const double sc[5] = {1.0, invn, invn, invn, invn};
+    // inverse FFTs are unnormalised; K5 applies 1/N^4 (two 2D inverses) at once
+    const double sc[5] = {1.0, 1.0, 1.0, 1.0, invn * invn * invn * invn};
+    const int sign_only[5] = {p.q_active[0] ? 0 : 1, 0, 0, 0, p.q_active[4] ? 0 : 1};
     for (int k = 0; k < 5; ++k) {
       pl->args[k].tw = pl->tw;
       pl->args[k].n_lines = batch * n;
       pl->args[k].ph = ph[k];
       pl->args[k].scale = sc[k];
+      pl->args[k].sign_only = sign_only[k];
     }
     {
       int sms = 0;
