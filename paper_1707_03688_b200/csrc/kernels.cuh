@@ -265,18 +265,25 @@ struct ExPad {
   static constexpr bool kPadded = true;
   cpx<T>* buf;
   template <int X>
+  __device__ __forceinline__ void after_barrier() const {}
+  template <int X>
   __device__ __forceinline__ cpx<T>* b() const { return buf; }
   __device__ __forceinline__ int idx(int i) const { return pad16(i); }
 };
-template <typename T>
+template <typename T, class Hook>
 struct ExPad2 {   // two padded buffers used alternately: write, barrier, read
   static constexpr bool kDouble = true;
   static constexpr bool kPadded = true;
-  cpx<T>* buf0;
-  cpx<T>* buf1;
+  cpx<T>* buf0;   // used by exchanges 0, 2, 4, ...
+  cpx<T>* buf1;   // used by exchanges 1, 3, ...
+  const Hook* hook;
   template <int X>
   __device__ __forceinline__ cpx<T>* b() const { return (X & 1) ? buf1 : buf0; }
   __device__ __forceinline__ int idx(int i) const { return pad16(i); }
+  template <int X>
+  __device__ __forceinline__ void after_barrier() const {
+    if constexpr (X == 0) hook->run();
+  }
 };
 template <typename T>
 struct ExSwz {
@@ -285,6 +292,8 @@ struct ExSwz {
   cpx<T>* buf0;
   cpx<T>* buf1;
   int c;
+  template <int X>
+  __device__ __forceinline__ void after_barrier() const {}
   template <int X>
   __device__ __forceinline__ cpx<T>* b() const { return (X & 1) ? buf1 : buf0; }
   __device__ __forceinline__ int idx(int i) const { return i ^ (((i >> 4) + c) & 15); }
@@ -335,6 +344,7 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TwSet<T,
   }
   if constexpr (!LAST) {
     __syncthreads();
+    ex.template after_barrier<X>();
     if constexpr (FAST) {
       const cpx<T>* rb = buf + pad16(j);
 #pragma unroll
@@ -703,19 +713,31 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = src[(j + TL * e) * Cfg::IL];
     }
-    // Everyone has its inputs, and everyone has finished iteration k-1: buffer b^1 (used
-    // by iteration k-1) may now be refilled and buffer b becomes exchange space.
-    __syncthreads();
-    if (tid == 0) {   // claim and prefetch the next group
-      const long long gn = (long long)atomicAdd(counter, 1ull);
-      if (gn < n_groups) {
-        fence_proxy_async_smem();      // order the generic-proxy uses of buffer b^1 before TMA
-        load_group<T, LOG2N, MODE>(stage + (b ^ 1) * BE, in + gn * GE, &bar[b ^ 1]);
+    // No barrier here: exchange 0 writes the spare buffer, so the staging buffer sb is
+    // only overwritten (exchange 1) after exchange 0's barrier, which every thread
+    // reaches after reading its inputs.  That same barrier also proves iteration k-1 is
+    // finished everywhere, so the hook run right after it may refill buffer b^1.
+    struct Prefetch {
+      int tid, b;
+      unsigned long long* counter;
+      long long n_groups;
+      cpx<T>* next_buf;
+      const cpx<T>* in;
+      uint64_t* bar;
+      long long* s_next;
+      __device__ __forceinline__ void run() const {
+        if (tid == 0) {   // claim and prefetch the next group
+          const long long gn = (long long)atomicAdd(counter, 1ull);
+          if (gn < n_groups) {
+            fence_proxy_async_smem();    // order the generic-proxy uses of the buffer before TMA
+            load_group<T, LOG2N, MODE>(next_buf, in + gn * GE, &bar[b ^ 1]);
+          }
+          s_next[b] = gn;
+        }
       }
-      s_next[b] = gn;
-    }
-
-    const ExPad2<T> ex{sb + gl * LS, xbuf + gl * LS};
+    };
+    const Prefetch pf{tid, b, counter, n_groups, stage + (b ^ 1) * BE, in, bar, s_next};
+    const ExPad2<T, Prefetch> ex{xbuf + gl * LS, sb + gl * LS, &pf};
     pass_body<T, LOG2N, MODE>(v, j, tws, a.ph, (uint64_t)l, (T)a.scale, a.sign_only != 0, ex);
 
     if constexpr (MODE == 3) {
