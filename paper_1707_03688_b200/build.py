@@ -15,6 +15,7 @@ SOURCES = [os.path.join(CSRC, f) for f in ("nslct.cu", "planner.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "planner.h")] + \
     [os.path.join(ROOT, "include", "nslct.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+EXTRA = os.environ.get("NSLCT_NVCC_EXTRA", "").split()
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC,-O3", "-shared", "-Xptxas", "-v", "--threads", "0"]
 
@@ -29,7 +30,7 @@ def up_to_date():
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB
-    cmd = [NVCC] + FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp"] + SOURCES
+    cmd = [NVCC] + FLAGS + EXTRA + ["-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp"] + SOURCES
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:

@@ -55,6 +55,95 @@ template <typename T>
 __device__ __forceinline__ cpx<T> mul_mj(cpx<T> a) {
   return {a.y, -a.x};
 }
+// real scale
+template <typename T>
+__device__ __forceinline__ cpx<T> cscale(cpx<T> a, T s) {
+  return {a.x * s, a.y * s};
+}
+// a * (c - j s) = (c x + s y, c y - s x)
+template <typename T>
+__device__ __forceinline__ cpx<T> crot(cpx<T> a, T c, T s) {
+  return {c * a.x + s * a.y, c * a.y - s * a.x};
+}
+// r * (x + y, y - x): multiplication by r (1 - j)
+template <typename T>
+__device__ __forceinline__ cpx<T> cmul_1mj(cpx<T> a, T r) {
+  return {r * (a.x + a.y), r * (a.y - a.x)};
+}
+// r * (x - y, x + y): multiplication by r (1 + j)
+template <typename T>
+__device__ __forceinline__ cpx<T> cmul_1pj(cpx<T> a, T r) {
+  return {r * (a.x - a.y), r * (a.x + a.y)};
+}
+
+// ---- complex64 on sm_100a: packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2) --------
+// One packed instruction does both halves of a complex add; a complex multiply is
+// FMUL2 + FFMA2.  ptxas folds the lane swaps / broadcasts / single-lane negations of
+// the packing moves into operand selectors, so these helpers cost no extra moves.
+// (Packed ops halve issue slots, not FP-pipe cycles: tools/micro_fp.cu.)
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk2(float x, float y) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ cpx<float> up2(u64 v) {
+  cpx<float> r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+#ifdef NSLCT_PACKED_FP32   // opt-in: measured ~4% slower than scalar in the 512-thread pass
+template <>
+__device__ __forceinline__ cpx<float> cadd<float>(cpx<float> a, cpx<float> b) {
+  return up2(add2(pk2(a.x, a.y), pk2(b.x, b.y)));
+}
+template <>
+__device__ __forceinline__ cpx<float> csub<float>(cpx<float> a, cpx<float> b) {
+  return up2(sub2(pk2(a.x, a.y), pk2(b.x, b.y)));
+}
+template <>
+__device__ __forceinline__ cpx<float> cmul<float>(cpx<float> a, cpx<float> b) {
+  // (ax bx, ay bx) + (-ay, ax) * by
+  return up2(fma2(pk2(-a.y, a.x), pk2(b.y, b.y), mul2(pk2(a.x, a.y), pk2(b.x, b.x))));
+}
+template <>
+__device__ __forceinline__ cpx<float> cscale<float>(cpx<float> a, float s) {
+  return up2(mul2(pk2(a.x, a.y), pk2(s, s)));
+}
+template <>
+__device__ __forceinline__ cpx<float> crot<float>(cpx<float> a, float c, float s) {
+  // (x, y) c + (y, -x) s
+  return up2(fma2(pk2(a.x, a.y), pk2(c, c), mul2(pk2(a.y, -a.x), pk2(s, s))));
+}
+template <>
+__device__ __forceinline__ cpx<float> cmul_1mj<float>(cpx<float> a, float r) {
+  return up2(mul2(add2(pk2(a.x, a.y), pk2(a.y, -a.x)), pk2(r, r)));
+}
+template <>
+__device__ __forceinline__ cpx<float> cmul_1pj<float>(cpx<float> a, float r) {
+  return up2(mul2(add2(pk2(a.x, a.y), pk2(-a.y, a.x)), pk2(r, r)));
+}
+#endif  // NSLCT_PACKED_FP32
 
 // ---------------------------------------------------------------------------------
 // Small DFTs in registers (forward, e^{-2 pi i n k / R}), natural order in and out.
@@ -75,20 +164,20 @@ __device__ __forceinline__ cpx<T> w16(cpx<T> a) {
   } else if constexpr (q == 12) {
     return {-a.y, a.x};
   } else if constexpr (q == 2) {  // (1 - j)/sqrt2
-    return {T(R2) * (a.x + a.y), T(R2) * (a.y - a.x)};
-  } else if constexpr (q == 6) {  // (-1 - j)/sqrt2
-    return {T(R2) * (a.y - a.x), T(-R2) * (a.x + a.y)};
-  } else if constexpr (q == 10) {  // (-1 + j)/sqrt2
-    return {T(-R2) * (a.x + a.y), T(R2) * (a.x - a.y)};
+    return cmul_1mj(a, T(R2));
+  } else if constexpr (q == 6) {  // (-1 - j)/sqrt2 = -(1 + j)/sqrt2
+    return cmul_1pj(a, T(-R2));
+  } else if constexpr (q == 10) {  // (-1 + j)/sqrt2 = -(1 - j)/sqrt2
+    return cmul_1mj(a, T(-R2));
   } else if constexpr (q == 14) {  // (1 + j)/sqrt2
-    return {T(R2) * (a.x - a.y), T(R2) * (a.x + a.y)};
+    return cmul_1pj(a, T(R2));
   } else {
     // generic: cos(2 pi q/16) - j sin(2 pi q/16)
     constexpr double c = (q == 1 || q == 15) ? C1 : (q == 3 || q == 13) ? S1
                          : (q == 5 || q == 11) ? -S1 : -C1;  // q = 7, 9
     constexpr double s = (q == 1 || q == 7) ? S1 : (q == 3 || q == 5) ? C1
                          : (q == 9 || q == 15) ? -S1 : -C1;  // q = 11, 13
-    return {T(c) * a.x + T(s) * a.y, T(c) * a.y - T(s) * a.x};
+    return crot(a, T(c), T(s));
   }
 }
 
@@ -228,6 +317,10 @@ struct TwSet {
   __device__ __forceinline__ void load(const cpx<T>* __restrict__ tw, int j) {
     load_stage<1>(tw, j);
   }
+  template <int S, int R>
+  __device__ __forceinline__ void apply(cpx<T>* u, int b, int /*jp*/) const {
+    apply_twiddles<R>(u, w[S][b]);
+  }
   template <int S>
   __device__ __forceinline__ void load_stage(const cpx<T>* __restrict__ tw, int j) {
     if constexpr (S < Sh::NS) {
@@ -249,6 +342,48 @@ struct TwSet {
 // buf: this line's shared-memory buffer, padded index P(i) = i + (i >> 4).
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+
+// Twiddle powers from shared-memory tables: stage S (>= 1) holds, for every residue
+// m = jp % Ns and r = 1..R-1, exp(-2 pi i m r / (Ns R)) at [S-offset + (r-1) Ns + m]
+// (the entries come from the fp64-accurate global table, so they are exact to rounding).
+// Consecutive lanes read consecutive m: conflict-free.  Used by the persistent kernels,
+// which fill the tables once; it saves the 14 power-generation products per butterfly.
+template <typename T, int LOG2N>
+struct TwTab {
+  using Sh = FftShape<LOG2N>;
+  template <int S>
+  __host__ __device__ static constexpr int off() {
+    if constexpr (S <= 1) {
+      return 0;
+    } else {
+      return off<S - 1>() + Sh::template Ns<S - 1>() * (Sh::template R<S - 1>() - 1);
+    }
+  }
+  __host__ __device__ static constexpr int elems() { return off<Sh::NS>(); }
+  const cpx<T>* tab;
+  template <int S, int R>
+  __device__ __forceinline__ void apply(cpx<T>* u, int /*b*/, int jp) const {
+    constexpr int Ns = Sh::template Ns<S>();
+    const cpx<T>* t = tab + off<S>() + (jp % Ns);
+#pragma unroll
+    for (int r = 1; r < R; ++r) u[r] = cmul(u[r], t[(r - 1) * Ns]);
+  }
+  // all threads of the CTA: tab[...] = tw[m * r * N/(Ns R)]
+  __device__ static void fill(cpx<T>* tab, const cpx<T>* __restrict__ tw, int tid, int nthreads) {
+    fill_stage<1>(tab, tw, tid, nthreads);
+  }
+  template <int S>
+  __device__ static void fill_stage(cpx<T>* tab, const cpx<T>* __restrict__ tw, int tid, int nthreads) {
+    if constexpr (S < Sh::NS) {
+      constexpr int Ns = Sh::template Ns<S>(), R = Sh::template R<S>();
+      for (int i = tid; i < Ns * (R - 1); i += nthreads) {
+        const int r = i / Ns + 1, m = i % Ns;
+        tab[off<S>() + i] = tw[m * r * (Sh::N / (Ns * R))];
+      }
+      fill_stage<S + 1>(tab, tw, tid, nthreads);
+    }
+  }
+};
 
 // Exchange policies (how a stage hands its outputs to the next stage through shared
 // memory).  X is the compile-time index of the exchange within the pass.
@@ -285,23 +420,25 @@ struct ExPad2 {   // two padded buffers used alternately: write, barrier, read
     if constexpr (X == 0) hook->run();
   }
 };
-template <typename T>
-struct ExSwz {
+template <typename T, class Hook>
+struct ExSwz {   // two unpadded XOR-swizzled buffers used alternately (see above)
   static constexpr bool kDouble = true;
   static constexpr bool kPadded = false;
-  cpx<T>* buf0;
-  cpx<T>* buf1;
-  int c;
-  template <int X>
-  __device__ __forceinline__ void after_barrier() const {}
+  cpx<T>* buf0;   // exchanges 0, 2, ...
+  cpx<T>* buf1;   // exchanges 1, 3, ...
+  int c;          // per-line swizzle constant
+  const Hook* hook;
   template <int X>
   __device__ __forceinline__ cpx<T>* b() const { return (X & 1) ? buf1 : buf0; }
   __device__ __forceinline__ int idx(int i) const { return i ^ (((i >> 4) + c) & 15); }
+  template <int X>
+  __device__ __forceinline__ void after_barrier() const {
+    if constexpr (X == 0) hook->run();
+  }
 };
 
-template <typename T, int LOG2N, int STAGE, int NS, int X, class E>
-__device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TwSet<T, LOG2N>& tw,
-                                          const E& ex) {
+template <typename T, int LOG2N, int STAGE, int NS, int X, class E, class TW>
+__device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TW& tw, const E& ex) {
   constexpr int N = 1 << LOG2N;
   constexpr int TL = N / 16;
   constexpr int NFULL = LOG2N / 4;
@@ -314,6 +451,7 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TwSet<T,
   // or i is a multiple of 16 and k < 16 -- so one base per butterfly/thread plus
   // compile-time offsets (the compiler cannot prove j < TL by itself).
   constexpr bool FAST = E::kPadded && (TL % 16 == 0);
+  constexpr bool FAST_SWZ = !E::kPadded && (TL % 16 == 0);
   constexpr int WSTEP = (Ns >= 16) ? Ns + Ns / 16 : Ns;
   constexpr int RSTEP = TL + TL / 16;
 #pragma unroll
@@ -322,11 +460,7 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TwSet<T,
     cpx<T> u[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) u[r] = v[b + r * NB];
-    if constexpr (Ns > 1) {
-      // twiddles w^r, w = exp(-2 pi i k0/N): one (L1-resident) table load per butterfly,
-      // powers by products of depth <= 5 (error a few ulp), instead of R-1 strided loads.
-      apply_twiddles<R>(u, tw.w[STAGE][b]);
-    }
+    if constexpr (Ns > 1) tw.template apply<STAGE, R>(u, b, jp);
     dft<R>(u);
 #pragma unroll
     for (int r = 0; r < R; ++r) v[b + r * NB] = u[r];
@@ -336,6 +470,20 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TwSet<T,
         cpx<T>* wb = buf + pad16(idxD);
 #pragma unroll
         for (int r = 0; r < R; ++r) wb[r * WSTEP] = u[r];
+      } else if constexpr (FAST_SWZ) {
+        // element idxD + r*Ns; its 16-group index is (idxD >> 4) + r*Ns/16 (Ns >= 16) or
+        // idxD >> 4 (Ns == 1, r < 16); the low 4 bits are (jp & 15) or r.
+        if constexpr (Ns == 1) {
+          cpx<T>* wb = buf + idxD;
+          const int x = ((idxD >> 4) + ex.c) & 15;
+#pragma unroll
+          for (int r = 0; r < R; ++r) wb[r ^ x] = u[r];
+        } else {
+          cpx<T>* wb = buf + (idxD & ~15);
+          const int y = (idxD >> 4) + ex.c, lo = jp & 15;
+#pragma unroll
+          for (int r = 0; r < R; ++r) wb[r * Ns + (lo ^ ((y + r * (Ns / 16)) & 15))] = u[r];
+        }
       } else {
 #pragma unroll
         for (int r = 0; r < R; ++r) buf[ex.idx(idxD + r * Ns)] = u[r];
@@ -349,6 +497,11 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TwSet<T,
       const cpx<T>* rb = buf + pad16(j);
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = rb[e * RSTEP];
+    } else if constexpr (FAST_SWZ) {
+      // element j + TL e (j < TL): group (j >> 4) + (TL/16) e, low bits j & 15
+      const int y = (j >> 4) + ex.c, lo = j & 15;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = buf[TL * e + (j & ~15) + (lo ^ ((y + (TL / 16) * e) & 15))];
     } else {
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = buf[ex.idx(j + TL * e)];
@@ -357,17 +510,16 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TwSet<T,
   }
 }
 
-template <typename T, int LOG2N, int STAGE, int NS, int X0, class E>
+template <typename T, int LOG2N, int STAGE, int NS, int X0, class E, class TW>
 struct FftStages {
-  __device__ __forceinline__ static void run(cpx<T> (&v)[16], int j, const TwSet<T, LOG2N>& tw,
-                                             const E& ex) {
-    fft_stage<T, LOG2N, STAGE, NS, X0 + STAGE, E>(v, j, tw, ex);
-    FftStages<T, LOG2N, STAGE + 1, NS, X0, E>::run(v, j, tw, ex);
+  __device__ __forceinline__ static void run(cpx<T> (&v)[16], int j, const TW& tw, const E& ex) {
+    fft_stage<T, LOG2N, STAGE, NS, X0 + STAGE, E, TW>(v, j, tw, ex);
+    FftStages<T, LOG2N, STAGE + 1, NS, X0, E, TW>::run(v, j, tw, ex);
   }
 };
-template <typename T, int LOG2N, int NS, int X0, class E>
-struct FftStages<T, LOG2N, NS, NS, X0, E> {
-  __device__ __forceinline__ static void run(cpx<T> (&)[16], int, const TwSet<T, LOG2N>&, const E&) {}
+template <typename T, int LOG2N, int NS, int X0, class E, class TW>
+struct FftStages<T, LOG2N, NS, NS, X0, E, TW> {
+  __device__ __forceinline__ static void run(cpx<T> (&)[16], int, const TW&, const E&) {}
 };
 
 template <int LOG2N>
@@ -377,10 +529,9 @@ struct FftInfo {
 };
 
 // FFT of the thread's line; X0 = index of its first exchange within the pass.
-template <typename T, int LOG2N, int X0, class E>
-__device__ __forceinline__ void line_fft(cpx<T> (&v)[16], int j, const TwSet<T, LOG2N>& tw,
-                                         const E& ex) {
-  FftStages<T, LOG2N, 0, FftInfo<LOG2N>::NS, X0, E>::run(v, j, tw, ex);
+template <typename T, int LOG2N, int X0, class E, class TW>
+__device__ __forceinline__ void line_fft(cpx<T> (&v)[16], int j, const TW& tw, const E& ex) {
+  FftStages<T, LOG2N, 0, FftInfo<LOG2N>::NS, X0, E, TW>::run(v, j, tw, ex);
 }
 
 // ---------------------------------------------------------------------------------
@@ -427,7 +578,7 @@ __device__ __forceinline__ void apply_chirp(cpx<T> (&v)[16], const Phase& ph, ui
     for (int k = 0; k < 16; ++k) {
       cpx<T> x = v[k];
       if (CONJ_IN) x = cconj(x);
-      v[k] = {x.x * s, x.y * s};
+      v[k] = cscale(x, s);
     }
     return;
   }
@@ -474,8 +625,8 @@ struct PassInfo {
   static constexpr int NX = FftInfo<LOG2N>::NX * ((MODE == 1 || MODE == 2) ? 2 : 1);
 };
 
-template <typename T, int LOG2N, int MODE, class E>
-__device__ __forceinline__ void pass_body(cpx<T> (&v)[16], int j, const TwSet<T, LOG2N>& tw,
+template <typename T, int LOG2N, int MODE, class E, class TW>
+__device__ __forceinline__ void pass_body(cpx<T> (&v)[16], int j, const TW& tw,
                                           const Phase& ph0, uint64_t l, T scale, bool sign_only,
                                           const E& ex) {
   // The inverse FFTs are left unnormalised; the whole 1/N^4 is applied in MODE 3 (K5).
@@ -754,6 +905,272 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
       for (int e = 0; e < 16; ++e) dst[(long long)e * (TL / Cfg::IL) * (Cfg::IL * N)] = v[e];
     }
     g = s_next[b];   // written by thread 0 before at least one later barrier
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Line-pair kernel (c64, N = 4096): the MIO-lean variant of the persistent pass.
+//
+// Shared-memory instructions issue at ~1 per 2 clocks per SM whatever their width
+// (tools/micro_smem.cu), so the exchanges are done with 128-bit accesses: thread j of a
+// 256-thread CTA holds element j + TL*e (e = 0..15) of BOTH lines of a 2-line group, and
+// the exchange buffer interleaves the two lines ([i][line], 16 B per index, XOR-swizzled
+// in 16-byte units).  Both lines share the thread's twiddles, which are precomputed once
+// per kernel into registers (2 stages x 15 powers).  The pair-interleaved transposed
+// store needs (line, i), (line, i+1) in one lane: one shuffle between lanes j and j^1
+// builds them, and every lane writes a 16-byte piece of a full 32-byte segment.
+// ---------------------------------------------------------------------------------
+template <int LOG2N>
+struct PairCfg {
+  static constexpr int N = 1 << LOG2N;
+  static constexpr int TL = N / 16;
+  static constexpr int THREADS = TL;          // one thread per element slot; both lines
+  static constexpr int G = 2;
+  static constexpr int GE = G * N;            // elements per group
+  static constexpr int BE = GE + 16;          // elements per buffer
+  static constexpr int NBUF = 3;              // 2 staging + 1 exchange
+  static constexpr int IL = 2;                // pair-interleaved intermediate layout
+  static constexpr int NS = (LOG2N + 3) / 4;  // stages
+  static constexpr int NX = NS - 1;           // exchanges per FFT
+  static_assert(LOG2N % 4 == 0 && TL >= 128 && TL <= 512, "pair kernel: radix-16 stages only");
+};
+
+struct __align__(16) cpx2f {
+  cpx<float> a, b;   // line 0, line 1
+};
+
+__device__ __forceinline__ void st_pair(cpx<float>* base_pairs, int unit, cpx<float> a, cpx<float> b) {
+  float4 v = make_float4(a.x, a.y, b.x, b.y);
+  reinterpret_cast<float4*>(base_pairs)[unit] = v;
+}
+__device__ __forceinline__ void ld_pair(const cpx<float>* base_pairs, int unit, cpx<float>& a, cpx<float>& b) {
+  const float4 v = reinterpret_cast<const float4*>(base_pairs)[unit];
+  a = {v.x, v.y};
+  b = {v.z, v.w};
+}
+
+template <int LOG2N>
+struct PairTw {   // w[s][r] = exp(-2 pi i k0_s r / N), k0_s = (j % Ns) N/(Ns 16), s = 1..NS-1
+  using C = PairCfg<LOG2N>;
+  cpx<float> w[C::NS][16];
+  __device__ __forceinline__ void load(const cpx<float>* __restrict__ tw, int j) {
+#pragma unroll
+    for (int s = 1; s < C::NS; ++s) {
+      const int Ns = 1 << (4 * s);
+      const int k0 = (j % Ns) * (C::N / (Ns * 16));
+#pragma unroll
+      for (int r = 1; r < 16; ++r) w[s][r] = tw[k0 * r];
+    }
+  }
+};
+
+template <int LOG2N, int STAGE, int X, class Hook>
+__device__ __forceinline__ void pair_stage(cpx<float> (&v0)[16], cpx<float> (&v1)[16], int j,
+                                           const PairTw<LOG2N>& tw, cpx<float>* xb0, cpx<float>* xb1,
+                                           const Hook& hook) {
+  using C = PairCfg<LOG2N>;
+  constexpr int TL = C::TL;
+  constexpr int Ns = 1 << (4 * STAGE);
+  constexpr bool LAST = (STAGE == C::NS - 1);
+  if constexpr (STAGE > 0) {
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+      v0[r] = cmul(v0[r], tw.w[STAGE][r]);
+      v1[r] = cmul(v1[r], tw.w[STAGE][r]);
+    }
+  }
+  dft<16>(v0);
+  dft<16>(v1);
+  if constexpr (!LAST) {
+    cpx<float>* buf = (X & 1) ? xb1 : xb0;
+    // unit (16 B) index of element i: i ^ ((i >> 4) & 15)
+    const int idxD = (j / Ns) * Ns * 16 + (j % Ns);
+    if constexpr (Ns == 1) {
+      const int x = (idxD >> 4) & 15;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) st_pair(buf, idxD + (r ^ x), v0[r], v1[r]);
+    } else {
+      const int y = idxD >> 4, lo = j & 15, hi = idxD & ~15;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) st_pair(buf, hi + r * Ns + (lo ^ ((y + r * (Ns / 16)) & 15)), v0[r], v1[r]);
+    }
+    __syncthreads();
+    if constexpr (X == 0) hook.run();
+    const int y = j >> 4, lo = j & 15, hi = j & ~15;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) ld_pair(buf, TL * e + hi + (lo ^ ((y + (TL / 16) * e) & 15)), v0[e], v1[e]);
+  }
+}
+
+template <int LOG2N, int STAGE, int X0, class Hook>
+__device__ __forceinline__ void pair_stages(cpx<float> (&v0)[16], cpx<float> (&v1)[16], int j,
+                                            const PairTw<LOG2N>& tw, cpx<float>* xb0, cpx<float>* xb1,
+                                            const Hook& hook) {
+  if constexpr (STAGE < PairCfg<LOG2N>::NS) {
+    pair_stage<LOG2N, STAGE, X0 + STAGE, Hook>(v0, v1, j, tw, xb0, xb1, hook);
+    pair_stages<LOG2N, STAGE + 1, X0, Hook>(v0, v1, j, tw, xb0, xb1, hook);
+  }
+}
+
+template <int LOG2N, int X0, class Hook>
+__device__ __forceinline__ void pair_fft(cpx<float> (&v0)[16], cpx<float> (&v1)[16], int j,
+                                         const PairTw<LOG2N>& tw, cpx<float>* xb0, cpx<float>* xb1,
+                                         const Hook& hook) {
+  pair_stages<LOG2N, 0, X0, Hook>(v0, v1, j, tw, xb0, xb1, hook);
+}
+
+template <int LOG2N, int MODE, class Hook>
+__device__ __forceinline__ void pair_body(cpx<float> (&v0)[16], cpx<float> (&v1)[16], int j,
+                                          const PairTw<LOG2N>& tw, cpx<float>* xb0, cpx<float>* xb1,
+                                          const Hook& hook, const Phase& ph0, uint64_t l, float scale,
+                                          bool sign_only) {
+  constexpr int TL = PairCfg<LOG2N>::TL;
+  constexpr int NX = PairCfg<LOG2N>::NX;
+  if constexpr (MODE == 0) {
+    apply_chirp<float, TL, false, false>(v0, ph0, l, (uint64_t)j, scale, sign_only);
+    apply_chirp<float, TL, false, false>(v1, ph0, l + 1, (uint64_t)j, scale, sign_only);
+    pair_fft<LOG2N, 0>(v0, v1, j, tw, xb0, xb1, hook);
+  } else if constexpr (MODE == 1) {
+    pair_fft<LOG2N, 0>(v0, v1, j, tw, xb0, xb1, hook);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      v0[e] = cconj(v0[e]);
+      v1[e] = cconj(v1[e]);
+    }
+    Phase ph = ph0;   // conj(chirp) = chirp of -t
+    ph.cA = 0 - ph.cA; ph.cB = 0 - ph.cB; ph.cC = 0 - ph.cC;
+    ph.cL = 0 - ph.cL; ph.cE = 0 - ph.cE; ph.cK = 0 - ph.cK;
+    apply_chirp<float, TL, false, false>(v0, ph, l, (uint64_t)j, scale, false);
+    apply_chirp<float, TL, false, false>(v1, ph, l + 1, (uint64_t)j, scale, false);
+    pair_fft<LOG2N, NX>(v0, v1, j, tw, xb0, xb1, hook);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      v0[e] = cconj(v0[e]);
+      v1[e] = cconj(v1[e]);
+    }
+  } else if constexpr (MODE == 2) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      v0[e] = cconj(v0[e]);
+      v1[e] = cconj(v1[e]);
+    }
+    pair_fft<LOG2N, 0>(v0, v1, j, tw, xb0, xb1, hook);
+    apply_chirp<float, TL, true, false>(v0, ph0, l, (uint64_t)j, scale, false);
+    apply_chirp<float, TL, true, false>(v1, ph0, l + 1, (uint64_t)j, scale, false);
+    pair_fft<LOG2N, NX>(v0, v1, j, tw, xb0, xb1, hook);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      v0[e] = cconj(v0[e]);
+      v1[e] = cconj(v1[e]);
+    }
+    pair_fft<LOG2N, 0>(v0, v1, j, tw, xb0, xb1, hook);
+    apply_chirp<float, TL, true, true>(v0, ph0, l, (uint64_t)j, scale, sign_only);
+    apply_chirp<float, TL, true, true>(v1, ph0, l + 1, (uint64_t)j, scale, sign_only);
+  }
+}
+
+template <int LOG2N, int MODE>
+__global__ void __launch_bounds__(PairCfg<LOG2N>::THREADS, 1)
+line_pass_pair_kernel(PassArgs a, long long n_groups, unsigned long long* counter) {
+  using C = PairCfg<LOG2N>;
+  constexpr int N = C::N, TL = C::TL, GE = C::GE, BE = C::BE;
+  constexpr uint32_t GROUP_BYTES = GE * sizeof(cpx<float>);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cpx<float>* stage = reinterpret_cast<cpx<float>*>(smem_raw);                       // buffers 0, 1
+  cpx<float>* xbuf = stage + 2 * BE;                                                // buffer 2
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 3 * BE * sizeof(cpx<float>));
+  long long* s_next = reinterpret_cast<long long*>(bar + 2);
+
+  const int j = threadIdx.x;
+  const cpx<float>* __restrict__ tw = reinterpret_cast<const cpx<float>*>(a.tw);
+  const cpx<float>* __restrict__ in = reinterpret_cast<const cpx<float>*>(a.in);
+  cpx<float>* __restrict__ out = reinterpret_cast<cpx<float>*>(a.out);
+  PairTw<LOG2N> tws;
+  tws.load(tw, j);
+
+  if (j == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+    const long long g0 = (long long)atomicAdd(counter, 1ull);
+    if (g0 < n_groups) {
+      mbar_expect_tx(&bar[0], GROUP_BYTES);
+      bulk_g2s(stage, in + g0 * GE, GROUP_BYTES, &bar[0]);
+    }
+    s_next[1] = g0;
+  }
+  __syncthreads();
+  long long g = s_next[1];
+  for (int k = 0; g < n_groups; ++k) {
+    const int b = k & 1;
+    cpx<float>* sb = stage + b * BE;
+    mbar_wait(&bar[b], (uint32_t)((k >> 1) & 1));
+    const long long line0 = g * 2;
+    const int l = (int)(line0 % N);
+    cpx<float> v0[16], v1[16];
+    if constexpr (MODE == 0) {   // user's row-major lines, contiguous
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        v0[e] = sb[j + TL * e];
+        v1[e] = sb[N + j + TL * e];
+      }
+    } else {                     // pair-interleaved: element mu of line ll at 2 mu + ll
+#pragma unroll
+      for (int e = 0; e < 16; ++e) ld_pair(sb, j + TL * e, v0[e], v1[e]);
+    }
+    struct Prefetch {
+      int tid, b;
+      unsigned long long* counter;
+      long long n_groups;
+      cpx<float>* next_buf;
+      const cpx<float>* in;
+      uint64_t* bar;
+      long long* s_next;
+      __device__ __forceinline__ void run() const {
+        if (tid == 0) {
+          const long long gn = (long long)atomicAdd(counter, 1ull);
+          if (gn < n_groups) {
+            fence_proxy_async_smem();
+            mbar_expect_tx(&bar[b ^ 1], GROUP_BYTES);
+            bulk_g2s(next_buf, in + gn * GE, GROUP_BYTES, &bar[b ^ 1]);
+          }
+          s_next[b] = gn;
+        }
+      }
+    };
+    const Prefetch pf{j, b, counter, n_groups, stage + (b ^ 1) * BE, in, bar, s_next};
+    // exchange 0 uses the spare buffer, so the staging buffer is free only after its
+    // barrier (see line_pass_pipe_kernel)
+    pair_body<LOG2N, MODE>(v0, v1, j, tws, xbuf, sb, pf, a.ph, (uint64_t)l, (float)a.scale,
+                           a.sign_only != 0);
+
+    if constexpr (MODE == 3) {
+      cpx<float>* d0 = out + line0 * N + j;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        d0[TL * e] = v0[e];
+        d0[N + TL * e] = v1[e];
+      }
+    } else {
+      // element i = j + TL e of lines (l, l+1) -> pair-interleaved transposed output:
+      // (i/2)*2N + 2*line + i%2.  Lanes j, j^1 swap one value so that the even lane
+      // holds line l at (i, i+1) and the odd lane line l+1 at (i, i+1).
+      const bool odd = (j & 1) != 0;
+      cpx<float>* dst = out + (line0 / N) * (long long)N * N + (long long)(j >> 1) * (2 * N) + 2 * l +
+                        (odd ? 2 : 0);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const cpx<float> send = odd ? v0[e] : v1[e];
+        cpx<float> recv;
+        recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+        recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+        const cpx<float> lo = odd ? recv : v0[e];
+        const cpx<float> hi = odd ? v1[e] : recv;
+        *reinterpret_cast<float4*>(dst + (long long)e * (TL / 2) * (2 * N)) = make_float4(lo.x, lo.y, hi.x, hi.y);
+      }
+    }
+    g = s_next[b];
   }
 }
 

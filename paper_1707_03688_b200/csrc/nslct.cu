@@ -74,6 +74,24 @@ cudaError_t set_attr_pipe() {
 }
 typedef cudaError_t (*pipe_fn)(const PassArgs&, cudaStream_t, int, unsigned long long*);
 
+// line-pair variant (c64, N = 4096): 256 threads, both lines of a group per thread
+template <int LOG2N, int MODE>
+cudaError_t launch_pair(const PassArgs& a, cudaStream_t s, int grid, unsigned long long* counter) {
+  using Cfg = nslct::PairCfg<LOG2N>;
+  const size_t smem = (size_t)Cfg::NBUF * Cfg::BE * sizeof(nslct::cpx<float>) + kPipeExtra;
+  const long long n_groups = a.n_lines / Cfg::G;
+  const long long g = n_groups < grid ? n_groups : grid;
+  nslct::line_pass_pair_kernel<LOG2N, MODE><<<(unsigned)g, Cfg::THREADS, smem, s>>>(a, n_groups, counter);
+  return cudaGetLastError();
+}
+template <int LOG2N, int MODE>
+cudaError_t set_attr_pair() {
+  using Cfg = nslct::PairCfg<LOG2N>;
+  const size_t smem = (size_t)Cfg::NBUF * Cfg::BE * sizeof(nslct::cpx<float>) + kPipeExtra;
+  return cudaFuncSetAttribute(nslct::line_pass_pair_kernel<LOG2N, MODE>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 template <typename T, int LOG2N>
 struct PipeRow {
   static void fill(pipe_fn* l, attr_fn* at) {
@@ -111,6 +129,8 @@ struct Table {
   attr_fn at[2][kMaxLog + 1][4] = {};
   pipe_fn lp[kMaxLog + 1][4] = {};   // c64 only
   attr_fn atp[kMaxLog + 1][4] = {};
+  pipe_fn lpair[4] = {launch_pair<12, 0>, launch_pair<12, 1>, launch_pair<12, 2>, launch_pair<12, 3>};
+  attr_fn atpair[4] = {set_attr_pair<12, 0>, set_attr_pair<12, 1>, set_attr_pair<12, 2>, set_attr_pair<12, 3>};
   Table() {
     PipeRow<float, 10>::fill(lp[10], atp[10]);
     PipeRow<float, 11>::fill(lp[11], atp[11]);
@@ -205,6 +225,7 @@ struct nslct_plan_s {
   PassArgs args[5];
   int mode[5] = {0, 1, 2, 1, 3};
   bool pipe = false;   // persistent TMA-pipelined kernels
+  bool pair = false;   // ... in the line-pair variant (c64, N = 4096)
   unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
   int num_sms = 148;
   nslct::B0Args b0{};
@@ -407,6 +428,9 @@ nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16],
         pl->num_sms = sms;
       const char* np = std::getenv("NSLCT_NO_PIPE");
       pl->pipe = (ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
+      // the line-pair kernel is an opt-in experiment (measured slower)
+      const char* ypair = std::getenv("NSLCT_PAIR");
+      pl->pair = pl->pipe && lg == 12 && (ypair && ypair[0] == '1');
     }
     if (pl->pipe) {
       cudaError_t e = cudaMalloc(&pl->counters, 8 * sizeof(unsigned long long));
@@ -415,6 +439,14 @@ nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16],
         break;
       }
     }
+    for (int m = 0; m < 4 && pl->pair; ++m) {
+      cudaError_t e = table().atpair[m]();
+      if (e != cudaSuccess) {
+        result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(pair): ") + cudaGetErrorString(e));
+        break;
+      }
+    }
+    if (result != NSLCT_OK) break;
     for (int m = 0; m < 4 && pl->pipe; ++m) {
       cudaError_t e = table().atp[lg][m]();
       if (e != cudaSuccess) {
@@ -484,7 +516,9 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
     PassArgs a = pl->args[k];
     a.in = src[k];
     a.out = dst[k];
-    if (pl->pipe)
+    if (pl->pair)
+      CUDA_TRY(table().lpair[pl->mode[k]](a, s, pl->num_sms, pl->counters + k));
+    else if (pl->pipe)
       CUDA_TRY(table().lp[pl->log2n][pl->mode[k]](a, s, pl->num_sms, pl->counters + k));
     else
       CUDA_TRY(table().l[ti][pl->log2n][pl->mode[k]](a, s));
