@@ -1,0 +1,59 @@
+"""World-size-2 gloo test (CPU) of the multi-rank host logic of bench.py: the timing is
+the MAX over ranks and the work is the SUM over ranks (weak scaling, no collective on the
+data path).  Rendezvous on 127.0.0.1."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    import bench
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w, r, lr = bench.dist_env()
+        t = bench.max_over_ranks(1.5 + rank, w)           # rank-dependent step time
+        units = bench.sum_over_ranks(32, w)                # per-rank batch of 32 images
+        q.put((rank, w, r, t, units))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_rank_aggregation_gloo():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(world))
+    for rank, w, r, t, units in res:
+        assert w == 2 and r == rank
+        assert t == 2.5            # max over ranks of (1.5, 2.5)
+        assert units == 64.0       # weak scaling: 2 x 32 images per step
+
+
+def test_bench_single_rank_defaults(monkeypatch):
+    import bench
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        monkeypatch.delenv(k, raising=False)
+    assert bench.dist_env() == (1, 0, 0)
+    assert bench.max_over_ranks(3.0, 1) == 3.0
+    assert bench.sum_over_ranks(32, 1) == 32.0
