@@ -385,6 +385,93 @@ struct TwTab {
   }
 };
 
+// Twiddle powers cached in TENSOR MEMORY (sm_100a).  The persistent c64 kernels issue no
+// MMAs, so TMEM (512 columns x 128 lanes x 32 bit per SM) is free: each thread parks its
+// stage twiddles w^r = exp(-2 pi i k0 r / N) (up to 15 complex = 30 columns per stage, from
+// the fp64-accurate table) in its own TMEM lane once per kernel and reloads them with
+// tcgen05.ld (measured ~390 B/clk/SM, a path separate from shared memory,
+// tools/micro_tmem.cu), instead of regenerating them by 14 complex products per butterfly.
+// Warp w owns lanes 32*(w%4)..+31 and, with 16 warps, columns (w/4)*128..+127.
+__device__ __forceinline__ void tmem_ld16(uint32_t ta, float (&f)[16]) {
+  uint32_t v[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(ta));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t ta, const float (&f)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+      "r"(__float_as_uint(f[0])), "r"(__float_as_uint(f[1])), "r"(__float_as_uint(f[2])), "r"(__float_as_uint(f[3])),
+      "r"(__float_as_uint(f[4])), "r"(__float_as_uint(f[5])), "r"(__float_as_uint(f[6])), "r"(__float_as_uint(f[7])),
+      "r"(__float_as_uint(f[8])), "r"(__float_as_uint(f[9])), "r"(__float_as_uint(f[10])), "r"(__float_as_uint(f[11])),
+      "r"(__float_as_uint(f[12])), "r"(__float_as_uint(f[13])), "r"(__float_as_uint(f[14])), "r"(__float_as_uint(f[15]))
+      : "memory");
+}
+
+template <int LOG2N>
+struct TwTmem {
+  using Sh = FftShape<LOG2N>;
+  uint32_t ta;   // this thread's TMEM address: lane quadrant + its warp's column base
+  // stage S (>= 1) uses columns (S-1)*32 .. +31: complex index b*(R-1) + (r-1)
+  __device__ __forceinline__ void fill(const cpx<float>* __restrict__ tw, int j) const {
+    fill_stage<1>(tw, j);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  template <int S>
+  __device__ __forceinline__ void fill_stage(const cpx<float>* __restrict__ tw, int j) const {
+    if constexpr (S < Sh::NS) {
+      constexpr int R = Sh::template R<S>(), Ns = Sh::template Ns<S>(), NB = 16 / R;
+      float f[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) f[i] = 0.f;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int jp = j + b * Sh::TL;
+        const int k0 = (jp % Ns) * (Sh::N / (Ns * R));
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          const cpx<float> w = tw[k0 * r];
+          f[2 * (b * (R - 1) + r - 1)] = w.x;
+          f[2 * (b * (R - 1) + r - 1) + 1] = w.y;
+        }
+      }
+      float h0[16], h1[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        h0[i] = f[i];
+        h1[i] = f[16 + i];
+      }
+      tmem_st16(ta + (uint32_t)((S - 1) * 32), h0);
+      tmem_st16(ta + (uint32_t)((S - 1) * 32 + 16), h1);
+      fill_stage<S + 1>(tw, j);
+    }
+  }
+  template <int S, int R>
+  __device__ __forceinline__ void apply(cpx<float>* u, int b, int /*jp*/) const {
+    // complex index c = b*(R-1) + r-1 lives in columns 2c, 2c+1 of the stage block
+    float h[16];
+    tmem_ld16(ta + (uint32_t)((S - 1) * 32), h);           // complex 0..7
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const int c = b * (R - 1) + r - 1;
+      if (c < 8) u[r] = cmul(u[r], cpx<float>{h[2 * c], h[2 * c + 1]});
+    }
+    if ((16 / R) * (R - 1) > 8) {
+      tmem_ld16(ta + (uint32_t)((S - 1) * 32 + 16), h);    // complex 8..15
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        const int c = b * (R - 1) + r - 1;
+        if (c >= 8) u[r] = cmul(u[r], cpx<float>{h[2 * (c - 8)], h[2 * (c - 8) + 1]});
+      }
+    }
+  }
+};
+
 // Exchange policies (how a stage hands its outputs to the next stage through shared
 // memory).  X is the compile-time index of the exchange within the pass.
 //  ExPad: one padded buffer (index i + i/16, N + N/16 per line); write, barrier, read,
@@ -820,6 +907,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
   cpx<T>* xbuf = stage + 2 * BE;                                            // buffer 2
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 3 * BE * sizeof(cpx<T>));  // 2 mbarriers
   long long* s_next = reinterpret_cast<long long*>(bar + 2);                // 2 slots
+  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(s_next + 2);              // TMEM base
 
   // Lines of a group are interleaved across lanes (line gl = tid % G): the lanes holding
   // elements (i, i+1) of all G lines then form one contiguous G*IL-element segment of the
@@ -832,8 +920,25 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
   const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in);
   cpx<T>* __restrict__ out = reinterpret_cast<cpx<T>*>(a.out);
 
+#ifdef NSLCT_TMEM_TWIDDLES
+  // this thread's twiddle powers, the same for every group, cached in TMEM (TwTmem);
+  // opt-in: measured ~2% slower than TwSet (fewer FP instructions, more moves)
+  const int warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_taddr)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *s_taddr;
+  const TwTmem<LOG2N> tws{tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128)};
+  tws.fill(tw, j);
+#else
+  (void)s_taddr;
   TwSet<T, LOG2N> tws;   // this thread's twiddle bases, the same for every group
   tws.load(tw, j);
+#endif
 
   // Groups are claimed in order from a global counter (not round-robin) so the groups
   // in flight across the GPU stay a contiguous window: the 8*G-byte pieces of the
@@ -906,6 +1011,11 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     }
     g = s_next[b];   // written by thread 0 before at least one later barrier
   }
+#ifdef NSLCT_TMEM_TWIDDLES
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+#endif
 }
 
 // ---------------------------------------------------------------------------------
@@ -950,55 +1060,101 @@ __device__ __forceinline__ void ld_pair(const cpx<float>* base_pairs, int unit, 
 }
 
 template <int LOG2N>
-struct PairTw {   // w[s][r] = exp(-2 pi i k0_s r / N), k0_s = (j % Ns) N/(Ns 16), s = 1..NS-1
+struct PairTw {   // both lines' twiddles w^r (r = 1..15) per stage, cached in TMEM (see TwTmem)
   using C = PairCfg<LOG2N>;
-  cpx<float> w[C::NS][16];
-  __device__ __forceinline__ void load(const cpx<float>* __restrict__ tw, int j) {
+  uint32_t ta;
+  __device__ __forceinline__ void fill(const cpx<float>* __restrict__ tw, int j) const {
 #pragma unroll
     for (int s = 1; s < C::NS; ++s) {
       const int Ns = 1 << (4 * s);
       const int k0 = (j % Ns) * (C::N / (Ns * 16));
+      float h0[16], h1[16];
 #pragma unroll
-      for (int r = 1; r < 16; ++r) w[s][r] = tw[k0 * r];
+      for (int r = 1; r < 16; ++r) {
+        const cpx<float> w = tw[k0 * r];
+        const int c = r - 1;
+        if (c < 8) {
+          h0[2 * c] = w.x;
+          h0[2 * c + 1] = w.y;
+        } else {
+          h1[2 * (c - 8)] = w.x;
+          h1[2 * (c - 8) + 1] = w.y;
+        }
+      }
+      h1[14] = 0.f;
+      h1[15] = 0.f;
+      tmem_st16(ta + (uint32_t)((s - 1) * 32), h0);
+      tmem_st16(ta + (uint32_t)((s - 1) * 32 + 16), h1);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  template <int S>
+  __device__ __forceinline__ void apply2(cpx<float> (&v0)[16], cpx<float> (&v1)[16]) const {
+    float h[16];
+    tmem_ld16(ta + (uint32_t)((S - 1) * 32), h);
+#pragma unroll
+    for (int r = 1; r <= 8; ++r) {
+      const cpx<float> w{h[2 * (r - 1)], h[2 * (r - 1) + 1]};
+      v0[r] = cmul(v0[r], w);
+      v1[r] = cmul(v1[r], w);
+    }
+    tmem_ld16(ta + (uint32_t)((S - 1) * 32 + 16), h);
+#pragma unroll
+    for (int r = 9; r < 16; ++r) {
+      const cpx<float> w{h[2 * (r - 9)], h[2 * (r - 9) + 1]};
+      v0[r] = cmul(v0[r], w);
+      v1[r] = cmul(v1[r], w);
     }
   }
 };
 
+// Exchange of one line of the pair: buf holds [line 0: N][line 1: N], XOR swizzle of each
+// 16-element group (c = 0; all lanes of an access belong to one line).
+template <int LOG2N, int Ns>
+__device__ __forceinline__ void pair_store_line(cpx<float>* lb, int j, const cpx<float> (&u)[16]) {
+  const int idxD = (j / Ns) * Ns * 16 + (j % Ns);
+  if constexpr (Ns == 1) {
+    cpx<float>* wb = lb + idxD;
+    const int x = (idxD >> 4) & 15;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) wb[r ^ x] = u[r];
+  } else {
+    cpx<float>* wb = lb + (idxD & ~15);
+    const int y = idxD >> 4, lo = j & 15;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) wb[r * Ns + (lo ^ ((y + r * (Ns / 16)) & 15))] = u[r];
+  }
+}
+template <int LOG2N>
+__device__ __forceinline__ void pair_load_line(const cpx<float>* lb, int j, cpx<float> (&v)[16]) {
+  constexpr int TL = PairCfg<LOG2N>::TL;
+  const int y = j >> 4, lo = j & 15, hi = j & ~15;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] = lb[TL * e + hi + (lo ^ ((y + (TL / 16) * e) & 15))];
+}
+
+// One radix-16 stage of both lines.  Line 0's exchange stores are issued before line 1's
+// butterfly is computed, and after the barrier line 0's loads come first, so in every
+// warp the shared-memory traffic of one line overlaps the FP work of the other.
 template <int LOG2N, int STAGE, int X, class Hook>
 __device__ __forceinline__ void pair_stage(cpx<float> (&v0)[16], cpx<float> (&v1)[16], int j,
                                            const PairTw<LOG2N>& tw, cpx<float>* xb0, cpx<float>* xb1,
                                            const Hook& hook) {
   using C = PairCfg<LOG2N>;
-  constexpr int TL = C::TL;
+  constexpr int N = C::N;
   constexpr int Ns = 1 << (4 * STAGE);
   constexpr bool LAST = (STAGE == C::NS - 1);
-  if constexpr (STAGE > 0) {
-#pragma unroll
-    for (int r = 1; r < 16; ++r) {
-      v0[r] = cmul(v0[r], tw.w[STAGE][r]);
-      v1[r] = cmul(v1[r], tw.w[STAGE][r]);
-    }
-  }
+  if constexpr (STAGE > 0) tw.template apply2<STAGE>(v0, v1);
+  cpx<float>* buf = (X & 1) ? xb1 : xb0;
   dft<16>(v0);
+  if constexpr (!LAST) pair_store_line<LOG2N, Ns>(buf, j, v0);
   dft<16>(v1);
   if constexpr (!LAST) {
-    cpx<float>* buf = (X & 1) ? xb1 : xb0;
-    // unit (16 B) index of element i: i ^ ((i >> 4) & 15)
-    const int idxD = (j / Ns) * Ns * 16 + (j % Ns);
-    if constexpr (Ns == 1) {
-      const int x = (idxD >> 4) & 15;
-#pragma unroll
-      for (int r = 0; r < 16; ++r) st_pair(buf, idxD + (r ^ x), v0[r], v1[r]);
-    } else {
-      const int y = idxD >> 4, lo = j & 15, hi = idxD & ~15;
-#pragma unroll
-      for (int r = 0; r < 16; ++r) st_pair(buf, hi + r * Ns + (lo ^ ((y + r * (Ns / 16)) & 15)), v0[r], v1[r]);
-    }
+    pair_store_line<LOG2N, Ns>(buf + N, j, v1);
     __syncthreads();
     if constexpr (X == 0) hook.run();
-    const int y = j >> 4, lo = j & 15, hi = j & ~15;
-#pragma unroll
-    for (int e = 0; e < 16; ++e) ld_pair(buf, TL * e + hi + (lo ^ ((y + (TL / 16) * e) & 15)), v0[e], v1[e]);
+    pair_load_line<LOG2N>(buf, j, v0);
+    pair_load_line<LOG2N>(buf + N, j, v1);
   }
 }
 
@@ -1081,13 +1237,25 @@ line_pass_pair_kernel(PassArgs a, long long n_groups, unsigned long long* counte
   cpx<float>* xbuf = stage + 2 * BE;                                                // buffer 2
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 3 * BE * sizeof(cpx<float>));
   long long* s_next = reinterpret_cast<long long*>(bar + 2);
+  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(s_next + 2);
 
   const int j = threadIdx.x;
   const cpx<float>* __restrict__ tw = reinterpret_cast<const cpx<float>*>(a.tw);
   const cpx<float>* __restrict__ in = reinterpret_cast<const cpx<float>*>(a.in);
   cpx<float>* __restrict__ out = reinterpret_cast<cpx<float>*>(a.out);
-  PairTw<LOG2N> tws;
-  tws.load(tw, j);
+  const int warp = j >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_taddr)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *s_taddr;
+  constexpr int WARPS = C::THREADS / 32;
+  constexpr int COLS = 512 / ((WARPS + 3) / 4);
+  const PairTw<LOG2N> tws{tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * COLS)};
+  tws.fill(tw, j);
 
   if (j == 0) {
     mbar_init(&bar[0], 1);
@@ -1172,6 +1340,9 @@ line_pass_pair_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     }
     g = s_next[b];
   }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
 }
 
 // ---------------------------------------------------------------------------------
