@@ -223,6 +223,8 @@ def run_ours(args):
     n, batch, dtype, desc = CONFIGS[args.config]
     mr, _ = synth.config_streams(args.config)
     M = synth.random_symplectic(mr)                 # same matrix on every rank
+    if args.config == 5 and world > 1:
+        return run_slab(args, n, M, dtype, desc, world, rank, local, dev)
     gen = torch.Generator(device=dev)
     gen.manual_seed(synth.SEED_BASE + 1000 * args.config + rank)
     x = torch.randn((batch, n, n), dtype=torch.complex64, device=dev, generator=gen)   # CN(0,1)
@@ -321,6 +323,60 @@ def run_ours(args):
         print(json.dumps(res))
     if world > 1:
         torch.distributed.destroy_process_group()
+    return 0
+
+
+def run_slab(args, n, M, dtype, desc, world, rank, local, dev):
+    """C5: ONE n x n transform as row slabs over `world` GPUs, NCCL all-to-all between the
+    5 passes (nslct_plan_slab / nslct_exec_pass).  Strong scaling."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_1707_03688_b200 import nslct
+    L = n // world
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(synth.SEED_BASE + 5000 + rank)
+    x = torch.randn((L, n), dtype=torch.complex64, device=dev, generator=gen)
+    out = torch.empty_like(x)
+    plan = nslct.SlabPlan(n, M, world, rank, device=local)
+    exchange = nslct.torch_all_to_all()
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        plan.run(x, exchange, out, stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        plan.run(x, exchange, out, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, dev)
+    passes = plan.n_passes
+    plan.close()
+    hbm_bytes_gpu = passes * 2.0 * n * L * 8
+    a2a_bytes_gpu = (passes - 1) * (world - 1) / world * n * L * 8     # per GPU per direction
+    nvlink_gbs = 900.0
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": 1.0 / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": desc + ", row slabs of %d x %d per GPU" % (L, n), "n": n, "global_batch": 1,
+                       "parallelism": "row-slab x%d, NCCL all-to-all between passes" % world},
+            "roofline": {"bound": "nvlink", "achieved": a2a_bytes_gpu / (ms * 1e-3) / 1e9, "peak": nvlink_gbs,
+                         "unit": "GB/s", "frac": a2a_bytes_gpu / (ms * 1e-3) / 1e9 / nvlink_gbs, "traffic": None,
+                         "hbm_alg_bytes_per_gpu": hbm_bytes_gpu, "alltoall_bytes_per_gpu_per_dir": a2a_bytes_gpu,
+                         "nvlink_bound_ms": a2a_bytes_gpu / nvlink_gbs / 1e6},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": passes * args.steps, "clocks": clk,
+        }
+        print(json.dumps(res))
+    dist.destroy_process_group()
     return 0
 
 

@@ -102,6 +102,29 @@ nslct_status nslct_exec(nslct_plan_t plan, const void* in, void* out, void* cuda
 nslct_status nslct_exec_host(nslct_plan_t plan, const void* host_in, void* host_out,
                              void* cuda_stream);
 
+/* Row-slab mode: ONE n x n transform sharded over nranks processes (one
+ * per GPU) as row slabs of L = n/nranks rows; rank `rank` holds rows [rank*L, (rank+1)*L)
+ * of the input and of the output, row-major [L][n].  The transform runs as n_passes
+ * passes (nslct_plan_info); between consecutive passes the CALLER performs one all-to-all
+ * of nranks equal blocks of L*L complex elements (e.g. NCCL through torch.distributed
+ * all_to_all_single): the send buffer is the previous pass's `out`, laid out [n][L] =
+ * nranks row-blocks of [L][L] (block s goes to rank s), and the receive buffer (block
+ * from rank s at element offset s*L*L) is the next pass's `in`.  This exchange is the
+ * distributed form of the transposes the single-GPU passes fold into their stores.
+ * Requires B != 0 (the B = 0 gather has no slab form), nranks | n, and L a multiple of
+ * the kernel's lines per CTA (L >= 16 suffices for n >= 4096).  The plan allocates no
+ * scratch: the caller owns all buffers (each n*L complex elements).  Errors: as
+ * nslct_plan_ex, E_ARG for bad nranks/rank/L. */
+nslct_status nslct_plan_slab(nslct_plan_t* plan, int64_t n, const double abcd[16], int nranks,
+                             int rank, nslct_dtype dtype, const nslct_opts* opts);
+
+/* Run ONE pass (0 <= pass < n_passes) of a plan on `cuda_stream`: for a slab plan, the
+ * pass of this rank's slab (layouts above); for a batched plan, pass k of nslct_exec
+ * with the batched layouts (in/out are then the plan-documented intermediates; mainly
+ * for debugging).  Asynchronous, no allocation.  Errors: E_ARG, E_CUDA. */
+nslct_status nslct_exec_pass(nslct_plan_t plan, int pass, const void* in, void* out,
+                             void* cuda_stream);
+
 typedef struct {
   int kind;                    /* 0 = B=0 (Eq. Intro20), 1 = form I (Eq. HA28), 2 = form II  */
   int variant;                 /* variant actually used (LC falls back to HA: PAPER.md:840)  */

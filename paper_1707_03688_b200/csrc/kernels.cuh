@@ -703,6 +703,12 @@ struct PassArgs {
   Phase ph;
   double scale;
   int sign_only;       // the chirp is only the centring checkerboard (Q0/Q4 absent)
+  // Row-slab mode (one transform over P ranks; line_pass_kernel only).  Defaults give
+  // the batched layout: L = N lines per image, offset 0, one chunk per line.
+  int lines_per_img;   // L: lines of one image handled here (N, or N/P in slab mode)
+  int line_offset;     // global index of local line 0 (chirps use global indices)
+  int in_chunk;        // C: input line = N/C chunks of C contiguous elements ...
+  long long in_chunk_stride;  // ... CS elements apart (slab: C = L, CS = L*L)
 };
 
 // The per-line work of one pass (registers v hold elements j + TL*e of line l).
@@ -771,42 +777,55 @@ line_pass_kernel(PassArgs a) {
   const int tid = threadIdx.x;
   const int j = tid % TL;
   const int gl = tid / TL;
-  const long long line0 = (long long)blockIdx.x * G;   // first global line of this CTA
+  const int L = a.lines_per_img;
+  const long long line0 = (long long)blockIdx.x * G;   // first line (over the batch) of this CTA
   const long long line = line0 + gl;
-  const long long img = line / N;
-  const int l = (int)(line % N);
+  const long long img = line / L;
+  const int ll = (int)(line % L);                       // local line within the image
+  const int l = a.line_offset + ll;                      // global line index
+  const long long img_elems = (long long)N * L;
   cpx<T>* buf = smem + gl * LS;
   const cpx<T>* __restrict__ tw = reinterpret_cast<const cpx<T>*>(a.tw);
-  const cpx<T>* __restrict__ src = reinterpret_cast<const cpx<T>*>(a.in) + line * N;
+  const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in) + img * img_elems;
 
   cpx<T> v[16];
+  if (a.in_chunk == N) {
+    const cpx<T>* src = in + (long long)ll * N + j;
 #pragma unroll
-  for (int e = 0; e < 16; ++e) v[e] = src[j + TL * e];
+    for (int e = 0; e < 16; ++e) v[e] = src[TL * e];
+  } else {   // slab mode: element i of the line is at (i / C) * CS + ll * C + i % C
+    const int C = a.in_chunk;
+    const long long CS = a.in_chunk_stride;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int i = j + TL * e;
+      v[e] = in[(long long)(i / C) * CS + (long long)ll * C + (i % C)];
+    }
+  }
 
   TwSet<T, LOG2N> tws;
   tws.load(tw, j);
   pass_body<T, LOG2N, MODE>(v, j, tws, a.ph, (uint64_t)l, (T)a.scale, a.sign_only != 0, ExPad<T>{buf});
 
+  cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * img_elems;
   if constexpr (MODE == 3) {
-    cpx<T>* dst = reinterpret_cast<cpx<T>*>(a.out) + line * N;
+    cpx<T>* dst = out + (long long)ll * N;
 #pragma unroll
     for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
   } else {
-    // transposed store: out[img][e][l] ; stage through shared memory so that
-    // consecutive threads write consecutive l.
+    // transposed store: out[img][e][ll] (L lines per row); staged through shared memory
+    // so that consecutive threads write consecutive lines.
     __syncthreads();   // all FFT reads of buf done (last stage keeps data in registers)
 #pragma unroll
     for (int e = 0; e < 16; ++e) buf[pad16(j + TL * e)] = v[e];
     __syncthreads();
-    const int l0 = (int)(line0 % N);
-    const long long img0 = line0 / N;
-    cpx<T>* dst = reinterpret_cast<cpx<T>*>(a.out) + img0 * (long long)N * N;
+    const int l0 = (int)(line0 % L);
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const int f = tid + k * THREADS;
-      const int ll = f % G;
+      const int gg = f % G;
       const int e = f / G;
-      dst[(long long)e * N + l0 + ll] = smem[ll * LS + pad16(e)];
+      out[(long long)e * L + l0 + gg] = smem[gg * LS + pad16(e)];
     }
   }
 }

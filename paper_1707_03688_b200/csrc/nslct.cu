@@ -224,6 +224,8 @@ struct nslct_plan_s {
   void* h_out = nullptr;
   PassArgs args[5];
   int mode[5] = {0, 1, 2, 1, 3};
+  bool slab = false;   // row-slab plan (nslct_plan_slab)
+  int nranks = 1, rank = 0;
   bool pipe = false;   // persistent TMA-pipelined kernels
   bool pair = false;   // ... in the line-pair variant (c64, N = 4096)
   unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
@@ -287,8 +289,22 @@ nslct_status nslct_plan(nslct_plan_t* plan, int64_t n, const double abcd[16], in
   return nslct_plan_ex(plan, n, abcd, batch, dtype, &o);
 }
 
+static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double abcd[16], int64_t batch,
+                                  nslct_dtype dtype, const nslct_opts* opts, int nranks, int rank);
+
 nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16], int64_t batch,
                            nslct_dtype dtype, const nslct_opts* opts) {
+  return plan_internal(plan, n, abcd, batch, dtype, opts, 0, 0);
+}
+
+nslct_status nslct_plan_slab(nslct_plan_t* plan, int64_t n, const double abcd[16], int nranks, int rank,
+                             nslct_dtype dtype, const nslct_opts* opts) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(NSLCT_E_ARG, "bad nranks/rank");
+  return plan_internal(plan, n, abcd, 1, dtype, opts, nranks, rank);
+}
+
+static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double abcd[16], int64_t batch,
+                                  nslct_dtype dtype, const nslct_opts* opts, int nranks, int rank) {
   g_err.clear();
   if (!plan || !abcd) return fail(NSLCT_E_ARG, "null plan or abcd pointer");
   *plan = nullptr;
@@ -309,10 +325,21 @@ nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16],
   if (!(std::isfinite(o.dx)) || (o.dx > 0 && !(o.dx < 1e30)))
     return fail(NSLCT_E_ARG, "bad dx");
 
+  const bool slab = nranks > 0;
+  int64_t L = n;
+  if (slab) {
+    if (n % nranks) return fail(NSLCT_E_ARG, "nranks must divide n");
+    L = n / nranks;
+    const int64_t TL = n / 16;
+    const int64_t TB = (n <= 2048) ? 256 : (n <= 8192 ? 512 : 1024);
+    const int64_t G = (TB / TL < n) ? TB / TL : n;
+    if (L % G) return fail(NSLCT_E_ARG, "slab height n/nranks must be a multiple of the lines per CTA");
+  }
   std::string err;
   nslct::Plan p;
   int st = nslct::make_plan(abcd, o.variant, o.dispatch, o.h_fixed, &p, &err);
   if (st) return fail((nslct_status)st, err);
+  if (slab && p.kind == 0) return fail(NSLCT_E_ARG, "B = 0 has no row-slab form");
 
   nslct_plan_s* pl = new (std::nothrow) nslct_plan_s();
   if (!pl) return fail(NSLCT_E_OOM, "host allocation failed");
@@ -325,6 +352,9 @@ nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16],
   pl->dx = (o.dx > 0) ? o.dx : std::sqrt(2.0 * M_PI / (double)n);
   pl->elem = (dtype == NSLCT_C64) ? 8 : 16;
   pl->bytes = (size_t)batch * (size_t)n * (size_t)n * pl->elem;
+  pl->slab = slab;
+  pl->nranks = slab ? nranks : 1;
+  pl->rank = slab ? rank : 0;
   if (o.device >= 0) {
     pl->device = o.device;
   } else {
@@ -393,7 +423,7 @@ nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16],
         break;
       }
     }
-    {
+    if (!slab) {
       cudaError_t e = cudaMalloc(&pl->scratch, pl->bytes);
       if (e != cudaSuccess) {
         result = fail(e == cudaErrorMemoryAllocation ? NSLCT_E_OOM : NSLCT_E_CUDA,
@@ -421,13 +451,18 @@ nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16],
       pl->args[k].ph = ph[k];
       pl->args[k].scale = sc[k];
       pl->args[k].sign_only = sign_only[k];
+      pl->args[k].lines_per_img = (int)L;
+      pl->args[k].line_offset = slab ? (int)(rank * L) : 0;
+      pl->args[k].in_chunk = (slab && k > 0) ? (int)L : (int)n;
+      pl->args[k].in_chunk_stride = (slab && k > 0) ? L * L : n * n;
+      if (slab) pl->args[k].n_lines = L;
     }
     {
       int sms = 0;
       if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device) == cudaSuccess && sms > 0)
         pl->num_sms = sms;
       const char* np = std::getenv("NSLCT_NO_PIPE");
-      pl->pipe = (ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
+      pl->pipe = (!slab && ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
       // the line-pair kernel is an opt-in experiment (measured slower)
       const char* ypair = std::getenv("NSLCT_PAIR");
       pl->pair = pl->pipe && lg == 12 && (ypair && ypair[0] == '1');
@@ -477,6 +512,7 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
   if (!in || !out) return fail(NSLCT_E_ARG, "null in/out pointer");
   if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(NSLCT_E_ARG, "in/out must be 16-byte aligned");
+  if (pl->slab) return fail(NSLCT_E_ARG, "slab plans run pass by pass: nslct_exec_pass");
   DeviceGuard guard(pl->device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int ti = (pl->dtype == NSLCT_C64) ? 0 : 1;
@@ -530,8 +566,35 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
   return NSLCT_OK;
 }
 
+nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* out, void* stream) {
+  if (!pl) return fail(NSLCT_E_ARG, "null plan");
+  if (!in || !out) return fail(NSLCT_E_ARG, "null in/out pointer");
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(NSLCT_E_ARG, "in/out must be 16-byte aligned");
+  if (pl->p.kind == 0) return fail(NSLCT_E_ARG, "the B = 0 plan has a single pass: use nslct_exec");
+  if (pass < 0 || pass >= 5) return fail(NSLCT_E_ARG, "pass out of range");
+  if (pass < 4 && in == out) return fail(NSLCT_E_ARG, "transposing passes cannot run in place");
+  DeviceGuard guard(pl->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int ti = (pl->dtype == NSLCT_C64) ? 0 : 1;
+  PassArgs a = pl->args[pass];
+  a.in = in;
+  a.out = out;
+  if (pl->pipe) {
+    CUDA_TRY(cudaMemsetAsync(pl->counters + pass, 0, sizeof(unsigned long long), s));
+    if (pl->pair)
+      CUDA_TRY(table().lpair[pl->mode[pass]](a, s, pl->num_sms, pl->counters + pass));
+    else
+      CUDA_TRY(table().lp[pl->log2n][pl->mode[pass]](a, s, pl->num_sms, pl->counters + pass));
+  } else {
+    CUDA_TRY(table().l[ti][pl->log2n][pl->mode[pass]](a, s));
+  }
+  return NSLCT_OK;
+}
+
 nslct_status nslct_exec_host(nslct_plan_t pl, const void* host_in, void* host_out, void* stream) {
   if (!pl) return fail(NSLCT_E_ARG, "null plan");
+  if (pl->slab) return fail(NSLCT_E_ARG, "slab plans run pass by pass: nslct_exec_pass");
   if (!host_in || !host_out) return fail(NSLCT_E_ARG, "null host pointer");
   DeviceGuard guard(pl->device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

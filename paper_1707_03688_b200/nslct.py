@@ -23,7 +23,7 @@ KINDS = {0: "B0", 1: "I", 2: "II"}
 # every symbol include/nslct.h declares
 EXPORTS = ("nslct_opts_default", "nslct_plan", "nslct_plan_ex", "nslct_exec", "nslct_exec_host",
            "nslct_plan_info", "nslct_plan_describe", "nslct_pass_ms", "nslct_destroy",
-           "nslct_last_error", "nslct_abi_version")
+           "nslct_last_error", "nslct_abi_version", "nslct_plan_slab", "nslct_exec_pass")
 
 
 class NslctError(RuntimeError):
@@ -65,6 +65,9 @@ def lib():
         L.nslct_plan.argtypes = [ctypes.POINTER(vp), i64, dp, i64, ctypes.c_int]
         L.nslct_plan_ex.argtypes = [ctypes.POINTER(vp), i64, dp, i64, ctypes.c_int, ctypes.POINTER(nslct_opts)]
         L.nslct_exec.argtypes = [vp, vp, vp, vp]
+        L.nslct_plan_slab.argtypes = [ctypes.POINTER(vp), i64, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.POINTER(nslct_opts)]
+        L.nslct_exec_pass.argtypes = [vp, ctypes.c_int, vp, vp, vp]
         L.nslct_exec_host.argtypes = [vp, vp, vp, vp]
         L.nslct_plan_info.argtypes = [vp, ctypes.POINTER(nslct_plan_desc)]
         L.nslct_plan_describe.argtypes = [i64, dp, ctypes.POINTER(nslct_opts), ctypes.POINTER(nslct_plan_desc)]
@@ -73,7 +76,8 @@ def lib():
         L.nslct_last_error.restype = ctypes.c_char_p
         L.nslct_abi_version.restype = ctypes.c_int
         for f in ("nslct_plan", "nslct_plan_ex", "nslct_exec", "nslct_exec_host", "nslct_plan_info",
-                  "nslct_plan_describe", "nslct_pass_ms", "nslct_destroy"):
+                  "nslct_plan_describe", "nslct_pass_ms", "nslct_destroy", "nslct_plan_slab",
+                  "nslct_exec_pass"):
             getattr(L, f).restype = ctypes.c_int
         _LIB = L
     return _LIB
@@ -194,6 +198,94 @@ class Plan:
         nw = ctypes.c_int(0)
         _check(lib().nslct_pass_ms(self._h, buf, 8, ctypes.byref(nw)))
         return [buf[i] for i in range(nw.value)]
+
+
+class SlabPlan(Plan):
+    """One n x n transform sharded as row slabs over nranks (nslct_plan_slab).
+
+    run(x_slab, exchange) executes the passes of this rank's slab of L = n/nranks rows;
+    exchange(send, recv) must perform the all-to-all of nranks blocks of L*L elements
+    between passes (torch_all_to_all() for NCCL/gloo process groups)."""
+
+    def __init__(self, n, M, nranks, rank, dtype="c64", dx=None, variant="HA", dispatch="reversible",
+                 h_fixed=None, device=None):
+        self.n, self.batch, self.dtype = int(n), 1, dtype
+        self.nranks, self.rank = int(nranks), int(rank)
+        self.L = self.n // self.nranks
+        a, ap = _abcd(M)
+        o = make_opts(dx, variant, dispatch, h_fixed, device, False)
+        h = ctypes.c_void_p()
+        _check(lib().nslct_plan_slab(ctypes.byref(h), self.n, ap, self.nranks, self.rank,
+                                     C64 if dtype == "c64" else C128, ctypes.byref(o)))
+        self._h = h
+        self.profile = False
+        self.n_passes = self.info()["n_passes"]
+
+    def exec_pass(self, k, x, out, stream=None):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream(x.device)
+        _check(lib().nslct_exec_pass(self._h, int(k), ctypes.c_void_p(x.data_ptr()),
+                                     ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(s.cuda_stream)))
+        return out
+
+    def run(self, x_slab, exchange, out=None, stream=None):
+        """x_slab: contiguous CUDA tensor [L, n] (this rank's rows).  Returns [L, n]."""
+        import torch
+        want = torch.complex64 if self.dtype == "c64" else torch.complex128
+        if not (x_slab.is_cuda and x_slab.dtype == want and x_slab.is_contiguous()
+                and tuple(x_slab.shape) == (self.L, self.n)):
+            raise ValueError("run expects a contiguous CUDA %s tensor of %d x %d" % (want, self.L, self.n))
+        send = torch.empty_like(x_slab)    # pass outputs: nranks row-blocks of [L][L]
+        recv = torch.empty_like(x_slab)    # all-to-all results: the next pass's input
+        out = torch.empty_like(x_slab) if out is None else out
+        cur = x_slab
+        for k in range(self.n_passes):
+            if k == self.n_passes - 1:
+                self.exec_pass(k, cur, out, stream)
+            else:
+                self.exec_pass(k, cur, send, stream)
+                exchange(send, recv)   # stream-ordered after pass k; recv was last read by pass k
+                cur = recv
+        return out
+
+
+def torch_all_to_all(group=None):
+    """exchange(send, recv) for SlabPlan.run over a torch.distributed process group
+    (NCCL on GPUs): nranks equal blocks of L*L elements."""
+    import torch.distributed as dist
+
+    def exchange(send, recv):
+        dist.all_to_all_single(recv.view(-1), send.view(-1), group=group)
+    return exchange
+
+
+def emulate_slabs(n, M, x_full, nranks, dtype="c64", **kw):
+    """Single-GPU emulation of the row-slab mode: nranks slab plans run one after another,
+    the all-to-all done by block copies on the device (no kernel waits on another).
+    x_full: CUDA tensor [n, n].  Returns the assembled [n, n] output."""
+    import torch
+    L = n // nranks
+    plans = [SlabPlan(n, M, nranks, r, dtype=dtype, **kw) for r in range(nranks)]
+    cur = [x_full[r * L:(r + 1) * L].contiguous() for r in range(nranks)]
+    outs = [torch.empty_like(c) for c in cur]
+    np_ = plans[0].n_passes
+    for k in range(np_):
+        last = (k == np_ - 1)
+        for r in range(nranks):
+            plans[r].exec_pass(k, cur[r], outs[r])
+        if last:
+            break
+        # all-to-all: block s of rank r's output -> block r of rank s's input
+        nxt = [torch.empty_like(c) for c in cur]
+        for r in range(nranks):
+            src = outs[r].view(nranks, L * L)
+            for s_ in range(nranks):
+                nxt[s_].view(nranks, L * L)[r].copy_(src[s_])
+        cur = nxt
+        outs = [torch.empty_like(c) for c in cur]
+    for p in plans:
+        p.close()
+    return torch.cat(outs, dim=0)
 
 
 def default_dx(n):

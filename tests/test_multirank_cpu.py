@@ -57,3 +57,48 @@ def test_bench_single_rank_defaults(monkeypatch):
     assert bench.dist_env() == (1, 0, 0)
     assert bench.max_over_ranks(3.0, 1) == 3.0
     assert bench.sum_over_ranks(32, 1) == 32.0
+
+
+def _slab_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_03688_b200.nslct import torch_all_to_all
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, L = 8, 8 // world
+        # a pass output on rank r: [n][L] with element (e, l_local) = code of
+        # (global element e, global line r*L + l_local)
+        e = torch.arange(n).view(n, 1)
+        l = torch.arange(L).view(1, L) + rank * L
+        send = (1000 * e + l).to(torch.complex64)
+        recv = torch.empty_like(send)
+        torch_all_to_all()(send, recv)
+        q.put((rank, recv.real.to(torch.int64).tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_all_to_all_layout_gloo():
+    """The slab protocol (include/nslct.h, nslct_plan_slab): after the all-to-all, rank s
+    holds block r of every rank r at offset r*L*L, i.e. its next-pass line q_local (global
+    s*L + q_local) with element m at (m / L)*L*L + q_local*L + m % L."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    n, L = 8, 4
+    for _ in range(world):
+        s, recv = q.get(timeout=10)
+        flat = [v for row in recv for v in row]
+        for ql in range(L):
+            for m in range(n):
+                # the value at that position is the pass output (element = s*L+ql, line = m)
+                assert flat[(m // L) * L * L + ql * L + m % L] == 1000 * (s * L + ql) + m
