@@ -129,7 +129,8 @@ typedef struct {
   int kind;                    /* 0 = B=0 (Eq. Intro20), 1 = form I (Eq. HA28), 2 = form II  */
   int variant;                 /* variant actually used (LC falls back to HA: PAPER.md:840)  */
   int lc_axis;                 /* 0 none, 1 = H=(h,0;0,0) (x), 2 = H=(0,0;0,h) (y)            */
-  int n_passes;                /* device passes per transform (5 for HA, 1 for B=0)           */
+  int n_passes;                /* device passes per transform: 5 (HA, LC with x-axis H),      */
+                               /* 3 (LC with y-axis H), 1 (B=0)               */
   double H[3], Bp[3], P2[3], P4[3];  /* form-I plan of M (form I) or of M^-1 (form II):
                                         (q11, q22, q12) of H, B', P2=B'^-1(A-I), P4=(D'-I)B'^-1 */
   double Q[5][3];              /* the executed chirps, application order:

@@ -650,16 +650,22 @@ __device__ __forceinline__ cpx<double> chirp_of<double>(uint64_t t, double scale
 struct Phase {
   uint64_t cA, cB, cC, cL, cE, cK;
 };
+// conj(chirp of t) = chirp of -t
+__device__ __forceinline__ Phase neg_phase(Phase p) {
+  return {0 - p.cA, 0 - p.cB, 0 - p.cC, 0 - p.cL, 0 - p.cE, 0 - p.cK};
+}
 
 // Multiply the thread's 16 elements (e = j + TL*k) of line l by the chirp.
 // Exact second-difference recurrence in k:  t_k = a0 + d0 k + dd k(k-1)/2 ...
 template <typename T, int TL, bool CONJ_IN, bool SCALE>
 __device__ __forceinline__ void apply_chirp(cpx<T> (&v)[16], const Phase& ph, uint64_t l, uint64_t j,
-                                            T scale, bool sign_only) {
-  if (sign_only) {
-    // Q = 0: only the centring checkerboard (-1)^(l+e); e = j + TL k with TL even, so the
-    // sign is the same for all 16 elements of the thread.
-    T s = (((l + j) & 1) ? T(-1) : T(1));
+                                            T scale, int sign_mode) {
+  if (sign_mode) {
+    // Q = 0: only a centring checkerboard: 1 = (-1)^(l+e) (both axes), 2 = (-1)^e (the
+    // element axis); e = j + TL k with TL even, so the sign is the same for all 16
+    // elements of the thread.
+    const uint64_t par = (sign_mode == 1) ? (l + j) : j;
+    T s = ((par & 1) ? T(-1) : T(1));
     if (SCALE) s *= scale;
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
@@ -702,7 +708,9 @@ struct PassArgs {
   long long n_lines;   // batch * N
   Phase ph;
   double scale;
-  int sign_only;       // the chirp is only the centring checkerboard (Q0/Q4 absent)
+  int sign_only;       // chirp a is only a checkerboard: 0 no, 1 (-1)^(l+e), 2 (-1)^e
+  Phase ph_b, ph_c;    // chirps b, c of the 3-FFT passes (MODE 4, 5: LC schedule)
+  int sign_c;          // chirp c sign-only mode (as sign_only)
   // Row-slab mode (one transform over P ranks; line_pass_kernel only).  Defaults give
   // the batched layout: L = N lines per image, offset 0, one chunk per line.
   int lines_per_img;   // L: lines of one image handled here (N, or N/P in slab mode)
@@ -715,44 +723,71 @@ struct PassArgs {
 // Exchanges used: MODE 0, 3: NX;  MODE 1, 2: 2 NX.
 template <int LOG2N, int MODE>
 struct PassInfo {
-  static constexpr int NX = FftInfo<LOG2N>::NX * ((MODE == 1 || MODE == 2) ? 2 : 1);
+  static constexpr int NX = FftInfo<LOG2N>::NX * ((MODE == 1 || MODE == 2) ? 2 : (MODE >= 4 ? 3 : 1));
 };
 
 template <typename T, int LOG2N, int MODE, class E, class TW>
-__device__ __forceinline__ void pass_body(cpx<T> (&v)[16], int j, const TW& tw,
-                                          const Phase& ph0, uint64_t l, T scale, bool sign_only,
-                                          const E& ex) {
-  // The inverse FFTs are left unnormalised; the whole 1/N^4 is applied in MODE 3 (K5).
+__device__ __forceinline__ void pass_body(cpx<T> (&v)[16], int j, const TW& tw, const PassArgs& a,
+                                          uint64_t l, const E& ex) {
+  // The inverse FFTs are left unnormalised; the whole 1/N^k is applied by the last pass
+  // (MODE 3 / MODE 5) through its scale.
   constexpr int TL = (1 << LOG2N) / 16;
   constexpr int NX = FftInfo<LOG2N>::NX;
-  if constexpr (MODE == 0) {
-    apply_chirp<T, TL, false, false>(v, ph0, l, (uint64_t)j, scale, sign_only);
+  const T scale = (T)a.scale;
+  const uint64_t jj = (uint64_t)j;
+  if constexpr (MODE == 0) {          // CM, FFT
+    apply_chirp<T, TL, false, false>(v, a.ph, l, jj, scale, a.sign_only);
     line_fft<T, LOG2N, 0>(v, j, tw, ex);
-  } else if constexpr (MODE == 1) {
+  } else if constexpr (MODE == 1) {   // FFT, CM, IFFT
     line_fft<T, LOG2N, 0>(v, j, tw, ex);
     // IFFT(CM X) = conj(FFT(conj(X) conj(CM))); conj(CM) is the chirp of -t
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
-    Phase ph = ph0;
-    ph.cA = 0 - ph.cA; ph.cB = 0 - ph.cB; ph.cC = 0 - ph.cC;
-    ph.cL = 0 - ph.cL; ph.cE = 0 - ph.cE; ph.cK = 0 - ph.cK;
-    apply_chirp<T, TL, false, false>(v, ph, l, (uint64_t)j, scale, false);
+    apply_chirp<T, TL, false, false>(v, neg_phase(a.ph), l, jj, scale, 0);
     line_fft<T, LOG2N, NX>(v, j, tw, ex);
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
-  } else if constexpr (MODE == 2) {
+  } else if constexpr (MODE == 2) {   // IFFT, CM, FFT
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
     line_fft<T, LOG2N, 0>(v, j, tw, ex);
-    apply_chirp<T, TL, true, false>(v, ph0, l, (uint64_t)j, scale, false);
+    apply_chirp<T, TL, true, false>(v, a.ph, l, jj, scale, 0);
     line_fft<T, LOG2N, NX>(v, j, tw, ex);
-  } else {
+  } else if constexpr (MODE == 3) {   // IFFT, CM (scaled)
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
     line_fft<T, LOG2N, 0>(v, j, tw, ex);
-    apply_chirp<T, TL, true, true>(v, ph0, l, (uint64_t)j, scale, sign_only);
+    apply_chirp<T, TL, true, true>(v, a.ph, l, jj, scale, a.sign_only);
+  } else if constexpr (MODE == 4) {   // CM a, FFT, CM b, IFFT, CM c, FFT  (LC form I, P1)
+    apply_chirp<T, TL, false, false>(v, a.ph, l, jj, scale, a.sign_only);
+    line_fft<T, LOG2N, 0>(v, j, tw, ex);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
+    apply_chirp<T, TL, false, false>(v, neg_phase(a.ph_b), l, jj, scale, 0);
+    line_fft<T, LOG2N, NX>(v, j, tw, ex);
+    apply_chirp<T, TL, true, false>(v, a.ph_c, l, jj, scale, a.sign_c);
+    line_fft<T, LOG2N, 2 * NX>(v, j, tw, ex);
+  } else {                            // IFFT, CM a, FFT, CM b, IFFT, CM c (scaled)  (LC form II, P3)
+    static_assert(MODE == 5, "pass mode");
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
+    line_fft<T, LOG2N, 0>(v, j, tw, ex);
+    apply_chirp<T, TL, true, false>(v, a.ph, l, jj, scale, 0);
+    line_fft<T, LOG2N, NX>(v, j, tw, ex);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = cconj(v[e]);
+    apply_chirp<T, TL, false, false>(v, neg_phase(a.ph_b), l, jj, scale, 0);
+    line_fft<T, LOG2N, 2 * NX>(v, j, tw, ex);
+    apply_chirp<T, TL, true, true>(v, a.ph_c, l, jj, scale, a.sign_c);
   }
 }
+
+// which passes read the user's row-major input / write the user's row-major output
+template <int MODE>
+struct ModeIO {
+  static constexpr bool kUserIn = (MODE == 0 || MODE == 4);
+  static constexpr bool kStraightOut = (MODE == 3 || MODE == 5);
+};
 
 template <int LOG2N>
 struct LineCfg {
@@ -805,10 +840,10 @@ line_pass_kernel(PassArgs a) {
 
   TwSet<T, LOG2N> tws;
   tws.load(tw, j);
-  pass_body<T, LOG2N, MODE>(v, j, tws, a.ph, (uint64_t)l, (T)a.scale, a.sign_only != 0, ExPad<T>{buf});
+  pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ExPad<T>{buf});
 
   cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * img_elems;
-  if constexpr (MODE == 3) {
+  if constexpr (ModeIO<MODE>::kStraightOut) {
     cpx<T>* dst = out + (long long)ll * N;
 #pragma unroll
     for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
@@ -905,7 +940,7 @@ __device__ __forceinline__ void load_group(cpx<T>* dst, const cpx<T>* src, uint6
   using Cfg = PipeCfg<LOG2N>;
   constexpr uint32_t LINE_BYTES = Cfg::N * sizeof(cpx<T>);
   mbar_expect_tx(bar, Cfg::G * LINE_BYTES);
-  if constexpr (MODE == 0) {
+  if constexpr (ModeIO<MODE>::kUserIn) {
 #pragma unroll
     for (int ll = 0; ll < Cfg::G; ++ll) bulk_g2s(dst + ll * Cfg::LS, src + ll * Cfg::N, LINE_BYTES, bar);
   } else {
@@ -980,7 +1015,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     const long long line0 = g * G;
     const int l = (int)((line0 + gl) % N);
     cpx<T> v[16];
-    if constexpr (MODE == 0) {   // the user's row-major input, lines staged LS apart
+    if constexpr (ModeIO<MODE>::kUserIn) {   // the user's row-major input, lines staged LS apart
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = sb[gl * LS + j + TL * e];
     } else {                     // pair-interleaved intermediate
@@ -1013,9 +1048,9 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     };
     const Prefetch pf{tid, b, counter, n_groups, stage + (b ^ 1) * BE, in, bar, s_next};
     const ExPad2<T, Prefetch> ex{xbuf + gl * LS, sb + gl * LS, &pf};
-    pass_body<T, LOG2N, MODE>(v, j, tws, a.ph, (uint64_t)l, (T)a.scale, a.sign_only != 0, ex);
+    pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ex);
 
-    if constexpr (MODE == 3) {
+    if constexpr (ModeIO<MODE>::kStraightOut) {
       cpx<T>* dst = out + (line0 + gl) * N + j;
 #pragma unroll
       for (int e = 0; e < 16; ++e) dst[TL * e] = v[e];

@@ -92,6 +92,8 @@ cudaError_t set_attr_pair() {
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
+constexpr int kModes = 6;   // pass modes 0..5 (kernels.cuh pass_body)
+
 template <typename T, int LOG2N>
 struct PipeRow {
   static void fill(pipe_fn* l, attr_fn* at) {
@@ -99,10 +101,14 @@ struct PipeRow {
     l[1] = launch_pipe<T, LOG2N, 1>;
     l[2] = launch_pipe<T, LOG2N, 2>;
     l[3] = launch_pipe<T, LOG2N, 3>;
+    l[4] = launch_pipe<T, LOG2N, 4>;
+    l[5] = launch_pipe<T, LOG2N, 5>;
     at[0] = set_attr_pipe<T, LOG2N, 0>;
     at[1] = set_attr_pipe<T, LOG2N, 1>;
     at[2] = set_attr_pipe<T, LOG2N, 2>;
     at[3] = set_attr_pipe<T, LOG2N, 3>;
+    at[4] = set_attr_pipe<T, LOG2N, 4>;
+    at[5] = set_attr_pipe<T, LOG2N, 5>;
   }
 };
 constexpr int kPipeMinLog = 10, kPipeMaxLog = 12;  // needs an even number of lines per group
@@ -114,10 +120,14 @@ struct Row {
     l[1] = launch_pass<T, LOG2N, 1>;
     l[2] = launch_pass<T, LOG2N, 2>;
     l[3] = launch_pass<T, LOG2N, 3>;
+    l[4] = launch_pass<T, LOG2N, 4>;
+    l[5] = launch_pass<T, LOG2N, 5>;
     at[0] = set_attr<T, LOG2N, 0>;
     at[1] = set_attr<T, LOG2N, 1>;
     at[2] = set_attr<T, LOG2N, 2>;
     at[3] = set_attr<T, LOG2N, 3>;
+    at[4] = set_attr<T, LOG2N, 4>;
+    at[5] = set_attr<T, LOG2N, 5>;
   }
 };
 
@@ -125,10 +135,10 @@ constexpr int kMinLog = 5, kMaxLog = 14;
 constexpr int kMaxLog128 = 13;  // c128 line buffer of 16384 would exceed shared memory
 
 struct Table {
-  launch_fn l[2][kMaxLog + 1][4] = {};
-  attr_fn at[2][kMaxLog + 1][4] = {};
-  pipe_fn lp[kMaxLog + 1][4] = {};   // c64 only
-  attr_fn atp[kMaxLog + 1][4] = {};
+  launch_fn l[2][kMaxLog + 1][kModes] = {};
+  attr_fn at[2][kMaxLog + 1][kModes] = {};
+  pipe_fn lp[kMaxLog + 1][kModes] = {};   // c64 only
+  attr_fn atp[kMaxLog + 1][kModes] = {};
   pipe_fn lpair[4] = {launch_pair<12, 0>, launch_pair<12, 1>, launch_pair<12, 2>, launch_pair<12, 3>};
   attr_fn atpair[4] = {set_attr_pair<12, 0>, set_attr_pair<12, 1>, set_attr_pair<12, 2>, set_attr_pair<12, 3>};
   Table() {
@@ -223,7 +233,8 @@ struct nslct_plan_s {
   void* h_in = nullptr;   // device staging for exec_host
   void* h_out = nullptr;
   PassArgs args[5];
-  int mode[5] = {0, 1, 2, 1, 3};
+  int n_passes = 5;
+  int mode[5] = {0, 1, 2, 1, 3};   // HA schedule; LC (y-axis H) uses 3 passes
   bool slab = false;   // row-slab plan (nslct_plan_slab)
   int nranks = 1, rank = 0;
   bool pipe = false;   // persistent TMA-pipelined kernels
@@ -287,6 +298,12 @@ nslct_status nslct_plan(nslct_plan_t* plan, int64_t n, const double abcd[16], in
   nslct_opts o;
   nslct_opts_default(&o);
   return nslct_plan_ex(plan, n, abcd, batch, dtype, &o);
+}
+
+// The chain's H is rank one along y, H = (0,0;0,h) (Eq. LC12 with the F_y form; LC plans
+// with that axis, or a FIXED_H plan given such an H): the 3-pass schedule applies.
+static bool lc_y(const nslct::Plan& p) {
+  return p.kind != 0 && p.H.q11 == 0.0 && p.H.q12 == 0.0 && p.H.q22 != 0.0;
 }
 
 static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double abcd[16], int64_t batch,
@@ -442,20 +459,57 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
     Poly P4 = chirp_poly(p.q_active[4] ? p.Q[4] : zero, dx, (int)n, true);
     const Phase ph[5] = {to_phase(P0, true), to_phase(P1, false), to_phase(P2, true),
                          to_phase(P3, false), to_phase(P4, true)};
-    // inverse FFTs are unnormalised; K5 applies 1/N^4 (two 2D inverses) at once
+    // inverse FFTs are unnormalised; the last pass applies 1/N^4 (two 2D inverses)
     const double sc[5] = {1.0, 1.0, 1.0, 1.0, invn * invn * invn * invn};
     const int sign_only[5] = {p.q_active[0] ? 0 : 1, 0, 0, 0, p.q_active[4] ? 0 : 1};
     for (int k = 0; k < 5; ++k) {
+      pl->args[k] = PassArgs{};
       pl->args[k].tw = pl->tw;
       pl->args[k].n_lines = batch * n;
       pl->args[k].ph = ph[k];
       pl->args[k].scale = sc[k];
       pl->args[k].sign_only = sign_only[k];
+    }
+    if (lc_y(p)) {
+      // LC-NsDLCT with H = (0,0;0,h) (Eq. LC12 with F_y): the 1D CC along y merges with
+      // the neighbouring y-axis FFTs, 3 passes.  S_x / S_y are the
+      // one-axis centring checkerboards left over when a 1D and a 2D DFT meet.
+      const uint64_t HALF = 1ull << 63;
+      Poly Pq1 = chirp_poly(p.Q[1], dw, (int)n, false);   // rank-1 y chirp: 1D freq grid
+      Poly Pq3 = chirp_poly(p.Q[3], dw, (int)n, false);   // rank-1 y chirp (form II)
+      Poly Psx2 = chirp_poly(p.Q[2], dx, (int)n, false);
+      Psx2.Li += HALF;                                      // S_x * CM(Q2)
+      const double inv3 = invn * invn * invn;               // W_y^-1 and one 2D W^-1
+      pl->n_passes = 3;
+      if (p.kind == 1) {
+        pl->mode[0] = 4; pl->mode[1] = 1; pl->mode[2] = 3;
+        PassArgs& a0 = pl->args[0];          // S_y, FFT_y, CM_wy(Q1), IFFT_y, S_x CM(Q2), FFT_y
+        a0.ph = Phase{};
+        a0.sign_only = 2;
+        a0.ph_b = to_phase(Pq1, true);
+        a0.ph_c = to_phase(Psx2, true);
+        a0.sign_c = 0;
+        pl->args[1].ph = to_phase(P3, false); // FFT_x, CM_w(Q3), IFFT_x
+        pl->args[2] = pl->args[4];            // IFFT_y, CM(Q4) S / N^3
+        pl->args[2].scale = inv3;
+      } else {
+        pl->mode[0] = 0; pl->mode[1] = 1; pl->mode[2] = 5;
+        // pass 0: S CM(Q0), FFT_y (as the HA K1); pass 1: FFT_x, CM_w(Q1), IFFT_x
+        PassArgs& a2 = pl->args[2];          // IFFT_y, S_x CM(Q2), FFT_y, CM_wy(Q3), IFFT_y, S_y / N^3
+        a2.ph = to_phase(Psx2, true);
+        a2.sign_only = 0;
+        a2.ph_b = to_phase(Pq3, true);
+        a2.ph_c = Phase{};
+        a2.sign_c = 2;
+        a2.scale = inv3;
+      }
+    }
+    for (int k = 0; k < 5; ++k) {
       pl->args[k].lines_per_img = (int)L;
       pl->args[k].line_offset = slab ? (int)(rank * L) : 0;
       pl->args[k].in_chunk = (slab && k > 0) ? (int)L : (int)n;
       pl->args[k].in_chunk_stride = (slab && k > 0) ? L * L : n * n;
-      if (slab) pl->args[k].n_lines = L;
+      pl->args[k].n_lines = slab ? L : batch * n;
     }
     {
       int sms = 0;
@@ -465,7 +519,7 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       pl->pipe = (!slab && ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
       // the line-pair kernel is an opt-in experiment (measured slower)
       const char* ypair = std::getenv("NSLCT_PAIR");
-      pl->pair = pl->pipe && lg == 12 && (ypair && ypair[0] == '1');
+      pl->pair = pl->pipe && lg == 12 && pl->n_passes == 5 && (ypair && ypair[0] == '1');
     }
     if (pl->pipe) {
       cudaError_t e = cudaMalloc(&pl->counters, 8 * sizeof(unsigned long long));
@@ -482,7 +536,7 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       }
     }
     if (result != NSLCT_OK) break;
-    for (int m = 0; m < 4 && pl->pipe; ++m) {
+    for (int m = 0; m < kModes && pl->pipe; ++m) {
       cudaError_t e = table().atp[lg][m]();
       if (e != cudaSuccess) {
         result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(pipe): ") + cudaGetErrorString(e));
@@ -490,7 +544,7 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       }
     }
     if (result != NSLCT_OK) break;
-    for (int m = 0; m < 4; ++m) {
+    for (int m = 0; m < kModes; ++m) {
       cudaError_t e = table().at[ti][lg][m]();
       if (e != cudaSuccess) {
         result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
@@ -544,23 +598,26 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
     return NSLCT_OK;
   }
   if (pl->pipe) CUDA_TRY(cudaMemsetAsync(pl->counters, 0, 5 * sizeof(unsigned long long), s));
-  // K1 in->S, K2 S->out, K3 out->S, K4 S->out, K5 out->out (straight pass, in place)
-  const void* src[5] = {in, pl->scratch, out, pl->scratch, out};
-  void* dst[5] = {pl->scratch, out, pl->scratch, out, out};
-  for (int k = 0; k < 5; ++k) {
+  // pass k writes the scratch (k even) or out (k odd); the last pass writes out in place.
+  // HA: K1 in->S, K2 S->out, K3 out->S, K4 S->out, K5 out->out; LC-y: in->S, S->out, out->out
+  const int np = pl->n_passes;
+  const void* src = in;
+  for (int k = 0; k < np; ++k) {
+    void* dst = (k == np - 1) ? out : ((k % 2 == 0) ? pl->scratch : out);
     if (ev) CUDA_TRY(cudaEventRecord(ev[k], s));
     PassArgs a = pl->args[k];
-    a.in = src[k];
-    a.out = dst[k];
+    a.in = src;
+    a.out = dst;
     if (pl->pair)
       CUDA_TRY(table().lpair[pl->mode[k]](a, s, pl->num_sms, pl->counters + k));
     else if (pl->pipe)
       CUDA_TRY(table().lp[pl->log2n][pl->mode[k]](a, s, pl->num_sms, pl->counters + k));
     else
       CUDA_TRY(table().l[ti][pl->log2n][pl->mode[k]](a, s));
+    src = dst;
   }
   if (ev) {
-    CUDA_TRY(cudaEventRecord(ev[5], s));
+    CUDA_TRY(cudaEventRecord(ev[np], s));
     ++pl->ev_used;
   }
   return NSLCT_OK;
@@ -572,8 +629,8 @@ nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* ou
   if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(NSLCT_E_ARG, "in/out must be 16-byte aligned");
   if (pl->p.kind == 0) return fail(NSLCT_E_ARG, "the B = 0 plan has a single pass: use nslct_exec");
-  if (pass < 0 || pass >= 5) return fail(NSLCT_E_ARG, "pass out of range");
-  if (pass < 4 && in == out) return fail(NSLCT_E_ARG, "transposing passes cannot run in place");
+  if (pass < 0 || pass >= pl->n_passes) return fail(NSLCT_E_ARG, "pass out of range");
+  if (pass < pl->n_passes - 1 && in == out) return fail(NSLCT_E_ARG, "transposing passes cannot run in place");
   DeviceGuard guard(pl->device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int ti = (pl->dtype == NSLCT_C64) ? 0 : 1;
@@ -613,7 +670,7 @@ static void describe(const nslct::Plan& p, double dx, nslct_plan_desc* d) {
   d->kind = p.kind;
   d->variant = p.variant;
   d->lc_axis = p.lc_axis;
-  d->n_passes = (p.kind == 0) ? 1 : 5;
+  d->n_passes = (p.kind == 0) ? 1 : lc_y(p) ? 3 : 5;
   auto put = [](double* o, const nslct::Sym& s) {
     o[0] = s.q11;
     o[1] = s.q22;
@@ -636,6 +693,7 @@ static void describe(const nslct::Plan& p, double dx, nslct_plan_desc* d) {
 nslct_status nslct_plan_info(nslct_plan_t pl, nslct_plan_desc* d) {
   if (!pl || !d) return fail(NSLCT_E_ARG, "null pointer");
   describe(pl->p, pl->dx, d);
+  if (pl->p.kind != 0) d->n_passes = pl->n_passes;
   return NSLCT_OK;
 }
 
@@ -663,7 +721,7 @@ nslct_status nslct_pass_ms(nslct_plan_t pl, float* ms, int capacity, int* n_writ
   if (!pl || !ms) return fail(NSLCT_E_ARG, "null pointer");
   if (!pl->profile || pl->ev_used == 0) return fail(NSLCT_E_ARG, "plan not profiled / no exec yet");
   DeviceGuard guard(pl->device);
-  const int np = (pl->p.kind == 0) ? 1 : 5;
+  const int np = (pl->p.kind == 0) ? 1 : pl->n_passes;
   if (capacity < np) return fail(NSLCT_E_ARG, "capacity too small");
   for (int k = 0; k < np; ++k) ms[k] = 0.0f;
   for (size_t i = 0; i < pl->ev_used; ++i) {

@@ -228,6 +228,70 @@ def test_lc_variant():
     assert me.rel_l2(G[0], ref) <= 1e-9
 
 
+def lc_matrix(seed, kind, axis):
+    """A G(rng) matrix whose LC plan (reversible dispatch) has the given form and axis."""
+    mr = np.random.default_rng(seed)
+    while True:
+        M = synth.random_symplectic(mr)
+        pl = opl.plan(M, variant="LC")
+        if pl["kind"] == kind and pl.get("axis") == axis:
+            return M, pl
+
+
+@pytest.mark.parametrize("kind", ["I", "II"])
+@pytest.mark.parametrize("n,dtype", [(32, "c128"), (256, "c128"), (512, "c64"), (1024, "c64"),
+                                     (2048, "c128"), (4096, "c64")])
+def test_lc_y_three_pass(kind, n, dtype):
+    """LC-NsDLCT with H = (0,0;0,h) runs as 3 device passes (the 1D CC
+    along y merges with its neighbouring y-axis FFTs); output = the oracle's LC chain."""
+    M, pl = lc_matrix(11, kind, "y")
+    mr, ir = synth.config_streams(300 + n)
+    b = 2 if n <= 2048 else 1
+    x = synth.iid_cn(ir, (b, n, n)).astype(NDT[dtype])
+    G, info = run_gpu(x, M, dtype, variant="LC")
+    assert info["n_passes"] == 3 and info["lc_axis"] == "y" and info["kind"] == kind
+    assert np.abs(info["h"] - pl["h"]).max() < 1e-9
+    for i in range(b):
+        ref, _ = op.nsdlct(x[i].astype(np.complex128), M, variant="LC", pl=pl)
+        err = me.rel_l2(G[i], ref)
+        assert err <= TOL[dtype], (kind, n, dtype, i, err)
+
+
+@pytest.mark.parametrize("kind", ["I", "II"])
+def test_lc_x_five_pass(kind):
+    """LC with H = (h,0;0,0) keeps the generic 5-pass schedule; parity vs the oracle LC."""
+    M, pl = lc_matrix(12, kind, "x")
+    x = synth.iid_cn(np.random.default_rng(4), (2, 256, 256))
+    G, info = run_gpu(x, M, "c128", variant="LC")
+    assert info["n_passes"] == 5 and info["lc_axis"] == "x"
+    for i in range(2):
+        ref, _ = op.nsdlct(x[i], M, variant="LC", pl=pl)
+        assert me.rel_l2(G[i], ref) <= 1e-10
+
+
+def test_lc_y_reversible_and_slab():
+    """LC 3-pass: exec(M^-1) exec(M) = I, and the slab form of the same plan (4 emulated
+    ranks, 3 passes + 2 exchanges) reproduces the single-GPU result."""
+    M, pl = lc_matrix(13, "I", "y")
+    n = 1024
+    x = synth.iid_cn(np.random.default_rng(5), (1, n, n)).astype(np.complex64)
+    xt = torch.from_numpy(x).to("cuda")
+    with nslct.Plan(n, M, 1, variant="LC") as p:
+        G = p.exec(xt)
+        assert p.info()["n_passes"] == 3
+    Minv = sy.inverse(M)
+    with nslct.Plan(n, Minv, 1, variant="LC") as pi:
+        back = pi.exec(G)
+    torch.cuda.synchronize()
+    rel = float(torch.linalg.vector_norm((back - xt).to(torch.complex128)) /
+                torch.linalg.vector_norm(xt.to(torch.complex128)))
+    assert rel < 1e-5, rel
+    Gs = nslct.emulate_slabs(n, M, xt[0], 4, "c64", variant="LC")
+    d = float(torch.linalg.vector_norm((Gs - G[0]).to(torch.complex128)) /
+              torch.linalg.vector_norm(G[0].to(torch.complex128)))
+    assert d < 1e-6, d
+
+
 def test_exact_special_cases():
     """P1: DFT matrix -> Eq. BasicDFT16 via numpy.fft; P3: identity -> bit-exact copy;
     P2: gyrator pi/2 -> twisted DFT."""
