@@ -24,8 +24,15 @@
 // an angle in [-pi, pi).  This keeps the phase error at the 2^-32 (c64) / 2^-53 (c128)
 // level at any N, where a naive fp32 phase would be off by 1e-3 at N = 8192.
 #pragma once
+#include <cuda.h>   // CUtensorMap (kernel parameter of the TMA tensor store)
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+// The persistent c64 kernels cache their twiddle powers in tensor memory (TwTmem);
+// -DNSLCT_NO_TMEM_TWIDDLES regenerates them from per-thread bases instead (TwSet).
+#ifndef NSLCT_NO_TMEM_TWIDDLES
+#define NSLCT_TMEM_TWIDDLES 1
+#endif
 
 namespace nslct {
 
@@ -322,6 +329,8 @@ struct TwSet {
     apply_twiddles<R>(u, w[S][b]);
   }
   template <int S>
+  __device__ __forceinline__ void prefetch() const {}
+  template <int S>
   __device__ __forceinline__ void load_stage(const cpx<T>* __restrict__ tw, int j) {
     if constexpr (S < Sh::NS) {
       constexpr int R = Sh::template R<S>(), Ns = Sh::template Ns<S>(), NB = 16 / R;
@@ -342,6 +351,10 @@ struct TwSet {
 // buf: this line's shared-memory buffer, padded index P(i) = i + (i >> 4).
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+// PW pad words per 16 elements: PW = 2 keeps every 16-element group 16-byte aligned, so
+// the first stage (which writes 16 contiguous outputs) can use 128-bit stores.
+template <int PW>
+__device__ __forceinline__ int padw(int i) { return i + PW * (i >> 4); }
 
 // Twiddle powers from shared-memory tables: stage S (>= 1) holds, for every residue
 // m = jp % Ns and r = 1..R-1, exp(-2 pi i m r / (Ns R)) at [S-offset + (r-1) Ns + m]
@@ -361,6 +374,8 @@ struct TwTab {
   }
   __host__ __device__ static constexpr int elems() { return off<Sh::NS>(); }
   const cpx<T>* tab;
+  template <int S>
+  __device__ __forceinline__ void prefetch() const {}
   template <int S, int R>
   __device__ __forceinline__ void apply(cpx<T>* u, int /*b*/, int jp) const {
     constexpr int Ns = Sh::template Ns<S>();
@@ -402,6 +417,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t ta, float (&f)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
+}
+__device__ __forceinline__ void tmem_ld16_async(uint32_t ta, float (&f)[32], int o) {
+  uint32_t v[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(ta)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) f[o + i] = __uint_as_float(v[i]);
 }
 __device__ __forceinline__ void tmem_st16(uint32_t ta, const float (&f)[16]) {
   asm volatile(
@@ -451,23 +477,26 @@ struct TwTmem {
       fill_stage<S + 1>(tw, j);
     }
   }
+  // Stage S's powers are loaded (tcgen05.ld, asynchronous) by the PREVIOUS stage just
+  // before its exchange barrier, so the TMEM latency hides behind the barrier and the
+  // shared-memory reads; apply() waits for them.
+  mutable float h[32];
+  template <int S>
+  __device__ __forceinline__ void prefetch() const {
+    if constexpr (S >= 1 && S < Sh::NS) {
+      constexpr int R = Sh::template R<S>();
+      tmem_ld16_async(ta + (uint32_t)((S - 1) * 32), h, 0);
+      if constexpr ((16 / R) * (R - 1) > 8) tmem_ld16_async(ta + (uint32_t)((S - 1) * 32 + 16), h, 16);
+    }
+  }
   template <int S, int R>
   __device__ __forceinline__ void apply(cpx<float>* u, int b, int /*jp*/) const {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     // complex index c = b*(R-1) + r-1 lives in columns 2c, 2c+1 of the stage block
-    float h[16];
-    tmem_ld16(ta + (uint32_t)((S - 1) * 32), h);           // complex 0..7
 #pragma unroll
     for (int r = 1; r < R; ++r) {
       const int c = b * (R - 1) + r - 1;
-      if (c < 8) u[r] = cmul(u[r], cpx<float>{h[2 * c], h[2 * c + 1]});
-    }
-    if ((16 / R) * (R - 1) > 8) {
-      tmem_ld16(ta + (uint32_t)((S - 1) * 32 + 16), h);    // complex 8..15
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        const int c = b * (R - 1) + r - 1;
-        if (c >= 8) u[r] = cmul(u[r], cpx<float>{h[2 * (c - 8)], h[2 * (c - 8) + 1]});
-      }
+      u[r] = cmul(u[r], cpx<float>{h[2 * c], h[2 * c + 1]});
     }
   }
 };
@@ -485,23 +514,29 @@ template <typename T>
 struct ExPad {
   static constexpr bool kDouble = false;
   static constexpr bool kPadded = true;
+  static constexpr int kPadW = 1;
   cpx<T>* buf;
+  template <int X>
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
   template <int X>
   __device__ __forceinline__ void after_barrier() const {}
   template <int X>
   __device__ __forceinline__ cpx<T>* b() const { return buf; }
   __device__ __forceinline__ int idx(int i) const { return pad16(i); }
 };
-template <typename T, class Hook>
+template <typename T, class Hook, int PW = 1>
 struct ExPad2 {   // two padded buffers used alternately: write, barrier, read
   static constexpr bool kDouble = true;
   static constexpr bool kPadded = true;
+  static constexpr int kPadW = PW;
   cpx<T>* buf0;   // used by exchanges 0, 2, 4, ...
   cpx<T>* buf1;   // used by exchanges 1, 3, ...
   const Hook* hook;
   template <int X>
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  template <int X>
   __device__ __forceinline__ cpx<T>* b() const { return (X & 1) ? buf1 : buf0; }
-  __device__ __forceinline__ int idx(int i) const { return pad16(i); }
+  __device__ __forceinline__ int idx(int i) const { return padw<PW>(i); }
   template <int X>
   __device__ __forceinline__ void after_barrier() const {
     if constexpr (X == 0) hook->run();
@@ -511,10 +546,13 @@ template <typename T, class Hook>
 struct ExSwz {   // two unpadded XOR-swizzled buffers used alternately (see above)
   static constexpr bool kDouble = true;
   static constexpr bool kPadded = false;
+  static constexpr int kPadW = 0;
   cpx<T>* buf0;   // exchanges 0, 2, ...
   cpx<T>* buf1;   // exchanges 1, 3, ...
   int c;          // per-line swizzle constant
   const Hook* hook;
+  template <int X>
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
   template <int X>
   __device__ __forceinline__ cpx<T>* b() const { return (X & 1) ? buf1 : buf0; }
   __device__ __forceinline__ int idx(int i) const { return i ^ (((i >> 4) + c) & 15); }
@@ -534,27 +572,30 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TW& tw, 
   constexpr bool LAST = (STAGE == NS - 1);
   constexpr int Ns = (STAGE < NFULL) ? (1 << (4 * STAGE)) : (1 << (4 * NFULL));
   cpx<T>* buf = ex.template b<X>();
-  // Padded layouts: pad16(i + k) = pad16(i) + k + k/16 whenever k is a multiple of 16,
+  // Padded layouts: pad(i + k) = pad(i) + k + PW k/16 whenever k is a multiple of 16,
   // or i is a multiple of 16 and k < 16 -- so one base per butterfly/thread plus
   // compile-time offsets (the compiler cannot prove j < TL by itself).
   constexpr bool FAST = E::kPadded && (TL % 16 == 0);
   constexpr bool FAST_SWZ = !E::kPadded && (TL % 16 == 0);
-  constexpr int WSTEP = (Ns >= 16) ? Ns + Ns / 16 : Ns;
-  constexpr int RSTEP = TL + TL / 16;
+  constexpr int PW = E::kPadW;
+  constexpr int WSTEP = (Ns >= 16) ? Ns + PW * Ns / 16 : Ns;
+  constexpr int RSTEP = TL + PW * TL / 16;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int jp = j + b * TL;
     cpx<T> u[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) u[r] = v[b + r * NB];
+#ifndef NSLCT_EXP_NOFP   // timing experiment only (tools/: wrong results): drop the FP work
     if constexpr (Ns > 1) tw.template apply<STAGE, R>(u, b, jp);
     dft<R>(u);
+#endif
 #pragma unroll
     for (int r = 0; r < R; ++r) v[b + r * NB] = u[r];
     if constexpr (!LAST) {
       const int idxD = (jp / Ns) * Ns * R + (jp % Ns);
       if constexpr (FAST) {
-        cpx<T>* wb = buf + pad16(idxD);
+        cpx<T>* wb = buf + padw<PW>(idxD);
 #pragma unroll
         for (int r = 0; r < R; ++r) wb[r * WSTEP] = u[r];
       } else if constexpr (FAST_SWZ) {
@@ -578,10 +619,11 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TW& tw, 
     }
   }
   if constexpr (!LAST) {
-    __syncthreads();
+    tw.template prefetch<STAGE + 1>();   // TMEM twiddles of the next stage (no-op otherwise)
+    ex.template sync<X>();
     ex.template after_barrier<X>();
     if constexpr (FAST) {
-      const cpx<T>* rb = buf + pad16(j);
+      const cpx<T>* rb = buf + padw<PW>(j);
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = rb[e * RSTEP];
     } else if constexpr (FAST_SWZ) {
@@ -867,12 +909,17 @@ line_pass_kernel(PassArgs a) {
 
 // ---------------------------------------------------------------------------------
 // Persistent, TMA-pipelined variant of the line pass (sm_100a).  One CTA per SM loops over
-// groups of G contiguous lines.  Each group is brought into shared memory by ONE bulk
-// async copy (cp.async.bulk, completion on an mbarrier) issued one iteration ahead, so HBM
-// reads overlap the FFT/chirp work of the previous group.  The staging buffer of the
-// current group is then reused, XOR-swizzled, as its FFT exchange buffer; two buffers
-// alternate.  Stores are issued from registers (straight) or through the swizzled
-// buffer (transposed) and drain while the next group computes.
+// groups of G contiguous lines (G*N = 8192 elements).  Loads AND stores are asynchronous
+// TMA operations, so the warps only compute:
+//  * each group arrives in shared memory by bulk copy (cp.async.bulk, mbarrier completion),
+//    issued one group ahead;
+//  * the result is written into shared memory in the output's layout and leaves by a TMA
+//    store (one bulk copy for straight output, a strided tensor store for the transposed
+//    intermediate layout) that drains while the next group computes.  Stores issued from
+//    registers stalled all 16 warps at the end of every group (+0.57 ms of 2.5 ms in K2).
+// Three buffers rotate: group k reads staging buffer k%3, exchanges through it and the
+// spare buffer (k+2)%3, and stages its output in the spare; buffer (k+1)%3 (the previous
+// group's output) is refilled with group k+1 once its store has been read out.
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -897,6 +944,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+// 4D tensor store from shared memory (box at coordinates c0..c3 of the tensor map)
+__device__ __forceinline__ void tensor_s2g_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                              int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -916,23 +984,28 @@ struct PipeCfg {
   static constexpr int THREADS = 512;
   static constexpr int G = THREADS / TL;                    // lines per group (>= 1)
   static constexpr int GROUP_ELEMS = G * N;                 // = 16 * THREADS = 8192
-  static constexpr int SWZ_STEP = (G >= 16) ? 1 : 16 / G;   // per-line swizzle offset
-  static constexpr int NBUF = 3;                            // 2 staging + 1 exchange
+  static constexpr int NBUF = 3;                            // rotating (see above)
   static constexpr int IL = 2;   // interleave of the intermediate layout (see below)
   // padded line stride of the exchange layout (index i + i/16): LS = 16/G (mod 16) so
-  // the G lines read together by the transposed store hit distinct banks
+  // the G lines read together hit distinct banks
   static constexpr int LS = N + N / 16 + ((G >= 16) ? 1 : 16 / G);
   static constexpr int BUF_ELEMS = ((G * LS + 15) / 16) * 16;   // >= G*N (TMA staging)
+  static constexpr int ROWS = N / IL;                           // output rows per group (transposed)
+  static constexpr int BOX_ROWS = ROWS < 256 ? ROWS : 256;      // tensor-store box height
   static_assert(G % IL == 0, "pipe kernels need an even number of lines per group");
 };
 // Intermediate layout between pipe passes ("pair-interleaved transposed"): element mu of
 // line lambda (lines as the NEXT pass reads them) lives at
 //     (lambda / IL) * IL*N + mu * IL + lambda % IL.
 // A consumer group of G lines is still one contiguous block (one bulk copy), and a
-// producer holding G lines writes G*IL-element contiguous segments (>= 32 B: full L2
-// sectors; 16-byte half-sector writes measured ~5x slower, tools/micro_bench.cu).
+// producer group of G lines owns, in each of the N/IL rows (lambda/IL), a G*IL-element
+// contiguous segment (>= 32 B: full L2 sectors; 16-byte half-sector writes measured ~5x
+// slower, tools/micro_bench.cu).  The producer stages [row][line][lambda % IL] in shared
+// memory and one tensor map (nslct.cu make_store_map) describes the strided rows:
+//   dim0 = G*IL*2 floats (the segment), dim1 = N/IL rows (stride IL*N elements),
+//   dim2 = N/G groups of an image (stride G*IL elements), dim3 = images (stride N*N).
 
-// One group into a staging buffer.  MODE 0 reads the user's row-major lines and lands
+// One group into a staging buffer.  MODE 0/4 read the user's row-major lines and land
 // line ll at ll*LS (LS = 16/G mod 16: the lanes of the G lines hit different banks);
 // other modes read one contiguous pair-interleaved block.
 template <typename T, int LOG2N, int MODE>
@@ -950,23 +1023,21 @@ __device__ __forceinline__ void load_group(cpx<T>* dst, const cpx<T>* src, uint6
 
 template <typename T, int LOG2N, int MODE>
 __global__ void __launch_bounds__(512, 1)
-line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counter) {
+line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counter,
+                      const __grid_constant__ CUtensorMap omap) {
   using Cfg = PipeCfg<LOG2N>;
-  constexpr int N = Cfg::N, TL = Cfg::TL, G = Cfg::G, THREADS = Cfg::THREADS;
+  constexpr int N = Cfg::N, TL = Cfg::TL, G = Cfg::G, IL = Cfg::IL;
   constexpr int GE = Cfg::GROUP_ELEMS;
   constexpr int BE = Cfg::BUF_ELEMS, LS = Cfg::LS;
-  constexpr uint32_t GROUP_BYTES = GE * sizeof(cpx<T>);
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  cpx<T>* stage = reinterpret_cast<cpx<T>*>(smem_raw);                       // buffers 0, 1
-  cpx<T>* xbuf = stage + 2 * BE;                                            // buffer 2
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 3 * BE * sizeof(cpx<T>));  // 2 mbarriers
-  long long* s_next = reinterpret_cast<long long*>(bar + 2);                // 2 slots
-  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(s_next + 2);              // TMEM base
+  cpx<T>* bufs = reinterpret_cast<cpx<T>*>(smem_raw);                             // 3 buffers
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 3 * BE * sizeof(cpx<T>));  // 3 mbarriers
+  long long* s_next = reinterpret_cast<long long*>(bar + 3);                      // 3 group slots
+  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(s_next + 3);                    // TMEM base
 
-  // Lines of a group are interleaved across lanes (line gl = tid % G): the lanes holding
-  // elements (i, i+1) of all G lines then form one contiguous G*IL-element segment of the
-  // pair-interleaved output, so the transposed store goes straight from registers, and
-  // the interleaved input is read without bank conflicts.
+  // Lines of a group are interleaved across lanes (line gl = tid % G): the G*IL-element
+  // output segments are then written to shared memory without bank conflicts, and the
+  // interleaved input is read without bank conflicts.
   const int tid = threadIdx.x;
   const int gl = tid % G;
   const int j = tid / G;
@@ -975,8 +1046,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
   cpx<T>* __restrict__ out = reinterpret_cast<cpx<T>*>(a.out);
 
 #ifdef NSLCT_TMEM_TWIDDLES
-  // this thread's twiddle powers, the same for every group, cached in TMEM (TwTmem);
-  // opt-in: measured ~2% slower than TwSet (fewer FP instructions, more moves)
+  // this thread's twiddle powers, the same for every group, cached in TMEM (TwTmem)
   const int warp = tid >> 5;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_taddr)));
@@ -995,22 +1065,34 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
 #endif
 
   // Groups are claimed in order from a global counter (not round-robin) so the groups
-  // in flight across the GPU stay a contiguous window: the 8*G-byte pieces of the
-  // transposed stores of neighbouring groups then meet in L2 and leave as full lines.
+  // in flight across the GPU stay a contiguous window: the segments of the transposed
+  // stores of neighbouring groups then meet in L2 and leave as full lines.  Thread 0
+  // claims, records the group index of buffer b in s_next[b] and arrives on bar[b]
+  // (release; the waiters' acquire makes the index visible).  Past the last group it
+  // arrives without a copy, so the waiters see the end marker.
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
     fence_mbar_init();
     const long long g0 = (long long)atomicAdd(counter, 1ull);
-    if (g0 < n_groups) load_group<T, LOG2N, MODE>(stage, in + g0 * GE, &bar[0]);
-    s_next[1] = g0;
+    s_next[0] = g0;
+    if (g0 < n_groups) {
+      load_group<T, LOG2N, MODE>(bufs, in + g0 * GE, &bar[0]);
+    } else {
+      mbar_arrive(&bar[0]);
+    }
   }
   __syncthreads();
-  long long g = s_next[1];
-  for (int k = 0; g < n_groups; ++k) {
-    const int b = k & 1;
-    cpx<T>* sb = stage + b * BE;
-    mbar_wait(&bar[b], (uint32_t)((k >> 1) & 1));
+  int bs = 0;   // staging buffer of group k = k % 3
+  for (int k = 0;; ++k) {
+    const int bn = (bs == 2) ? 0 : bs + 1;   // next group's staging (held group k-1's output)
+    const int bx = (bn == 2) ? 0 : bn + 1;   // spare: exchanges and this group's output
+    cpx<T>* sb = bufs + bs * BE;
+    cpx<T>* xb = bufs + bx * BE;
+    mbar_wait(&bar[bs], (uint32_t)((k / 3) & 1));
+    const long long g = s_next[bs];
+    if (g >= n_groups) break;
 
     const long long line0 = g * G;
     const int l = (int)((line0 + gl) % N);
@@ -1019,16 +1101,17 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = sb[gl * LS + j + TL * e];
     } else {                     // pair-interleaved intermediate
-      const cpx<T>* src = sb + (gl / Cfg::IL) * (Cfg::IL * N) + (gl % Cfg::IL);
+      const cpx<T>* src = sb + (gl / IL) * (IL * N) + (gl % IL);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = src[(j + TL * e) * Cfg::IL];
+      for (int e = 0; e < 16; ++e) v[e] = src[(j + TL * e) * IL];
     }
     // No barrier here: exchange 0 writes the spare buffer, so the staging buffer sb is
     // only overwritten (exchange 1) after exchange 0's barrier, which every thread
-    // reaches after reading its inputs.  That same barrier also proves iteration k-1 is
-    // finished everywhere, so the hook run right after it may refill buffer b^1.
+    // reaches after reading its inputs.  That barrier also proves group k-1 is finished
+    // everywhere, so the hook run right after it may refill buffer bn -- once the TMA
+    // store of group k-1's output (staged there) has been read out.
     struct Prefetch {
-      int tid, b;
+      int tid, bn;
       unsigned long long* counter;
       long long n_groups;
       cpx<T>* next_buf;
@@ -1038,365 +1121,54 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
       __device__ __forceinline__ void run() const {
         if (tid == 0) {   // claim and prefetch the next group
           const long long gn = (long long)atomicAdd(counter, 1ull);
+          s_next[bn] = gn;
+          bulk_wait_read0();
           if (gn < n_groups) {
             fence_proxy_async_smem();    // order the generic-proxy uses of the buffer before TMA
-            load_group<T, LOG2N, MODE>(next_buf, in + gn * GE, &bar[b ^ 1]);
+            load_group<T, LOG2N, MODE>(next_buf, in + gn * GE, &bar[bn]);
+          } else {
+            mbar_arrive(&bar[bn]);
           }
-          s_next[b] = gn;
         }
       }
     };
-    const Prefetch pf{tid, b, counter, n_groups, stage + (b ^ 1) * BE, in, bar, s_next};
-    const ExPad2<T, Prefetch> ex{xbuf + gl * LS, sb + gl * LS, &pf};
+    const Prefetch pf{tid, bn, counter, n_groups, bufs + bn * BE, in, bar, s_next};
+    const ExPad2<T, Prefetch> ex{xb + gl * LS, sb + gl * LS, &pf};
     pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ex);
 
+    // Output staging in the spare buffer: its last exchange use was read out before the
+    // last exchange barrier (the exchange count per pass is even, so the last one is sb).
     if constexpr (ModeIO<MODE>::kStraightOut) {
-      cpx<T>* dst = out + (line0 + gl) * N + j;
+      cpx<T>* o = xb + gl * N;   // the G lines, contiguous as in the output
 #pragma unroll
-      for (int e = 0; e < 16; ++e) dst[TL * e] = v[e];
+      for (int e = 0; e < 16; ++e) o[j + TL * e] = v[e];
     } else {
-      // pair-interleaved transposed store: element i = j + TL*e of line l0 + gl goes to
-      // (i / IL) * IL*N + (l0 + gl) * IL + i % IL of the output image.
-      const int l0 = (int)(line0 % N);
-      cpx<T>* dst = out + (line0 / N) * (long long)N * N + (long long)(j / Cfg::IL) * (Cfg::IL * N) +
-                    (l0 + gl) * Cfg::IL + (j % Cfg::IL);
+      // element i = j + TL e of line gl -> [i / IL][gl][i % IL]
+      cpx<T>* o = xb + (j / IL) * (G * IL) + gl * IL + (j % IL);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) dst[(long long)e * (TL / Cfg::IL) * (Cfg::IL * N)] = v[e];
+      for (int e = 0; e < 16; ++e) o[e * (TL / IL) * (G * IL)] = v[e];
     }
-    g = s_next[b];   // written by thread 0 before at least one later barrier
+    fence_proxy_async_smem();   // this thread's generic writes -> visible to the TMA store
+    __syncthreads();
+    if (tid == 0) {
+      if constexpr (ModeIO<MODE>::kStraightOut) {
+        bulk_s2g(out + line0 * N, xb, (uint32_t)(GE * sizeof(cpx<T>)));
+      } else {
+        const int gi = (int)(g % (N / G)), img = (int)(g / (N / G));
+#pragma unroll 1
+        for (int r = 0; r < Cfg::ROWS; r += Cfg::BOX_ROWS)
+          tensor_s2g_4d(&omap, xb + r * (G * IL), 0, r, gi, img);
+      }
+      bulk_commit();
+    }
+    bs = bn;
   }
+  if (tid == 0) bulk_wait0();
 #ifdef NSLCT_TMEM_TWIDDLES
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
 #endif
-}
-
-// ---------------------------------------------------------------------------------
-// Line-pair kernel (c64, N = 4096): the MIO-lean variant of the persistent pass.
-//
-// Shared-memory instructions issue at ~1 per 2 clocks per SM whatever their width
-// (tools/micro_smem.cu), so the exchanges are done with 128-bit accesses: thread j of a
-// 256-thread CTA holds element j + TL*e (e = 0..15) of BOTH lines of a 2-line group, and
-// the exchange buffer interleaves the two lines ([i][line], 16 B per index, XOR-swizzled
-// in 16-byte units).  Both lines share the thread's twiddles, which are precomputed once
-// per kernel into registers (2 stages x 15 powers).  The pair-interleaved transposed
-// store needs (line, i), (line, i+1) in one lane: one shuffle between lanes j and j^1
-// builds them, and every lane writes a 16-byte piece of a full 32-byte segment.
-// ---------------------------------------------------------------------------------
-template <int LOG2N>
-struct PairCfg {
-  static constexpr int N = 1 << LOG2N;
-  static constexpr int TL = N / 16;
-  static constexpr int THREADS = TL;          // one thread per element slot; both lines
-  static constexpr int G = 2;
-  static constexpr int GE = G * N;            // elements per group
-  static constexpr int BE = GE + 16;          // elements per buffer
-  static constexpr int NBUF = 3;              // 2 staging + 1 exchange
-  static constexpr int IL = 2;                // pair-interleaved intermediate layout
-  static constexpr int NS = (LOG2N + 3) / 4;  // stages
-  static constexpr int NX = NS - 1;           // exchanges per FFT
-  static_assert(LOG2N % 4 == 0 && TL >= 128 && TL <= 512, "pair kernel: radix-16 stages only");
-};
-
-struct __align__(16) cpx2f {
-  cpx<float> a, b;   // line 0, line 1
-};
-
-__device__ __forceinline__ void st_pair(cpx<float>* base_pairs, int unit, cpx<float> a, cpx<float> b) {
-  float4 v = make_float4(a.x, a.y, b.x, b.y);
-  reinterpret_cast<float4*>(base_pairs)[unit] = v;
-}
-__device__ __forceinline__ void ld_pair(const cpx<float>* base_pairs, int unit, cpx<float>& a, cpx<float>& b) {
-  const float4 v = reinterpret_cast<const float4*>(base_pairs)[unit];
-  a = {v.x, v.y};
-  b = {v.z, v.w};
-}
-
-template <int LOG2N>
-struct PairTw {   // both lines' twiddles w^r (r = 1..15) per stage, cached in TMEM (see TwTmem)
-  using C = PairCfg<LOG2N>;
-  uint32_t ta;
-  __device__ __forceinline__ void fill(const cpx<float>* __restrict__ tw, int j) const {
-#pragma unroll
-    for (int s = 1; s < C::NS; ++s) {
-      const int Ns = 1 << (4 * s);
-      const int k0 = (j % Ns) * (C::N / (Ns * 16));
-      float h0[16], h1[16];
-#pragma unroll
-      for (int r = 1; r < 16; ++r) {
-        const cpx<float> w = tw[k0 * r];
-        const int c = r - 1;
-        if (c < 8) {
-          h0[2 * c] = w.x;
-          h0[2 * c + 1] = w.y;
-        } else {
-          h1[2 * (c - 8)] = w.x;
-          h1[2 * (c - 8) + 1] = w.y;
-        }
-      }
-      h1[14] = 0.f;
-      h1[15] = 0.f;
-      tmem_st16(ta + (uint32_t)((s - 1) * 32), h0);
-      tmem_st16(ta + (uint32_t)((s - 1) * 32 + 16), h1);
-    }
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  }
-  template <int S>
-  __device__ __forceinline__ void apply2(cpx<float> (&v0)[16], cpx<float> (&v1)[16]) const {
-    float h[16];
-    tmem_ld16(ta + (uint32_t)((S - 1) * 32), h);
-#pragma unroll
-    for (int r = 1; r <= 8; ++r) {
-      const cpx<float> w{h[2 * (r - 1)], h[2 * (r - 1) + 1]};
-      v0[r] = cmul(v0[r], w);
-      v1[r] = cmul(v1[r], w);
-    }
-    tmem_ld16(ta + (uint32_t)((S - 1) * 32 + 16), h);
-#pragma unroll
-    for (int r = 9; r < 16; ++r) {
-      const cpx<float> w{h[2 * (r - 9)], h[2 * (r - 9) + 1]};
-      v0[r] = cmul(v0[r], w);
-      v1[r] = cmul(v1[r], w);
-    }
-  }
-};
-
-// Exchange of one line of the pair: buf holds [line 0: N][line 1: N], XOR swizzle of each
-// 16-element group (c = 0; all lanes of an access belong to one line).
-template <int LOG2N, int Ns>
-__device__ __forceinline__ void pair_store_line(cpx<float>* lb, int j, const cpx<float> (&u)[16]) {
-  const int idxD = (j / Ns) * Ns * 16 + (j % Ns);
-  if constexpr (Ns == 1) {
-    cpx<float>* wb = lb + idxD;
-    const int x = (idxD >> 4) & 15;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) wb[r ^ x] = u[r];
-  } else {
-    cpx<float>* wb = lb + (idxD & ~15);
-    const int y = idxD >> 4, lo = j & 15;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) wb[r * Ns + (lo ^ ((y + r * (Ns / 16)) & 15))] = u[r];
-  }
-}
-template <int LOG2N>
-__device__ __forceinline__ void pair_load_line(const cpx<float>* lb, int j, cpx<float> (&v)[16]) {
-  constexpr int TL = PairCfg<LOG2N>::TL;
-  const int y = j >> 4, lo = j & 15, hi = j & ~15;
-#pragma unroll
-  for (int e = 0; e < 16; ++e) v[e] = lb[TL * e + hi + (lo ^ ((y + (TL / 16) * e) & 15))];
-}
-
-// One radix-16 stage of both lines.  Line 0's exchange stores are issued before line 1's
-// butterfly is computed, and after the barrier line 0's loads come first, so in every
-// warp the shared-memory traffic of one line overlaps the FP work of the other.
-template <int LOG2N, int STAGE, int X, class Hook>
-__device__ __forceinline__ void pair_stage(cpx<float> (&v0)[16], cpx<float> (&v1)[16], int j,
-                                           const PairTw<LOG2N>& tw, cpx<float>* xb0, cpx<float>* xb1,
-                                           const Hook& hook) {
-  using C = PairCfg<LOG2N>;
-  constexpr int N = C::N;
-  constexpr int Ns = 1 << (4 * STAGE);
-  constexpr bool LAST = (STAGE == C::NS - 1);
-  if constexpr (STAGE > 0) tw.template apply2<STAGE>(v0, v1);
-  cpx<float>* buf = (X & 1) ? xb1 : xb0;
-  dft<16>(v0);
-  if constexpr (!LAST) pair_store_line<LOG2N, Ns>(buf, j, v0);
-  dft<16>(v1);
-  if constexpr (!LAST) {
-    pair_store_line<LOG2N, Ns>(buf + N, j, v1);
-    __syncthreads();
-    if constexpr (X == 0) hook.run();
-    pair_load_line<LOG2N>(buf, j, v0);
-    pair_load_line<LOG2N>(buf + N, j, v1);
-  }
-}
-
-template <int LOG2N, int STAGE, int X0, class Hook>
-__device__ __forceinline__ void pair_stages(cpx<float> (&v0)[16], cpx<float> (&v1)[16], int j,
-                                            const PairTw<LOG2N>& tw, cpx<float>* xb0, cpx<float>* xb1,
-                                            const Hook& hook) {
-  if constexpr (STAGE < PairCfg<LOG2N>::NS) {
-    pair_stage<LOG2N, STAGE, X0 + STAGE, Hook>(v0, v1, j, tw, xb0, xb1, hook);
-    pair_stages<LOG2N, STAGE + 1, X0, Hook>(v0, v1, j, tw, xb0, xb1, hook);
-  }
-}
-
-template <int LOG2N, int X0, class Hook>
-__device__ __forceinline__ void pair_fft(cpx<float> (&v0)[16], cpx<float> (&v1)[16], int j,
-                                         const PairTw<LOG2N>& tw, cpx<float>* xb0, cpx<float>* xb1,
-                                         const Hook& hook) {
-  pair_stages<LOG2N, 0, X0, Hook>(v0, v1, j, tw, xb0, xb1, hook);
-}
-
-template <int LOG2N, int MODE, class Hook>
-__device__ __forceinline__ void pair_body(cpx<float> (&v0)[16], cpx<float> (&v1)[16], int j,
-                                          const PairTw<LOG2N>& tw, cpx<float>* xb0, cpx<float>* xb1,
-                                          const Hook& hook, const Phase& ph0, uint64_t l, float scale,
-                                          bool sign_only) {
-  constexpr int TL = PairCfg<LOG2N>::TL;
-  constexpr int NX = PairCfg<LOG2N>::NX;
-  if constexpr (MODE == 0) {
-    apply_chirp<float, TL, false, false>(v0, ph0, l, (uint64_t)j, scale, sign_only);
-    apply_chirp<float, TL, false, false>(v1, ph0, l + 1, (uint64_t)j, scale, sign_only);
-    pair_fft<LOG2N, 0>(v0, v1, j, tw, xb0, xb1, hook);
-  } else if constexpr (MODE == 1) {
-    pair_fft<LOG2N, 0>(v0, v1, j, tw, xb0, xb1, hook);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      v0[e] = cconj(v0[e]);
-      v1[e] = cconj(v1[e]);
-    }
-    Phase ph = ph0;   // conj(chirp) = chirp of -t
-    ph.cA = 0 - ph.cA; ph.cB = 0 - ph.cB; ph.cC = 0 - ph.cC;
-    ph.cL = 0 - ph.cL; ph.cE = 0 - ph.cE; ph.cK = 0 - ph.cK;
-    apply_chirp<float, TL, false, false>(v0, ph, l, (uint64_t)j, scale, false);
-    apply_chirp<float, TL, false, false>(v1, ph, l + 1, (uint64_t)j, scale, false);
-    pair_fft<LOG2N, NX>(v0, v1, j, tw, xb0, xb1, hook);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      v0[e] = cconj(v0[e]);
-      v1[e] = cconj(v1[e]);
-    }
-  } else if constexpr (MODE == 2) {
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      v0[e] = cconj(v0[e]);
-      v1[e] = cconj(v1[e]);
-    }
-    pair_fft<LOG2N, 0>(v0, v1, j, tw, xb0, xb1, hook);
-    apply_chirp<float, TL, true, false>(v0, ph0, l, (uint64_t)j, scale, false);
-    apply_chirp<float, TL, true, false>(v1, ph0, l + 1, (uint64_t)j, scale, false);
-    pair_fft<LOG2N, NX>(v0, v1, j, tw, xb0, xb1, hook);
-  } else {
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      v0[e] = cconj(v0[e]);
-      v1[e] = cconj(v1[e]);
-    }
-    pair_fft<LOG2N, 0>(v0, v1, j, tw, xb0, xb1, hook);
-    apply_chirp<float, TL, true, true>(v0, ph0, l, (uint64_t)j, scale, sign_only);
-    apply_chirp<float, TL, true, true>(v1, ph0, l + 1, (uint64_t)j, scale, sign_only);
-  }
-}
-
-template <int LOG2N, int MODE>
-__global__ void __launch_bounds__(PairCfg<LOG2N>::THREADS, 1)
-line_pass_pair_kernel(PassArgs a, long long n_groups, unsigned long long* counter) {
-  using C = PairCfg<LOG2N>;
-  constexpr int N = C::N, TL = C::TL, GE = C::GE, BE = C::BE;
-  constexpr uint32_t GROUP_BYTES = GE * sizeof(cpx<float>);
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  cpx<float>* stage = reinterpret_cast<cpx<float>*>(smem_raw);                       // buffers 0, 1
-  cpx<float>* xbuf = stage + 2 * BE;                                                // buffer 2
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 3 * BE * sizeof(cpx<float>));
-  long long* s_next = reinterpret_cast<long long*>(bar + 2);
-  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(s_next + 2);
-
-  const int j = threadIdx.x;
-  const cpx<float>* __restrict__ tw = reinterpret_cast<const cpx<float>*>(a.tw);
-  const cpx<float>* __restrict__ in = reinterpret_cast<const cpx<float>*>(a.in);
-  cpx<float>* __restrict__ out = reinterpret_cast<cpx<float>*>(a.out);
-  const int warp = j >> 5;
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_taddr)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem_base = *s_taddr;
-  constexpr int WARPS = C::THREADS / 32;
-  constexpr int COLS = 512 / ((WARPS + 3) / 4);
-  const PairTw<LOG2N> tws{tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * COLS)};
-  tws.fill(tw, j);
-
-  if (j == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-    const long long g0 = (long long)atomicAdd(counter, 1ull);
-    if (g0 < n_groups) {
-      mbar_expect_tx(&bar[0], GROUP_BYTES);
-      bulk_g2s(stage, in + g0 * GE, GROUP_BYTES, &bar[0]);
-    }
-    s_next[1] = g0;
-  }
-  __syncthreads();
-  long long g = s_next[1];
-  for (int k = 0; g < n_groups; ++k) {
-    const int b = k & 1;
-    cpx<float>* sb = stage + b * BE;
-    mbar_wait(&bar[b], (uint32_t)((k >> 1) & 1));
-    const long long line0 = g * 2;
-    const int l = (int)(line0 % N);
-    cpx<float> v0[16], v1[16];
-    if constexpr (MODE == 0) {   // user's row-major lines, contiguous
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        v0[e] = sb[j + TL * e];
-        v1[e] = sb[N + j + TL * e];
-      }
-    } else {                     // pair-interleaved: element mu of line ll at 2 mu + ll
-#pragma unroll
-      for (int e = 0; e < 16; ++e) ld_pair(sb, j + TL * e, v0[e], v1[e]);
-    }
-    struct Prefetch {
-      int tid, b;
-      unsigned long long* counter;
-      long long n_groups;
-      cpx<float>* next_buf;
-      const cpx<float>* in;
-      uint64_t* bar;
-      long long* s_next;
-      __device__ __forceinline__ void run() const {
-        if (tid == 0) {
-          const long long gn = (long long)atomicAdd(counter, 1ull);
-          if (gn < n_groups) {
-            fence_proxy_async_smem();
-            mbar_expect_tx(&bar[b ^ 1], GROUP_BYTES);
-            bulk_g2s(next_buf, in + gn * GE, GROUP_BYTES, &bar[b ^ 1]);
-          }
-          s_next[b] = gn;
-        }
-      }
-    };
-    const Prefetch pf{j, b, counter, n_groups, stage + (b ^ 1) * BE, in, bar, s_next};
-    // exchange 0 uses the spare buffer, so the staging buffer is free only after its
-    // barrier (see line_pass_pipe_kernel)
-    pair_body<LOG2N, MODE>(v0, v1, j, tws, xbuf, sb, pf, a.ph, (uint64_t)l, (float)a.scale,
-                           a.sign_only != 0);
-
-    if constexpr (MODE == 3) {
-      cpx<float>* d0 = out + line0 * N + j;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        d0[TL * e] = v0[e];
-        d0[N + TL * e] = v1[e];
-      }
-    } else {
-      // element i = j + TL e of lines (l, l+1) -> pair-interleaved transposed output:
-      // (i/2)*2N + 2*line + i%2.  Lanes j, j^1 swap one value so that the even lane
-      // holds line l at (i, i+1) and the odd lane line l+1 at (i, i+1).
-      const bool odd = (j & 1) != 0;
-      cpx<float>* dst = out + (line0 / N) * (long long)N * N + (long long)(j >> 1) * (2 * N) + 2 * l +
-                        (odd ? 2 : 0);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const cpx<float> send = odd ? v0[e] : v1[e];
-        cpx<float> recv;
-        recv.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
-        recv.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
-        const cpx<float> lo = odd ? recv : v0[e];
-        const cpx<float> hi = odd ? v1[e] : recv;
-        *reinterpret_cast<float4*>(dst + (long long)e * (TL / 2) * (2 * N)) = make_float4(lo.x, lo.y, hi.x, hi.y);
-      }
-    }
-    g = s_next[b];
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
 }
 
 // ---------------------------------------------------------------------------------

@@ -1,5 +1,7 @@
 // C ABI of the B200 NsDLCT: plan / exec / exec_host / plan_info / pass_ms / destroy.
 // See include/nslct.h for the contract and kernels.cuh for the pass schedule.
+#include <cuda.h>
+#include <cudaTypedefs.h>   // PFN_cuTensorMapEncodeTiled (driver entry point, no -lcuda)
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -55,14 +57,15 @@ cudaError_t set_attr() {
 }
 
 // persistent TMA-pipelined variant: grid = #SMs (one CTA per SM)
-constexpr size_t kPipeExtra = 64;   // 2 mbarriers + 2 claimed-group slots
+constexpr size_t kPipeExtra = 64;   // 3 mbarriers + 3 claimed-group slots + TMEM base
 template <typename T, int LOG2N, int MODE>
-cudaError_t launch_pipe(const PassArgs& a, cudaStream_t s, int grid, unsigned long long* counter) {
+cudaError_t launch_pipe(const PassArgs& a, cudaStream_t s, int grid, unsigned long long* counter,
+                        const CUtensorMap& omap) {
   using Cfg = nslct::PipeCfg<LOG2N>;
   const size_t smem = (size_t)Cfg::NBUF * Cfg::BUF_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
   const long long n_groups = a.n_lines / Cfg::G;
   const long long g = n_groups < grid ? n_groups : grid;
-  nslct::line_pass_pipe_kernel<T, LOG2N, MODE><<<(unsigned)g, Cfg::THREADS, smem, s>>>(a, n_groups, counter);
+  nslct::line_pass_pipe_kernel<T, LOG2N, MODE><<<(unsigned)g, Cfg::THREADS, smem, s>>>(a, n_groups, counter, omap);
   return cudaGetLastError();
 }
 template <typename T, int LOG2N, int MODE>
@@ -72,24 +75,39 @@ cudaError_t set_attr_pipe() {
   return cudaFuncSetAttribute(nslct::line_pass_pipe_kernel<T, LOG2N, MODE>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
-typedef cudaError_t (*pipe_fn)(const PassArgs&, cudaStream_t, int, unsigned long long*);
+typedef cudaError_t (*pipe_fn)(const PassArgs&, cudaStream_t, int, unsigned long long*, const CUtensorMap&);
 
-// line-pair variant (c64, N = 4096): 256 threads, both lines of a group per thread
-template <int LOG2N, int MODE>
-cudaError_t launch_pair(const PassArgs& a, cudaStream_t s, int grid, unsigned long long* counter) {
-  using Cfg = nslct::PairCfg<LOG2N>;
-  const size_t smem = (size_t)Cfg::NBUF * Cfg::BE * sizeof(nslct::cpx<float>) + kPipeExtra;
-  const long long n_groups = a.n_lines / Cfg::G;
-  const long long g = n_groups < grid ? n_groups : grid;
-  nslct::line_pass_pair_kernel<LOG2N, MODE><<<(unsigned)g, Cfg::THREADS, smem, s>>>(a, n_groups, counter);
-  return cudaGetLastError();
+// cuTensorMapEncodeTiled through the runtime's driver entry point (resolved once)
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
 }
-template <int LOG2N, int MODE>
-cudaError_t set_attr_pair() {
-  using Cfg = nslct::PairCfg<LOG2N>;
-  const size_t smem = (size_t)Cfg::NBUF * Cfg::BE * sizeof(nslct::cpx<float>) + kPipeExtra;
-  return cudaFuncSetAttribute(nslct::line_pass_pair_kernel<LOG2N, MODE>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+
+// Tensor map of a pipe pass's transposed (pair-interleaved) output `out` of `images`
+// N x N complex64 images, as the kernel's TMA store sees it (kernels.cuh, PipeCfg):
+// dim0 = the G*IL-element segment (as 4G floats), dim1 = N/IL rows, dim2 = N/G groups,
+// dim3 = images.
+nslct_status make_store_map(CUtensorMap* m, void* out, int log2n, long long images) {
+  auto fn = encode_tiled();
+  if (!fn) return fail(NSLCT_E_CUDA, "cuTensorMapEncodeTiled entry point not available");
+  const cuuint64_t n = 1ull << log2n;
+  const cuuint64_t G = 8192 / n, IL = 2;
+  const cuuint64_t dims[4] = {2 * IL * G, n / IL, n / G, (cuuint64_t)images};
+  const cuuint64_t strides[3] = {IL * n * 8, IL * G * 8, n * n * 8};
+  const cuuint32_t box[4] = {(cuuint32_t)(2 * IL * G), (cuuint32_t)(n / IL < 256 ? n / IL : 256), 1, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NSLCT_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return NSLCT_OK;
 }
 
 constexpr int kModes = 6;   // pass modes 0..5 (kernels.cuh pass_body)
@@ -139,8 +157,6 @@ struct Table {
   attr_fn at[2][kMaxLog + 1][kModes] = {};
   pipe_fn lp[kMaxLog + 1][kModes] = {};   // c64 only
   attr_fn atp[kMaxLog + 1][kModes] = {};
-  pipe_fn lpair[4] = {launch_pair<12, 0>, launch_pair<12, 1>, launch_pair<12, 2>, launch_pair<12, 3>};
-  attr_fn atpair[4] = {set_attr_pair<12, 0>, set_attr_pair<12, 1>, set_attr_pair<12, 2>, set_attr_pair<12, 3>};
   Table() {
     PipeRow<float, 10>::fill(lp[10], atp[10]);
     PipeRow<float, 11>::fill(lp[11], atp[11]);
@@ -238,7 +254,6 @@ struct nslct_plan_s {
   bool slab = false;   // row-slab plan (nslct_plan_slab)
   int nranks = 1, rank = 0;
   bool pipe = false;   // persistent TMA-pipelined kernels
-  bool pair = false;   // ... in the line-pair variant (c64, N = 4096)
   unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
   int num_sms = 148;
   nslct::B0Args b0{};
@@ -517,9 +532,6 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
         pl->num_sms = sms;
       const char* np = std::getenv("NSLCT_NO_PIPE");
       pl->pipe = (!slab && ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
-      // the line-pair kernel is an opt-in experiment (measured slower)
-      const char* ypair = std::getenv("NSLCT_PAIR");
-      pl->pair = pl->pipe && lg == 12 && pl->n_passes == 5 && (ypair && ypair[0] == '1');
     }
     if (pl->pipe) {
       cudaError_t e = cudaMalloc(&pl->counters, 8 * sizeof(unsigned long long));
@@ -528,14 +540,6 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
         break;
       }
     }
-    for (int m = 0; m < 4 && pl->pair; ++m) {
-      cudaError_t e = table().atpair[m]();
-      if (e != cudaSuccess) {
-        result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(pair): ") + cudaGetErrorString(e));
-        break;
-      }
-    }
-    if (result != NSLCT_OK) break;
     for (int m = 0; m < kModes && pl->pipe; ++m) {
       cudaError_t e = table().atp[lg][m]();
       if (e != cudaSuccess) {
@@ -558,6 +562,19 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
     return result;
   }
   *plan = pl;
+  return NSLCT_OK;
+}
+
+// one pipe pass: the transposed passes get the tensor map of their output
+static nslct_status launch_pipe_pass(nslct_plan_t pl, int k, const PassArgs& a, cudaStream_t s) {
+  const int m = pl->mode[k];
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  if (!(m == 3 || m == 5)) {   // not a straight-output mode (kernels.cuh ModeIO)
+    nslct_status st = make_store_map(&map, a.out, pl->log2n, a.n_lines >> pl->log2n);
+    if (st != NSLCT_OK) return st;
+  }
+  CUDA_TRY(table().lp[pl->log2n][m](a, s, pl->num_sms, pl->counters + k, map));
   return NSLCT_OK;
 }
 
@@ -608,12 +625,12 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
     PassArgs a = pl->args[k];
     a.in = src;
     a.out = dst;
-    if (pl->pair)
-      CUDA_TRY(table().lpair[pl->mode[k]](a, s, pl->num_sms, pl->counters + k));
-    else if (pl->pipe)
-      CUDA_TRY(table().lp[pl->log2n][pl->mode[k]](a, s, pl->num_sms, pl->counters + k));
-    else
+    if (pl->pipe) {
+      nslct_status st = launch_pipe_pass(pl, k, a, s);
+      if (st != NSLCT_OK) return st;
+    } else {
       CUDA_TRY(table().l[ti][pl->log2n][pl->mode[k]](a, s));
+    }
     src = dst;
   }
   if (ev) {
@@ -639,10 +656,8 @@ nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* ou
   a.out = out;
   if (pl->pipe) {
     CUDA_TRY(cudaMemsetAsync(pl->counters + pass, 0, sizeof(unsigned long long), s));
-    if (pl->pair)
-      CUDA_TRY(table().lpair[pl->mode[pass]](a, s, pl->num_sms, pl->counters + pass));
-    else
-      CUDA_TRY(table().lp[pl->log2n][pl->mode[pass]](a, s, pl->num_sms, pl->counters + pass));
+    nslct_status st = launch_pipe_pass(pl, pass, a, s);
+    if (st != NSLCT_OK) return st;
   } else {
     CUDA_TRY(table().l[ti][pl->log2n][pl->mode[pass]](a, s));
   }
