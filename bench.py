@@ -223,13 +223,17 @@ def run_ours(args):
     n, batch, dtype, desc = CONFIGS[args.config]
     mr, _ = synth.config_streams(args.config)
     M = synth.random_symplectic(mr)                 # same matrix on every rank
+    if args.variant == "LC":   # the first G(rng) draw whose LC plan has a y-axis H (3 passes)
+        while nslct.nslct_plan_describe(n, M, variant="LC")["lc_axis"] != "y":
+            M = synth.random_symplectic(mr)
     if args.config == 5 and world > 1:
         return run_slab(args, n, M, dtype, desc, world, rank, local, dev)
     gen = torch.Generator(device=dev)
     gen.manual_seed(synth.SEED_BASE + 1000 * args.config + rank)
     x = torch.randn((batch, n, n), dtype=torch.complex64, device=dev, generator=gen)   # CN(0,1)
     out = torch.empty_like(x)
-    plan = nslct.Plan(n, M, batch, dtype=dtype, profile=True, device=local)
+    plan = nslct.Plan(n, M, batch, dtype=dtype, profile=True, device=local, schedule=args.schedule,
+                      variant=args.variant)
     info = plan.info()
     stream = torch.cuda.current_stream(dev)
 
@@ -237,6 +241,12 @@ def run_ours(args):
         if world > 1:
             torch.distributed.barrier()
 
+    # inputs + outputs smaller than 2x the 126 MB L2 (C2): flush L2 before every timed step
+    # (a 512 MiB memset outside the per-step events); larger workloads stream through HBM.
+    S = 8 if dtype == "c64" else 16
+    flush = None
+    if 2 * batch * n * n * S < 256 * 2 ** 20:
+        flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
         plan.exec(x, out, stream)
     torch.cuda.synchronize()
@@ -245,30 +255,47 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     clocks.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        plan.exec(x, out, stream)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.exec(x, out, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_local = e0.elapsed_time(e1) / args.steps
+    else:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            plan.exec(x, out, stream)
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms_local = sum(a.elapsed_time(b) for a, b in evs) / args.steps
     barrier()
     clk = clocks.stop()
-    ms_local = e0.elapsed_time(e1) / args.steps
     pass_ms = plan.pass_ms()
     ms = max_over_ranks(ms_local, world, dev)
     total_units = sum_over_ranks(batch, world, dev)
     value = total_units / (ms * 1e-3)
 
     # dominant kernel roofline: algorithmic bytes per launch = batch * 2 * N^2 * S
-    S = 8 if dtype == "c64" else 16
     ki = max(range(len(pass_ms)), key=lambda k: pass_ms[k])
     bytes_launch = batch * 2.0 * n * n * S
     peak, peak_src = peaks()
     achieved = bytes_launch / (pass_ms[ki] * 1e-3) / 1e9
     traffic, tr_kernel = traffic_from_profiles(args.config)
-    step_alg_bytes = info["n_passes"] * bytes_launch
-    names = ["K1 CM+FFT_y (transposed store)", "K2 FFT_x CM IFFT_x", "K3 IFFT_y CM FFT_y",
-             "K4 FFT_x CM IFFT_x", "K5 IFFT_y CM"] if info["n_passes"] == 5 else ["B0 gather"]
+    step_alg_bytes = info["n_launches"] * bytes_launch
+    if info["on_chip"]:
+        names = ["on-chip: all %d passes, image in shared memory" % info["n_passes"]]
+    elif info["n_passes"] == 5:
+        names = ["K1 CM+FFT_y (transposed store)", "K2 FFT_x CM IFFT_x", "K3 IFFT_y CM FFT_y",
+                 "K4 FFT_x CM IFFT_x", "K5 IFFT_y CM"]
+    elif info["n_passes"] == 3:
+        names = ["P1 (y lines)", "P2 FFT_x CM IFFT_x", "P3 (y lines)"]
+    else:
+        names = ["B0 gather"]
 
     # end-to-end through the public C API with host buffers (H2D + exec + D2H per step)
     e2e = None
@@ -290,7 +317,8 @@ def run_ours(args):
         plan.pass_ms()
         e2e = {"value": total_units / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(hin.numel() * 8),
                "d2h_bytes_per_step": int(hout.numel() * 8), "steps": nst,
-               "how": "nslct_exec_host: pinned host in -> device, 5 passes, device -> pinned host out, stream sync"}
+               "how": "nslct_exec_host: pinned host in -> device, %d launches, device -> pinned host out, "
+                      "stream sync" % info["n_launches"]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -305,9 +333,12 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-            "config": {"workload": desc, "n": n, "per_gpu_batch": batch, "global_batch": int(total_units),
+            "config": {"workload": desc + ("" if args.variant == "HA" else ", LC-NsDLCT variant"), "n": n,
+                       "variant": info["variant"], "per_gpu_batch": batch, "global_batch": int(total_units),
                        "plan_kind": info["kind"], "parallelism": "dp%d (independent images, no collective)" % world,
-                       "l2": "inputs 4 GiB/GPU >> 126 MB L2; no flush", "hbm_alg_bytes_per_step": step_alg_bytes},
+                       "l2": ("L2 flushed before every step (512 MiB memset outside the step events)" if flush is not None
+                              else "inputs %.2f GiB/GPU >> 126 MB L2; no flush" % (batch * n * n * S / 2 ** 30)),
+                       "schedule": "on-chip (1 launch)" if info["on_chip"] else "%d line passes" % info["n_passes"], "hbm_alg_bytes_per_step": step_alg_bytes},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": names[ki],
                          "alg_bytes_per_launch": bytes_launch, "launch_ms": pass_ms[ki],
@@ -317,7 +348,7 @@ def run_ours(args):
                          "pass_ms": pass_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": info["n_passes"] * args.steps,
+            "gpu_launches": info["n_launches"] * args.steps,
             "clocks": clk,
         }
         print(json.dumps(res))
@@ -390,6 +421,9 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--schedule", default="auto", choices=["auto", "line_passes", "on_chip"],
+                    help="on-chip kernel where available (auto) or one launch per pass")
+    ap.add_argument("--variant", default="HA", choices=["HA", "LC"], help="planner variant")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

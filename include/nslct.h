@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define NSLCT_ABI_VERSION 1
+#define NSLCT_ABI_VERSION 2
 
 typedef enum { NSLCT_C64 = 0, NSLCT_C128 = 1 } nslct_dtype;
 
@@ -72,8 +72,18 @@ typedef struct {
   double h_fixed[3];  /* (h11, h22, h12) for NSLCT_VARIANT_FIXED_H                      */
   int device;         /* CUDA device ordinal for the plan's buffers; -1 = current       */
   int profile;        /* 1: record per-pass CUDA events in nslct_exec (nslct_pass_ms)   */
-  int reserved[6];
+  int schedule;       /* NSLCT_SCHEDULE_*: how a batched plan's passes are launched      */
+  int reserved[5];
 } nslct_opts;
+/* schedules of a batched plan (all compute the same operator) */
+enum { NSLCT_SCHEDULE_AUTO = 0,        /* the on-chip kernel for N <= 64 (measured faster at
+                                          every batch size: tools/schedule_sweep.py,
+                                          DESIGN.md §6.8), else one launch per pass         */
+       NSLCT_SCHEDULE_LINE_PASSES = 1, /* always one launch per pass                        */
+       NSLCT_SCHEDULE_ON_CHIP = 2      /* the on-chip kernel wherever one exists: c64 N <= 256
+                                          (N = 256: 4-CTA cluster), c128 N <= 128 (N = 128:
+                                          4-CTA cluster); NSLCT_E_UNSUPPORTED_N otherwise     */
+};
 
 /* Fill *opts with the defaults (dx = sqrt(2 pi/N), HA, reversible, current device). */
 void nslct_opts_default(nslct_opts* opts);
@@ -141,6 +151,11 @@ typedef struct {
   double sym_residual;         /* max Eq. Intro12 residual of the input matrix                */
   double recomposition_residual; /* |product of stage matrices - M|_max                        */
   double dispatch_key;         /* s(M) of reading R7                                          */
+  int n_launches;              /* kernel launches per nslct_exec: 1 with on_chip, else
+                                  n_passes (0 from nslct_plan_describe: no device chosen)     */
+  int on_chip;                 /* 1: the whole transform runs in one kernel per image, the
+                                  image held in shared memory (see
+                                  NSLCT_SCHEDULE_*); nslct_exec_pass still runs line passes  */
 } nslct_plan_desc;
 
 nslct_status nslct_plan_info(nslct_plan_t plan, nslct_plan_desc* out);
@@ -154,7 +169,7 @@ nslct_status nslct_plan_describe(int64_t n, const double abcd[16], const nslct_o
 /* Per-pass device times (ms), averaged over every nslct_exec of a plan built with
  * opts.profile = 1 since the previous call (events recorded on the exec stream between
  * passes).  Synchronises on those events, then resets the average.  ms must hold
- * n_passes floats; *n_written receives n_passes. */
+ * n_launches floats; *n_written receives n_launches (one value for an on-chip plan). */
 nslct_status nslct_pass_ms(nslct_plan_t plan, float* ms, int capacity, int* n_written);
 
 /* Free the plan and everything it owns (device-synchronises its buffers). NULL is a no-op. */

@@ -1172,6 +1172,132 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
 }
 
 // ---------------------------------------------------------------------------------
+// Fully on-chip small-N transform.  One CTA -- or a thread-block
+// cluster of C CTAs sharing their shared memory (DSMEM) -- holds one image and runs every
+// pass of the schedule on it, so the image crosses HBM once each way instead of once per
+// pass.  CTA r of a cluster owns rows [r N/C, (r+1) N/C); a row pass works on the CTA's
+// own rows, a column pass on columns [r N/C, (r+1) N/C), reading and writing the column
+// elements in every CTA of the cluster.  The per-line work is pass_body(), with the same
+// PassArgs (chirps in global line/element indices) as the line-pass kernels.
+// ---------------------------------------------------------------------------------
+struct ImgArgs {
+  const void* in;
+  void* out;
+  const void* tw;
+  PassArgs pass[5];
+  int mode[5];
+  int n_passes;   // the passes alternate rows, columns, rows, ...
+};
+
+template <typename T, int LOG2N, int C>
+struct ImgCfg {
+  static constexpr int N = 1 << LOG2N;
+  static constexpr int TL = N / 16;                 // threads per line
+  static constexpr int ROWS = N / C;                // rows (and columns) owned by one CTA
+  static constexpr int THREADS = (ROWS * TL < 512) ? ROWS * TL : 512;
+  static constexpr int GR = THREADS / TL;           // lines per round (>= 32: see below)
+  static constexpr int ROUNDS = ROWS / GR;
+  // odd strides: with lines interleaved across lanes (line = tid % GR, GR >= 32) a warp
+  // touches 32 rows at one column (row pass) or 32 columns of one row (column pass),
+  // both conflict-free; the exchange buffers likewise
+  static constexpr int RS = N + 1;
+  static constexpr int LSX = N + N / 16 + 1;
+  static constexpr int IMG = ROWS * RS;
+  static constexpr int SCR = GR * LSX;
+  static constexpr size_t SMEM = (size_t)(IMG + SCR) * sizeof(cpx<T>);
+  static_assert(GR >= 32 && ROWS % GR == 0 && ROWS % TL == 0, "on-chip shape");
+};
+
+template <int C>
+__device__ __forceinline__ void img_sync() {
+  if constexpr (C == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
+}
+
+template <typename T, int LOG2N, int C, int MODE>
+__device__ __forceinline__ void img_pass(cpx<T>* img, cpx<T>* const (&rimg)[C], cpx<T>* scr, const TwSet<T, LOG2N>& tws,
+                                         const PassArgs& pa, bool rows, int rank, int gl, int j) {
+  using Cfg = ImgCfg<T, LOG2N, C>;
+  constexpr int TL = Cfg::TL, RS = Cfg::RS, ROWS = Cfg::ROWS;
+  constexpr int EPO = 16 / C;   // elements of a column per owning CTA: owner of slot e is e / EPO
+#pragma unroll 1
+  for (int r = 0; r < Cfg::ROUNDS; ++r) {
+    const int ll = r * Cfg::GR + gl;   // local line
+    const int l = rank * ROWS + ll;    // global line index (row or column)
+    cpx<T> v[16];
+    if (rows) {
+      const cpx<T>* p = img + ll * RS + j;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = p[TL * e];
+    } else {   // element i = j + TL e of column l: row i lives in CTA i / ROWS = e / EPO
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = rimg[e / EPO][(j + TL * (e % EPO)) * RS + l];
+    }
+    pass_body<T, LOG2N, MODE>(v, j, tws, pa, (uint64_t)l, ExPad<T>{scr + gl * Cfg::LSX});
+    if (rows) {
+      cpx<T>* p = img + ll * RS + j;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) p[TL * e] = v[e];
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) rimg[e / EPO][(j + TL * (e % EPO)) * RS + l] = v[e];
+    }
+  }
+}
+
+template <typename T, int LOG2N, int C>
+__global__ void __launch_bounds__(ImgCfg<T, LOG2N, C>::THREADS) image_kernel(ImgArgs a) {
+  using Cfg = ImgCfg<T, LOG2N, C>;
+  constexpr int N = Cfg::N, ROWS = Cfg::ROWS, RS = Cfg::RS, THREADS = Cfg::THREADS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cpx<T>* img = reinterpret_cast<cpx<T>*>(smem_raw);
+  cpx<T>* scr = img + Cfg::IMG;
+  const int tid = threadIdx.x;
+  const int gl = tid % Cfg::GR;
+  const int j = tid / Cfg::GR;
+  int rank = 0;
+  cpx<T>* rimg[C];
+  if constexpr (C == 1) {
+    rimg[0] = img;
+  } else {
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+#pragma unroll
+    for (int c = 0; c < C; ++c) {   // generic addresses of every CTA's image (DSMEM)
+      uint64_t ra;
+      asm volatile("mapa.u64 %0, %1, %2;" : "=l"(ra) : "l"(reinterpret_cast<uint64_t>(img)), "r"(c));
+      rimg[c] = reinterpret_cast<cpx<T>*>(ra);
+    }
+  }
+  const long long image = blockIdx.x / C;
+  const size_t off = (size_t)image * N * N + (size_t)rank * ROWS * N;
+  const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in) + off;
+#pragma unroll 4
+  for (int idx = tid; idx < ROWS * N; idx += THREADS) img[(idx / N) * RS + idx % N] = in[idx];
+  TwSet<T, LOG2N> tws;
+  tws.load(reinterpret_cast<const cpx<T>*>(a.tw), j);
+  img_sync<C>();
+#pragma unroll 1
+  for (int k = 0; k < a.n_passes; ++k) {
+    const bool rows = (k % 2) == 0;
+    switch (a.mode[k]) {
+      case 0: img_pass<T, LOG2N, C, 0>(img, rimg, scr, tws, a.pass[k], rows, rank, gl, j); break;
+      case 1: img_pass<T, LOG2N, C, 1>(img, rimg, scr, tws, a.pass[k], rows, rank, gl, j); break;
+      case 2: img_pass<T, LOG2N, C, 2>(img, rimg, scr, tws, a.pass[k], rows, rank, gl, j); break;
+      case 3: img_pass<T, LOG2N, C, 3>(img, rimg, scr, tws, a.pass[k], rows, rank, gl, j); break;
+      case 4: img_pass<T, LOG2N, C, 4>(img, rimg, scr, tws, a.pass[k], rows, rank, gl, j); break;
+      default: img_pass<T, LOG2N, C, 5>(img, rimg, scr, tws, a.pass[k], rows, rank, gl, j); break;
+    }
+    img_sync<C>();
+  }
+  cpx<T>* __restrict__ out = reinterpret_cast<cpx<T>*>(a.out) + off;
+#pragma unroll 4
+  for (int idx = tid; idx < ROWS * N; idx += THREADS) out[idx] = img[(idx / N) * RS + idx % N];
+}
+
+// ---------------------------------------------------------------------------------
 // B = 0: G[p,q] = sqrt(det D) chi(C D^T)[p,q] * bilinear(g)(p1, q1)   (Eq. Intro20,
 // Eq. BasicAffine12/16), p1 = d11 p + d21 q, q1 = d12 p + d22 q, taps outside -> 0.
 // Coordinates in fp64 without FMA contraction (same rounding as the plain formula).

@@ -152,12 +152,47 @@ struct Row {
 constexpr int kMinLog = 5, kMaxLog = 14;
 constexpr int kMaxLog128 = 13;  // c128 line buffer of 16384 would exceed shared memory
 
+// fully on-chip small-N variant (F2): one CTA (C = 1) or a C-CTA cluster per image
+typedef cudaError_t (*img_fn)(const nslct::ImgArgs&, cudaStream_t, long long);
+template <typename T, int LOG2N, int C>
+cudaError_t launch_img(const nslct::ImgArgs& a, cudaStream_t s, long long batch) {
+  using Cfg = nslct::ImgCfg<T, LOG2N, C>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(batch * C));
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (C > 1) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, nslct::image_kernel<T, LOG2N, C>, a);
+}
+template <typename T, int LOG2N, int C>
+cudaError_t set_attr_img() {
+  using Cfg = nslct::ImgCfg<T, LOG2N, C>;
+  return cudaFuncSetAttribute(nslct::image_kernel<T, LOG2N, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)Cfg::SMEM);
+}
+
 struct Table {
+  img_fn li[2][kMaxLog + 1] = {};   // on-chip kernels: c64 N <= 256, c128 N <= 128
+  attr_fn ati[2][kMaxLog + 1] = {};
   launch_fn l[2][kMaxLog + 1][kModes] = {};
   attr_fn at[2][kMaxLog + 1][kModes] = {};
   pipe_fn lp[kMaxLog + 1][kModes] = {};   // c64 only
   attr_fn atp[kMaxLog + 1][kModes] = {};
   Table() {
+    li[0][5] = launch_img<float, 5, 1>, ati[0][5] = set_attr_img<float, 5, 1>;
+    li[0][6] = launch_img<float, 6, 1>, ati[0][6] = set_attr_img<float, 6, 1>;
+    li[0][7] = launch_img<float, 7, 1>, ati[0][7] = set_attr_img<float, 7, 1>;
+    li[0][8] = launch_img<float, 8, 4>, ati[0][8] = set_attr_img<float, 8, 4>;
+    li[1][5] = launch_img<double, 5, 1>, ati[1][5] = set_attr_img<double, 5, 1>;
+    li[1][6] = launch_img<double, 6, 1>, ati[1][6] = set_attr_img<double, 6, 1>;
+    li[1][7] = launch_img<double, 7, 4>, ati[1][7] = set_attr_img<double, 7, 4>;
     PipeRow<float, 10>::fill(lp[10], atp[10]);
     PipeRow<float, 11>::fill(lp[11], atp[11]);
     PipeRow<float, 12>::fill(lp[12], atp[12]);
@@ -254,6 +289,7 @@ struct nslct_plan_s {
   bool slab = false;   // row-slab plan (nslct_plan_slab)
   int nranks = 1, rank = 0;
   bool pipe = false;   // persistent TMA-pipelined kernels
+  bool image = false;  // fully on-chip kernel (one launch per exec)
   unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
   int num_sms = 148;
   nslct::B0Args b0{};
@@ -347,7 +383,7 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
     nslct_opts_default(&o);
   if (dtype != NSLCT_C64 && dtype != NSLCT_C128) return fail(NSLCT_E_ARG, "bad dtype");
   if (batch < 1) return fail(NSLCT_E_ARG, "batch must be >= 1");
-  if (o.variant < 0 || o.variant > 2 || o.dispatch < 0 || o.dispatch > 1)
+  if (o.variant < 0 || o.variant > 2 || o.dispatch < 0 || o.dispatch > 1 || o.schedule < 0 || o.schedule > 2)
     return fail(NSLCT_E_ARG, "bad variant/dispatch option");
   int lg = 0;
   while ((int64_t(1) << lg) < n && lg < 62) ++lg;
@@ -532,6 +568,20 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
         pl->num_sms = sms;
       const char* np = std::getenv("NSLCT_NO_PIPE");
       pl->pipe = (!slab && ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
+      const bool have = !slab && table().li[ti][lg] != nullptr;
+      if (o.schedule == NSLCT_SCHEDULE_ON_CHIP && !have && pl->p.kind != 0) {
+        result = fail(NSLCT_E_UNSUPPORTED_N, "no on-chip kernel for this N / dtype (c64 N <= 256, c128 N <= 128)");
+        break;
+      }
+      // AUTO: on chip for N <= 64, where it beat the line passes at every batch size
+      pl->image = have && (o.schedule == NSLCT_SCHEDULE_ON_CHIP || (o.schedule == NSLCT_SCHEDULE_AUTO && lg <= 6));
+    }
+    if (pl->image) {
+      cudaError_t e = table().ati[ti][lg]();
+      if (e != cudaSuccess) {
+        result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(on-chip): ") + cudaGetErrorString(e));
+        break;
+      }
     }
     if (pl->pipe) {
       cudaError_t e = cudaMalloc(&pl->counters, 8 * sizeof(unsigned long long));
@@ -608,6 +658,24 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
     else
       nslct::b0_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(b);
     CUDA_TRY(cudaGetLastError());
+    if (ev) {
+      CUDA_TRY(cudaEventRecord(ev[1], s));
+      ++pl->ev_used;
+    }
+    return NSLCT_OK;
+  }
+  if (pl->image) {   // F2: every pass in one kernel, the image in shared memory
+    nslct::ImgArgs ia;
+    ia.in = in;
+    ia.out = out;
+    ia.tw = pl->tw;
+    for (int k = 0; k < 5; ++k) {
+      ia.pass[k] = pl->args[k];
+      ia.mode[k] = pl->mode[k];
+    }
+    ia.n_passes = pl->n_passes;
+    if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
+    CUDA_TRY(table().li[ti][pl->log2n](ia, s, pl->batch));
     if (ev) {
       CUDA_TRY(cudaEventRecord(ev[1], s));
       ++pl->ev_used;
@@ -709,6 +777,8 @@ nslct_status nslct_plan_info(nslct_plan_t pl, nslct_plan_desc* d) {
   if (!pl || !d) return fail(NSLCT_E_ARG, "null pointer");
   describe(pl->p, pl->dx, d);
   if (pl->p.kind != 0) d->n_passes = pl->n_passes;
+  d->on_chip = (pl->p.kind != 0 && pl->image) ? 1 : 0;
+  d->n_launches = (pl->p.kind == 0 || pl->image) ? 1 : pl->n_passes;
   return NSLCT_OK;
 }
 
@@ -722,7 +792,7 @@ nslct_status nslct_plan_describe(int64_t n, const double abcd[16], const nslct_o
   else
     nslct_opts_default(&o);
   if (n < 2) return fail(NSLCT_E_ARG, "n must be >= 2");
-  if (o.variant < 0 || o.variant > 2 || o.dispatch < 0 || o.dispatch > 1)
+  if (o.variant < 0 || o.variant > 2 || o.dispatch < 0 || o.dispatch > 1 || o.schedule < 0 || o.schedule > 2)
     return fail(NSLCT_E_ARG, "bad variant/dispatch option");
   std::string err;
   nslct::Plan p;
@@ -736,7 +806,7 @@ nslct_status nslct_pass_ms(nslct_plan_t pl, float* ms, int capacity, int* n_writ
   if (!pl || !ms) return fail(NSLCT_E_ARG, "null pointer");
   if (!pl->profile || pl->ev_used == 0) return fail(NSLCT_E_ARG, "plan not profiled / no exec yet");
   DeviceGuard guard(pl->device);
-  const int np = (pl->p.kind == 0) ? 1 : pl->n_passes;
+  const int np = (pl->p.kind == 0 || pl->image) ? 1 : pl->n_passes;
   if (capacity < np) return fail(NSLCT_E_ARG, "capacity too small");
   for (int k = 0; k < np; ++k) ms[k] = 0.0f;
   for (size_t i = 0; i < pl->ev_used; ++i) {

@@ -36,7 +36,7 @@ class NslctError(RuntimeError):
 class nslct_opts(ctypes.Structure):
     _fields_ = [("dx", ctypes.c_double), ("variant", ctypes.c_int), ("dispatch", ctypes.c_int),
                 ("h_fixed", ctypes.c_double * 3), ("device", ctypes.c_int), ("profile", ctypes.c_int),
-                ("reserved", ctypes.c_int * 6)]
+                ("schedule", ctypes.c_int), ("reserved", ctypes.c_int * 5)]
 
 
 class nslct_plan_desc(ctypes.Structure):
@@ -46,7 +46,7 @@ class nslct_plan_desc(ctypes.Structure):
                 ("P4", ctypes.c_double * 3), ("Q", (ctypes.c_double * 3) * 5),
                 ("dx", ctypes.c_double), ("objective", ctypes.c_double),
                 ("sym_residual", ctypes.c_double), ("recomposition_residual", ctypes.c_double),
-                ("dispatch_key", ctypes.c_double)]
+                ("dispatch_key", ctypes.c_double), ("n_launches", ctypes.c_int), ("on_chip", ctypes.c_int)]
 
 
 _LIB = None
@@ -93,7 +93,11 @@ def _abcd(M):
     return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
 
-def make_opts(dx=None, variant="HA", dispatch="reversible", h_fixed=None, device=None, profile=False):
+SCHEDULES = {"auto": 0, "line_passes": 1, "on_chip": 2}
+
+
+def make_opts(dx=None, variant="HA", dispatch="reversible", h_fixed=None, device=None, profile=False,
+              schedule="auto"):
     o = nslct_opts()
     lib().nslct_opts_default(ctypes.byref(o))
     o.dx = float(dx) if dx else 0.0
@@ -105,6 +109,7 @@ def make_opts(dx=None, variant="HA", dispatch="reversible", h_fixed=None, device
             o.h_fixed[i] = float(h_fixed[i])
     o.device = -1 if device is None else int(device)
     o.profile = 1 if profile else 0
+    o.schedule = SCHEDULES[schedule]
     return o
 
 
@@ -115,7 +120,7 @@ def _desc_dict(d):
                 h=np.array(list(d.H)), H=s(d.H), Bp=s(d.Bp), P2=s(d.P2), P4=s(d.P4),
                 Q=[s(d.Q[i]) for i in range(5)], dx=d.dx, objective=d.objective,
                 sym_residual=d.sym_residual, recomposition_residual=d.recomposition_residual,
-                dispatch_key=d.dispatch_key)
+                dispatch_key=d.dispatch_key, n_launches=d.n_launches, on_chip=bool(d.on_chip))
 
 
 def nslct_plan_describe(n, M, **kw):
@@ -131,11 +136,11 @@ class Plan:
     """RAII wrapper of nslct_plan_t.  exec() takes torch CUDA tensors (complex64/128)."""
 
     def __init__(self, n, M, batch, dtype="c64", dx=None, variant="HA", dispatch="reversible",
-                 h_fixed=None, device=None, profile=False):
+                 h_fixed=None, device=None, profile=False, schedule="auto"):
         self.n, self.batch = int(n), int(batch)
         self.dtype = dtype
         a, ap = _abcd(M)
-        o = make_opts(dx, variant, dispatch, h_fixed, device, profile)
+        o = make_opts(dx, variant, dispatch, h_fixed, device, profile, schedule)
         h = ctypes.c_void_p()
         _check(lib().nslct_plan_ex(ctypes.byref(h), self.n, ap, self.batch,
                                    C64 if dtype == "c64" else C128, ctypes.byref(o)))

@@ -50,10 +50,10 @@ def oracle(x, M, dx=None, variant="HA", policy="reversible", h=None):
     return G, pl
 
 
-def parity(x, M, dtype, variant="HA", policy="reversible", check_imgs=None):
+def parity(x, M, dtype, variant="HA", policy="reversible", check_imgs=None, schedule="auto"):
     """Run both sides with the oracle's H; return (max relL2 over checked images, plan)."""
     pl = opl.plan(M, variant=variant, policy=policy)
-    kw = dict(dispatch="formI" if policy == "formI" else "reversible")
+    kw = dict(dispatch="formI" if policy == "formI" else "reversible", schedule=schedule)
     if pl["kind"] != "B0":
         kw["h_fixed"] = pl["h"]
     G, info = run_gpu(x, M, dtype, **kw)
@@ -172,12 +172,44 @@ def test_config5_n16384_properties():
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 def test_all_sizes_random_matrix(n, dtype):
     """Every supported N (several tiles per line, both stage-radix tails) vs the oracle,
-    batch 3, both dispatch forms exercised across the sweep."""
+    batch 3, both dispatch forms exercised across the sweep; small N through both the
+    on-chip kernel (default) and the line passes."""
     mr, ir = synth.config_streams(100 + n)
     M = synth.random_symplectic(mr)
     x = synth.iid_cn(ir, (3, n, n)).astype(NDT[dtype])
     err, info, _ = parity(x, M, dtype, check_imgs=[0, 2])
     assert err <= TOL[dtype], (n, dtype, err)
+    small = n <= 64
+    assert info["on_chip"] == small and info["n_launches"] == (1 if small else 5)
+    if n <= (256 if dtype == "c64" else 128):   # the other schedule of this size
+        err, info, _ = parity(x, M, dtype, check_imgs=[0, 2], schedule="line_passes" if small else "on_chip")
+        assert info["on_chip"] != small and info["n_launches"] == (5 if small else 1)
+        assert err <= TOL[dtype], (n, dtype, "other schedule", err)
+
+
+@pytest.mark.parametrize("n,dtype", [(32, "c64"), (64, "c128"), (128, "c64"), (128, "c128"), (256, "c64")])
+@pytest.mark.parametrize("kind", ["I", "II"])
+def test_on_chip_forms_and_lc(n, dtype, kind):
+    """F2 on-chip kernel (one CTA, or a 4-CTA cluster exchanging columns through DSMEM):
+    HA in both forms and the 3-pass LC schedule vs the oracle, batch 5 (several clusters),
+    in place."""
+    mr, ir = synth.config_streams(400 + n)
+    while True:
+        M = synth.random_symplectic(mr)
+        if opl.plan(M)["kind"] == kind:
+            break
+    x = synth.iid_cn(ir, (5, n, n)).astype(NDT[dtype])
+    err, info, _ = parity(x, M, dtype, check_imgs=[0, 4], schedule="on_chip")
+    assert info["on_chip"] and err <= TOL[dtype], (n, dtype, kind, err)
+    Ml, pl = lc_matrix(21, kind, "y")
+    xt = torch.from_numpy(x).to("cuda")
+    with nslct.Plan(n, Ml, 5, dtype=dtype, variant="LC", schedule="on_chip") as p:
+        assert p.info()["on_chip"] and p.info()["n_passes"] == 3
+        p.exec(xt, out=xt)   # in place
+    G = xt.cpu().numpy()
+    for i in (0, 4):
+        ref, _ = op.nsdlct(x[i].astype(np.complex128), Ml, variant="LC", pl=pl)
+        assert me.rel_l2(G[i], ref) <= TOL[dtype], (n, dtype, kind, "LC", i)
 
 
 @pytest.mark.parametrize("n", [4096, 8192])
@@ -290,6 +322,14 @@ def test_lc_y_reversible_and_slab():
     d = float(torch.linalg.vector_norm((Gs - G[0]).to(torch.complex128)) /
               torch.linalg.vector_norm(G[0].to(torch.complex128)))
     assert d < 1e-6, d
+
+
+def test_schedule_errors():
+    """NSLCT_SCHEDULE_ON_CHIP where no on-chip kernel exists fails loudly."""
+    M = synth.random_symplectic(np.random.default_rng(3))
+    for n, dtype in ((512, "c64"), (256, "c128")):
+        with pytest.raises(nslct.NslctError):
+            nslct.Plan(n, M, 1, dtype=dtype, schedule="on_chip")
 
 
 def test_exact_special_cases():
