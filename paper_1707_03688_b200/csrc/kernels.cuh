@@ -318,6 +318,7 @@ struct FftShape {
 
 template <typename T, int LOG2N>
 struct TwSet {
+  static constexpr bool kFft64 = false;
   using Sh = FftShape<LOG2N>;
   static constexpr int NBMAX = 16 / Sh::template R<Sh::NS - 1>() > 1 ? 16 / Sh::template R<Sh::NS - 1>() : 1;
   cpx<T> w[Sh::NS][NBMAX];
@@ -363,6 +364,7 @@ __device__ __forceinline__ int padw(int i) { return i + PW * (i >> 4); }
 // which fill the tables once; it saves the 14 power-generation products per butterfly.
 template <typename T, int LOG2N>
 struct TwTab {
+  static constexpr bool kFft64 = false;
   using Sh = FftShape<LOG2N>;
   template <int S>
   __host__ __device__ static constexpr int off() {
@@ -441,6 +443,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t ta, const float (&f)[16]) {
 
 template <int LOG2N>
 struct TwTmem {
+  static constexpr bool kFft64 = false;
   using Sh = FftShape<LOG2N>;
   uint32_t ta;   // this thread's TMEM address: lane quadrant + its warp's column base
   // stage S (>= 1) uses columns (S-1)*32 .. +31: complex index b*(R-1) + (r-1)
@@ -500,6 +503,152 @@ struct TwTmem {
     }
   }
 };
+
+// ---------------------------------------------------------------------------------
+// 4096-point line FFT as 64 x 64 with tensor-memory quad exchanges (c64 pipe kernel).
+//
+// Same contract as line_fft: thread j (256 per line) holds x[j + 256 e], e = 0..15, in
+// and X[j + 256 e] out.  With p = j % 64, m = j / 64, n = n1 + 64 n2, k = k2 + 64 k1:
+//   step 1  Y[n1][k2]  = DFT64 over n2 of x[n1 + 64 n2]      (n1 = p, n2 = m + 4e)
+//   step 2  Y'[n1][k2] = W4096^(n1 k2) Y[n1][k2]
+//   step 3  X[k2 + 64 k1] = DFT64 over n1 of Y'[n1][k2]      (k2 = p, n1 = m + 4e)
+// Each DFT64 over an index r = m + 4e is a DFT16 over e in registers, the twiddle
+// W64^(m a), and a DFT4 over m ACROSS the four threads p + 64m.  Those four threads sit
+// in warps (p/16) + 4m at the same lane, i.e. on the same TMEM lane, so the DFT4 inputs
+// are exchanged through tensor memory (tcgen05.st / tcgen05.ld; thread m keeps outputs
+// a = m + 4i, which makes the output distribution equal the input one).  Only the
+// step 2 -> 3 transpose goes through shared memory: ONE exchange per FFT instead of the
+// Stockham kernel's two (shared-memory traffic was the floor of the 2-FFT passes,
+// DESIGN.md §6.6).  TMEM columns (512 per CTA): warp w keeps its constants in
+// [64 (w/4), +62) -- W64^(m a), a = 1..15, then W4096^(p k2) for its 16 k2 -- and the
+// quad exchanges alternate between two 128-column buffers at 256 and 384.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ void tmem_st8(uint32_t ta, float a0, float a1, float a2, float a3, float a4,
+                                         float a5, float a6, float a7) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
+               "r"(__float_as_uint(a0)), "r"(__float_as_uint(a1)), "r"(__float_as_uint(a2)),
+               "r"(__float_as_uint(a3)), "r"(__float_as_uint(a4)), "r"(__float_as_uint(a5)),
+               "r"(__float_as_uint(a6)), "r"(__float_as_uint(a7))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t ta, float (&f)[32]) {
+  uint32_t v[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(ta)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+}
+
+struct TwFft64 {
+  static constexpr bool kFft64 = true;
+  uint32_t tcol;   // lane quadrant << 16 | this warp's 64 constant columns
+  uint32_t xcol;   // lane quadrant << 16 | column 256 (two 128-column exchange buffers)
+  int m;           // j / 64 (warp-uniform)
+  int p;           // j % 64
+  int q;           // warp % 4: the quad's named barrier is 1 + q (128 threads)
+  // once per kernel: this thread's constants from the fp64-accurate table tw[k] = W4096^k
+  __device__ __forceinline__ void fill(const cpx<float>* __restrict__ tw) const {
+    float f[32];
+#pragma unroll
+    for (int a = 1; a < 16; ++a) {
+      const cpx<float> w = tw[(64 * m * a) & 4095];
+      f[2 * (a - 1)] = w.x;
+      f[2 * (a - 1) + 1] = w.y;
+    }
+    f[30] = f[31] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      tmem_st8(tcol + 8 * c, f[8 * c], f[8 * c + 1], f[8 * c + 2], f[8 * c + 3], f[8 * c + 4], f[8 * c + 5],
+               f[8 * c + 6], f[8 * c + 7]);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {   // r = i + 4b  <->  k2 = m + 4i + 16b
+      const int k2 = m + 4 * (r & 3) + 16 * (r >> 2);
+      const cpx<float> w = tw[(p * k2) & 4095];
+      f[2 * r] = w.x;
+      f[2 * r + 1] = w.y;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      tmem_st8(tcol + 32 + 8 * c, f[8 * c], f[8 * c + 1], f[8 * c + 2], f[8 * c + 3], f[8 * c + 4],
+               f[8 * c + 5], f[8 * c + 6], f[8 * c + 7]);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  template <int S>
+  __device__ __forceinline__ void prefetch() const {}
+  // v[a] *= W64^(m a)
+  __device__ __forceinline__ void twiddle64(cpx<float> (&v)[16]) const {
+    float h[32];
+    tmem_ld32(tcol, h);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int a = 1; a < 16; ++a) v[a] = cmul(v[a], cpx<float>{h[2 * (a - 1)], h[2 * (a - 1) + 1]});
+  }
+  // v[r] *= W4096^(p k2(r))
+  __device__ __forceinline__ void twiddle4096(cpx<float> (&v)[16]) const {
+    float h[32];
+    tmem_ld32(tcol + 32, h);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = cmul(v[r], cpx<float>{h[2 * r], h[2 * r + 1]});
+  }
+  // DFT4 over m across the quad: in v[a] = V_m[a]; out v[i + 4b] = sum_m' W4^(m' b) V_m'[m + 4i]
+  template <int B>
+  __device__ __forceinline__ void quad_dft4(cpx<float> (&v)[16]) const {
+    const uint32_t base = xcol + 128 * B;
+    // V[a] -> column (a % 4) * 32 + m * 8 + (a / 4) * 2: reader m' takes columns m' * 32 .. +31
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      tmem_st8(base + 32 * c + 8 * m, v[c].x, v[c].y, v[c + 4].x, v[c + 4].y, v[c + 8].x, v[c + 8].y,
+               v[c + 12].x, v[c + 12].y);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float h[32];
+    tmem_ld32(base + 32 * m, h);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      cpx<float> a0{h[2 * i], h[2 * i + 1]}, a1{h[8 + 2 * i], h[9 + 2 * i]};
+      cpx<float> a2{h[16 + 2 * i], h[17 + 2 * i]}, a3{h[24 + 2 * i], h[25 + 2 * i]};
+      dft4(a0, a1, a2, a3);
+      v[i] = a0;
+      v[i + 4] = a1;
+      v[i + 8] = a2;
+      v[i + 12] = a3;
+    }
+  }
+};
+
+// X = exchange index of this FFT's shared-memory transpose (ExPad2 buffer alternation)
+template <int X, class E>
+__device__ __forceinline__ void fft64x64(cpx<float> (&v)[16], const TwFft64& t, const E& ex) {
+  // step 1: DFT64 over n2 = m + 4e for n1 = p
+  dft<16>(v);
+  if (t.m != 0) t.twiddle64(v);
+  t.quad_dft4<0>(v);   // v[i + 4b] = Y[p][m + 4i + 16b]
+  // step 2: twiddle, transpose through shared memory: Y'[n1][k2] at k2 * 65 + n1
+  t.twiddle4096(v);
+  cpx<float>* buf = ex.template b<X>();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) buf[(t.m + 4 * (r & 3) + 16 * (r >> 2)) * 65 + t.p] = v[r];
+  ex.template sync<X>();
+  ex.template after_barrier<X>();
+  const cpx<float>* rb = buf + t.p * 65 + t.m;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] = rb[4 * e];   // Y'[m + 4e][p]
+  // step 3: DFT64 over n1 = m + 4e for k2 = p  ->  v[e] = X[p + 64 (m + 4e)] = X[j + 256 e]
+  dft<16>(v);
+  if (t.m != 0) t.twiddle64(v);
+  t.quad_dft4<1>(v);
+}
 
 // Exchange policies (how a stage hands its outputs to the next stage through shared
 // memory).  X is the compile-time index of the exchange within the pass.
@@ -586,10 +735,8 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TW& tw, 
     cpx<T> u[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) u[r] = v[b + r * NB];
-#ifndef NSLCT_EXP_NOFP   // timing experiment only (tools/: wrong results): drop the FP work
     if constexpr (Ns > 1) tw.template apply<STAGE, R>(u, b, jp);
     dft<R>(u);
-#endif
 #pragma unroll
     for (int r = 0; r < R; ++r) v[b + r * NB] = u[r];
     if constexpr (!LAST) {
@@ -660,8 +807,18 @@ struct FftInfo {
 // FFT of the thread's line; X0 = index of its first exchange within the pass.
 template <typename T, int LOG2N, int X0, class E, class TW>
 __device__ __forceinline__ void line_fft(cpx<T> (&v)[16], int j, const TW& tw, const E& ex) {
-  FftStages<T, LOG2N, 0, FftInfo<LOG2N>::NS, X0, E, TW>::run(v, j, tw, ex);
+  if constexpr (TW::kFft64) {
+    static_assert(LOG2N == 12, "the 64x64 FFT is for N = 4096");
+    fft64x64<X0>(v, tw, ex);
+  } else {
+    FftStages<T, LOG2N, 0, FftInfo<LOG2N>::NS, X0, E, TW>::run(v, j, tw, ex);
+  }
 }
+// shared-memory exchanges per line FFT
+template <int LOG2N, class TW>
+struct FftNX {
+  static constexpr int value = TW::kFft64 ? 1 : FftInfo<LOG2N>::NX;
+};
 
 // ---------------------------------------------------------------------------------
 // Chirp evaluation: exp(2 pi j t) * scale, t given in 64-bit fixed point (turns).
@@ -764,8 +921,8 @@ struct PassArgs {
 // The per-line work of one pass (registers v hold elements j + TL*e of line l).
 // Exchanges used: MODE 0, 3: NX;  MODE 1, 2: 2 NX.
 template <int LOG2N, int MODE>
-struct PassInfo {
-  static constexpr int NX = FftInfo<LOG2N>::NX * ((MODE == 1 || MODE == 2) ? 2 : (MODE >= 4 ? 3 : 1));
+struct PassInfo {   // line FFTs per pass
+  static constexpr int NFFT = (MODE == 1 || MODE == 2) ? 2 : (MODE >= 4 ? 3 : 1);
 };
 
 template <typename T, int LOG2N, int MODE, class E, class TW>
@@ -774,7 +931,7 @@ __device__ __forceinline__ void pass_body(cpx<T> (&v)[16], int j, const TW& tw, 
   // The inverse FFTs are left unnormalised; the whole 1/N^k is applied by the last pass
   // (MODE 3 / MODE 5) through its scale.
   constexpr int TL = (1 << LOG2N) / 16;
-  constexpr int NX = FftInfo<LOG2N>::NX;
+  constexpr int NX = FftNX<LOG2N, TW>::value;
   const T scale = (T)a.scale;
   const uint64_t jj = (uint64_t)j;
   if constexpr (MODE == 0) {          // CM, FFT
@@ -848,7 +1005,7 @@ __global__ void __launch_bounds__(LineCfg<LOG2N>::THREADS)
 line_pass_kernel(PassArgs a) {
   using Cfg = LineCfg<LOG2N>;
   constexpr int N = Cfg::N, TL = Cfg::TL, G = Cfg::G, LS = Cfg::LS, THREADS = Cfg::THREADS;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   cpx<T>* smem = reinterpret_cast<cpx<T>*>(smem_raw);
 
   const int tid = threadIdx.x;
@@ -1021,7 +1178,29 @@ __device__ __forceinline__ void load_group(cpx<T>* dst, const cpx<T>* src, uint6
   }
 }
 
-template <typename T, int LOG2N, int MODE>
+// The persistent kernels' TMEM-resident twiddles: the 64x64 FFT's constants at N = 4096
+// (NSLCT_FFT64), else the Stockham stage powers.  lanebase = TMEM base | lane quadrant.
+template <int LOG2N, bool F64>
+struct TwMaker {
+  using type = TwTmem<LOG2N>;
+  __device__ static type make(uint32_t lanebase, int warp, int j, const cpx<float>* __restrict__ tw) {
+    const type t{lanebase + (uint32_t)((warp >> 2) * 128)};
+    t.fill(tw, j);
+    return t;
+  }
+};
+template <int LOG2N>
+struct TwMaker<LOG2N, true> {
+  using type = TwFft64;
+  __device__ static type make(uint32_t lanebase, int warp, int j, const cpx<float>* __restrict__ tw) {
+    const type t{lanebase + (uint32_t)(64 * (warp >> 2)), lanebase + 256u, j / 64, j % 64, warp & 3};
+    t.fill(tw);
+    return t;
+  }
+};
+// F64: the 64x64 TMEM-exchange FFT at N = 4096 (parity-verified, measured 3% slower than
+// the Stockham kernel; selected at plan time by NSLCT_FFT64=1).
+template <typename T, int LOG2N, int MODE, bool F64 = false>
 __global__ void __launch_bounds__(512, 1)
 line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counter,
                       const __grid_constant__ CUtensorMap omap) {
@@ -1056,8 +1235,9 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *s_taddr;
-  const TwTmem<LOG2N> tws{tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128)};
-  tws.fill(tw, j);
+  static_assert(!F64 || LOG2N == 12, "the 64x64 FFT is for N = 4096");
+  using Maker = TwMaker<LOG2N, F64>;
+  const typename Maker::type tws = Maker::make(tmem_base + ((uint32_t)(32 * (warp & 3)) << 16), warp, j, tw);
 #else
   (void)s_taddr;
   TwSet<T, LOG2N> tws;   // this thread's twiddle bases, the same for every group
@@ -1084,13 +1264,19 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     }
   }
   __syncthreads();
-  int bs = 0;   // staging buffer of group k = k % 3
+  // Buffer roles: bs = staging of this group, bx = spare, bn = next group's staging (it
+  // held the previous group's output).  The output is staged in the buffer the last
+  // exchange did not use: the spare after an even number of exchanges, else the staging
+  // buffer (read out before exchange 0's barrier).
+  constexpr int NXP = FftNX<LOG2N, decltype(tws)>::value * PassInfo<LOG2N, MODE>::NFFT;
+  constexpr bool ODD = (NXP & 1) != 0;
+  int bs = 0, bx = 2, bn = 1;
+  uint32_t phases = 0;   // parity of the next completion of bar[0..2]
   for (int k = 0;; ++k) {
-    const int bn = (bs == 2) ? 0 : bs + 1;   // next group's staging (held group k-1's output)
-    const int bx = (bn == 2) ? 0 : bn + 1;   // spare: exchanges and this group's output
     cpx<T>* sb = bufs + bs * BE;
     cpx<T>* xb = bufs + bx * BE;
-    mbar_wait(&bar[bs], (uint32_t)((k / 3) & 1));
+    mbar_wait(&bar[bs], (phases >> bs) & 1u);
+    phases ^= 1u << bs;
     const long long g = s_next[bs];
     if (g >= n_groups) break;
 
@@ -1136,15 +1322,16 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     const ExPad2<T, Prefetch> ex{xb + gl * LS, sb + gl * LS, &pf};
     pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ex);
 
-    // Output staging in the spare buffer: its last exchange use was read out before the
-    // last exchange barrier (the exchange count per pass is even, so the last one is sb).
+    // Output staging (see above): the chosen buffer's last use was read out before the
+    // last exchange barrier.
+    cpx<T>* ob = ODD ? sb : xb;
     if constexpr (ModeIO<MODE>::kStraightOut) {
-      cpx<T>* o = xb + gl * N;   // the G lines, contiguous as in the output
+      cpx<T>* o = ob + gl * N;   // the G lines, contiguous as in the output
 #pragma unroll
       for (int e = 0; e < 16; ++e) o[j + TL * e] = v[e];
     } else {
       // element i = j + TL e of line gl -> [i / IL][gl][i % IL]
-      cpx<T>* o = xb + (j / IL) * (G * IL) + gl * IL + (j % IL);
+      cpx<T>* o = ob + (j / IL) * (G * IL) + gl * IL + (j % IL);
 #pragma unroll
       for (int e = 0; e < 16; ++e) o[e * (TL / IL) * (G * IL)] = v[e];
     }
@@ -1152,16 +1339,19 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     __syncthreads();
     if (tid == 0) {
       if constexpr (ModeIO<MODE>::kStraightOut) {
-        bulk_s2g(out + line0 * N, xb, (uint32_t)(GE * sizeof(cpx<T>)));
+        bulk_s2g(out + line0 * N, ob, (uint32_t)(GE * sizeof(cpx<T>)));
       } else {
         const int gi = (int)(g % (N / G)), img = (int)(g / (N / G));
 #pragma unroll 1
         for (int r = 0; r < Cfg::ROWS; r += Cfg::BOX_ROWS)
-          tensor_s2g_4d(&omap, xb + r * (G * IL), 0, r, gi, img);
+          tensor_s2g_4d(&omap, ob + r * (G * IL), 0, r, gi, img);
       }
       bulk_commit();
     }
-    bs = bn;
+    const int ob_i = ODD ? bs : bx, free_i = ODD ? bx : bs;
+    bs = bn;        // prefetched
+    bn = ob_i;      // refilled once its store has been read out
+    bx = free_i;
   }
   if (tid == 0) bulk_wait0();
 #ifdef NSLCT_TMEM_TWIDDLES
@@ -1252,7 +1442,7 @@ template <typename T, int LOG2N, int C>
 __global__ void __launch_bounds__(ImgCfg<T, LOG2N, C>::THREADS) image_kernel(ImgArgs a) {
   using Cfg = ImgCfg<T, LOG2N, C>;
   constexpr int N = Cfg::N, ROWS = Cfg::ROWS, RS = Cfg::RS, THREADS = Cfg::THREADS;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   cpx<T>* img = reinterpret_cast<cpx<T>*>(smem_raw);
   cpx<T>* scr = img + Cfg::IMG;
   const int tid = threadIdx.x;

@@ -58,21 +58,22 @@ cudaError_t set_attr() {
 
 // persistent TMA-pipelined variant: grid = #SMs (one CTA per SM)
 constexpr size_t kPipeExtra = 64;   // 3 mbarriers + 3 claimed-group slots + TMEM base
-template <typename T, int LOG2N, int MODE>
+template <typename T, int LOG2N, int MODE, bool F64 = false>
 cudaError_t launch_pipe(const PassArgs& a, cudaStream_t s, int grid, unsigned long long* counter,
                         const CUtensorMap& omap) {
   using Cfg = nslct::PipeCfg<LOG2N>;
   const size_t smem = (size_t)Cfg::NBUF * Cfg::BUF_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
   const long long n_groups = a.n_lines / Cfg::G;
   const long long g = n_groups < grid ? n_groups : grid;
-  nslct::line_pass_pipe_kernel<T, LOG2N, MODE><<<(unsigned)g, Cfg::THREADS, smem, s>>>(a, n_groups, counter, omap);
+  nslct::line_pass_pipe_kernel<T, LOG2N, MODE, F64><<<(unsigned)g, Cfg::THREADS, smem, s>>>(a, n_groups, counter,
+                                                                                           omap);
   return cudaGetLastError();
 }
-template <typename T, int LOG2N, int MODE>
+template <typename T, int LOG2N, int MODE, bool F64 = false>
 cudaError_t set_attr_pipe() {
   using Cfg = nslct::PipeCfg<LOG2N>;
   const size_t smem = (size_t)Cfg::NBUF * Cfg::BUF_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
-  return cudaFuncSetAttribute(nslct::line_pass_pipe_kernel<T, LOG2N, MODE>,
+  return cudaFuncSetAttribute(nslct::line_pass_pipe_kernel<T, LOG2N, MODE, F64>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 typedef cudaError_t (*pipe_fn)(const PassArgs&, cudaStream_t, int, unsigned long long*, const CUtensorMap&);
@@ -185,6 +186,12 @@ struct Table {
   attr_fn at[2][kMaxLog + 1][kModes] = {};
   pipe_fn lp[kMaxLog + 1][kModes] = {};   // c64 only
   attr_fn atp[kMaxLog + 1][kModes] = {};
+  pipe_fn lp64[kModes] = {launch_pipe<float, 12, 0, true>, launch_pipe<float, 12, 1, true>,
+                          launch_pipe<float, 12, 2, true>, launch_pipe<float, 12, 3, true>,
+                          launch_pipe<float, 12, 4, true>, launch_pipe<float, 12, 5, true>};
+  attr_fn atp64[kModes] = {set_attr_pipe<float, 12, 0, true>, set_attr_pipe<float, 12, 1, true>,
+                           set_attr_pipe<float, 12, 2, true>, set_attr_pipe<float, 12, 3, true>,
+                           set_attr_pipe<float, 12, 4, true>, set_attr_pipe<float, 12, 5, true>};
   Table() {
     li[0][5] = launch_img<float, 5, 1>, ati[0][5] = set_attr_img<float, 5, 1>;
     li[0][6] = launch_img<float, 6, 1>, ati[0][6] = set_attr_img<float, 6, 1>;
@@ -290,6 +297,7 @@ struct nslct_plan_s {
   int nranks = 1, rank = 0;
   bool pipe = false;   // persistent TMA-pipelined kernels
   bool image = false;  // fully on-chip kernel (one launch per exec)
+  bool fft64 = false;  // pipe kernels with the 64x64 TMEM-exchange FFT (N = 4096, opt-in)
   unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
   int num_sms = 148;
   nslct::B0Args b0{};
@@ -568,6 +576,8 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
         pl->num_sms = sms;
       const char* np = std::getenv("NSLCT_NO_PIPE");
       pl->pipe = (!slab && ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
+      const char* f64 = std::getenv("NSLCT_FFT64");
+      pl->fft64 = pl->pipe && lg == 12 && f64 && f64[0] == '1';
       const bool have = !slab && table().li[ti][lg] != nullptr;
       if (o.schedule == NSLCT_SCHEDULE_ON_CHIP && !have && pl->p.kind != 0) {
         result = fail(NSLCT_E_UNSUPPORTED_N, "no on-chip kernel for this N / dtype (c64 N <= 256, c128 N <= 128)");
@@ -591,7 +601,7 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       }
     }
     for (int m = 0; m < kModes && pl->pipe; ++m) {
-      cudaError_t e = table().atp[lg][m]();
+      cudaError_t e = pl->fft64 ? table().atp64[m]() : table().atp[lg][m]();
       if (e != cudaSuccess) {
         result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(pipe): ") + cudaGetErrorString(e));
         break;
@@ -624,7 +634,10 @@ static nslct_status launch_pipe_pass(nslct_plan_t pl, int k, const PassArgs& a, 
     nslct_status st = make_store_map(&map, a.out, pl->log2n, a.n_lines >> pl->log2n);
     if (st != NSLCT_OK) return st;
   }
-  CUDA_TRY(table().lp[pl->log2n][m](a, s, pl->num_sms, pl->counters + k, map));
+  if (pl->fft64)
+    CUDA_TRY(table().lp64[m](a, s, pl->num_sms, pl->counters + k, map));
+  else
+    CUDA_TRY(table().lp[pl->log2n][m](a, s, pl->num_sms, pl->counters + k, map));
   return NSLCT_OK;
 }
 

@@ -324,6 +324,26 @@ def test_lc_y_reversible_and_slab():
     assert d < 1e-6, d
 
 
+@pytest.mark.parametrize("kind", ["I", "II"])
+def test_fft64_variant(kind, monkeypatch):
+    """The opt-in 64x64 TMEM-exchange FFT (NSLCT_FFT64=1, N = 4096 pipe kernels): HA both
+    forms and the LC 3-pass schedule (odd exchange count per pass) vs the oracle."""
+    monkeypatch.setenv("NSLCT_FFT64", "1")
+    n = 4096
+    mr, ir = synth.config_streams(500)
+    while True:
+        M = synth.random_symplectic(mr)
+        if opl.plan(M)["kind"] == kind:
+            break
+    x = synth.iid_cn(ir, (2, n, n)).astype(np.complex64)
+    err, info, _ = parity(x, M, "c64", check_imgs=[1])
+    assert err <= TOL["c64"], (kind, err)
+    Ml, pl = lc_matrix(22, kind, "y")
+    G, info = run_gpu(x[:1], Ml, "c64", variant="LC")
+    ref, _ = op.nsdlct(x[0].astype(np.complex128), Ml, variant="LC", pl=pl)
+    assert info["n_passes"] == 3 and me.rel_l2(G[0], ref) <= TOL["c64"]
+
+
 def test_schedule_errors():
     """NSLCT_SCHEDULE_ON_CHIP where no on-chip kernel exists fails loudly."""
     M = synth.random_symplectic(np.random.default_rng(3))
