@@ -130,6 +130,7 @@ struct PipeRow {
     at[5] = set_attr_pipe<T, LOG2N, 5>;
   }
 };
+
 constexpr int kPipeMinLog = 10, kPipeMaxLog = 12;  // needs an even number of lines per group
 
 template <typename T, int LOG2N>
