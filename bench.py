@@ -155,6 +155,21 @@ def cpu_oracle_sample(x_img, M):
     return dt, cores
 
 
+def cpu_fft_sample(x_img, M):
+    """Time the plain CPU FFT-based decomposition (baselines/cpu_fft.py, fp64, scipy.fft on
+    every host core) on one image of the workload; the plan comes from the oracle planner."""
+    import numpy as np
+    from baselines import cpu_fft
+    from oracle import planner
+    cores = os.cpu_count()
+    pl = planner.plan(M)
+    g = np.asarray(x_img, np.complex128)
+    n = g.shape[-1]
+    t0 = time.perf_counter()
+    cpu_fft.transform(g, pl["chain"], math.sqrt(2.0 * math.pi / n), workers=cores)
+    return time.perf_counter() - t0, cores
+
+
 def run_reference(args):
     """Reference arm: the fp64 oracle, as it stands, on the host cores (rank 0 only).
 
@@ -321,11 +336,15 @@ def run_ours(args):
                       "stream sync" % info["n_launches"]}
 
     cpu = None
+    cpu_fft_line = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         img0 = x[0].cpu().numpy()
         dt, cores = cpu_oracle_sample(img0, M)
         cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": "1 of the %d %dx%d images of one step (image 0), fp64 dense-DFT O_plan" % (batch, n, n)}
+        dtf, coresf = cpu_fft_sample(img0, M)
+        cpu_fft_line = {"value": 1.0 / dtf, "unit": UNIT, "cores": coresf, "kind": "cpu_fft_decomposition",
+                        "sample": "image 0 of the step, fp64, scipy.fft (workers=%d): baselines/cpu_fft.py" % coresf}
 
     plan.close()
     if rank == 0:
@@ -347,6 +366,7 @@ def run_ours(args):
                          "step_frac_of_8TBs": step_alg_bytes / (ms * 1e-3) / 1e9 / 8000.0,
                          "pass_ms": pass_ms},
             "cpu_baseline": cpu,
+            "cpu_fft_baseline": cpu_fft_line,
             "e2e": e2e,
             "gpu_launches": info["n_launches"] * args.steps,
             "clocks": clk,
