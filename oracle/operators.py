@@ -176,6 +176,21 @@ def lc_chain(pl):
     return out
 
 
+def zero_pad(g, n_out):
+    """Zero-padding of the input to (N + dN) x (N + dN):
+    every sample keeps its centered coordinate (reading R1: array index m + floor(N/2)),
+    so sample m lands at index m + floor(N'/2); everything else is 0.  The padded field
+    is on the same spacing dx as the original."""
+    g = np.asarray(g, np.complex128)
+    n = g.shape[-1]
+    if n_out < n:
+        raise ValueError("n_out must be >= N")
+    off = n_out // 2 - n // 2
+    out = np.zeros(g.shape[:-2] + (n_out, n_out), np.complex128)
+    out[..., off:off + n, off:off + n] = g
+    return out
+
+
 def nsdlct(g, M, dx=None, variant="HA", policy="reversible", h_override=None, pl=None):
     """O_plan: the paper's NsDLCT of g for ABCD matrix M.
 

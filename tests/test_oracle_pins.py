@@ -448,3 +448,60 @@ def test_dispatch_pairs_opposite_forms():
     for a in (0.5, 2.5):
         G = synth.gyrator_matrix4(a)
         assert pl.dispatch_key(sy.inverse(G)) == -pl.dispatch_key(G) != 0.0
+
+
+# ---------------------------------------------------------------- zero-padding (row F3)
+@pytest.mark.parametrize("n,n_out", [(32, 45), (33, 48), (33, 33), (165, 215)])
+def test_f3_zero_pad_keeps_sample_positions(n, n_out):
+    """F3: the padded field is the same function sampled on
+    the larger centered grid, restricted to the original window -- checked against the
+    closed-form Gaussian sampled directly on both grids, for even and odd N and dN."""
+    dx = 0.3
+    K = np.array([[0.3 + 1.0j, 0.1], [0.1, -0.2 + 0.7j]])
+    gp = op.zero_pad(cf.gaussian(K, n, dx), n_out)
+    big = cf.gaussian(K, n_out, dx)
+    x = np.arange(n_out) - n_out // 2
+    inside = (x >= -(n // 2)) & (x <= (n - 1) - n // 2)
+    mask = np.outer(inside, inside)
+    assert np.array_equal(gp[mask], big[mask])
+    assert not np.any(gp[~mask])
+
+
+def test_f3_padding_removes_boundary_aliasing():
+    """F3 / experiment E3: when the output occupies more space than
+    the input window, the unpadded discrete operator aliases at the boundary; zero-padding
+    by dN brings it to the closed form (P7 Gaussian-beam law), on the same dx.  A wrong
+    padding offset or grid breaks the padded match."""
+    n = 48
+    dx = math.sqrt(2 * math.pi / n)
+    K = 1j * np.eye(2)                           # well-sampled Gaussian (P7 input)
+    r, _ = synth.config_streams(7)
+    for _ in range(3):                           # the third G(rng) draw spreads the
+        M = synth.random_symplectic(r)           # intermediate stages past the window
+    g = cf.gaussian(K, n, dx)
+    errs = []
+    for dn in (0, 16, 48):
+        n2 = n + dn
+        G, _ = op.nsdlct(op.zero_pad(g, n2), M, dx)
+        ref = cf.gaussian_lct(M, K, n2, dx)
+        errs.append(me.nmse(me.align_sign(G, ref), ref))
+    assert errs[0] > 1e-3, errs
+    assert errs[2] < 1e-6 and errs[2] < errs[1] < errs[0], errs
+
+
+@pytest.mark.parametrize("n", [6, 30, 33, 100])
+def test_f3_arbitrary_n_dft_and_unitarity(n):
+    """Arbitrary N (row F3): for even N the DFT matrix is exactly Eq. BasicDFT16 (the
+    Gauss-sum identity of P1, here against numpy.fft); for every N the chain is unitary
+    (P4) and reversible (P5)."""
+    r = rng(n)
+    g = r.standard_normal((n, n)) + 1j * r.standard_normal((n, n))
+    dx = math.sqrt(2 * math.pi / n)
+    if n % 2 == 0:
+        G, _ = op.nsdlct(g, synth.dft_matrix4(), dx)
+        assert me.rel_l2(G, dx * dx / (2j * math.pi) * cdft2(g)) < 1e-12
+    M = synth.random_symplectic(r)
+    G, _ = op.nsdlct(g, M, dx)
+    assert abs(np.sum(abs(G) ** 2) / np.sum(abs(g) ** 2) - 1) < 1e-12
+    back, _ = op.nsdlct(G, sy.inverse(M), dx)
+    assert me.rel_l2(back, g) < 1e-11
