@@ -105,10 +105,16 @@ nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16],
  * flight (the plan's scratch is shared).  Errors: E_ARG (null/misaligned), E_CUDA. */
 nslct_status nslct_exec(nslct_plan_t plan, const void* in, void* out, void* cuda_stream);
 
-/* Same transform from HOST memory: copies host_in -> device, runs nslct_exec, copies the
- * result back to host_out, all on cuda_stream, and synchronises that stream before it
- * returns.  host buffers [batch][n][n] complex (pinned memory gives full copy speed).
- * Device staging buffers are allocated on the first call and owned by the plan. */
+/* Same transform from HOST memory: copies host_in -> device, runs the passes, copies the
+ * result back to host_out, and returns only when host_out holds the result.  The batch
+ * runs as a pipeline of chunks of whole images (about 64 MiB each; NSLCT_HOST_CHUNK_MB
+ * overrides): the host->device copy of chunk i+1 (on a plan-owned copy stream), the
+ * passes of chunk i (on cuda_stream) and the device->host copy of chunk i-1 (a second
+ * plan-owned copy stream) overlap, so a large batch costs about one PCIe direction, not
+ * both plus the compute.  The copies start after the work already queued on cuda_stream.
+ * host buffers [batch][n][n] complex (pinned memory gives full copy speed and overlap).
+ * Device staging buffers, copy streams and events are created on the first call and
+ * owned by the plan.  Errors: E_ARG (null pointers, slab plan), E_CUDA, E_OOM. */
 nslct_status nslct_exec_host(nslct_plan_t plan, const void* host_in, void* host_out,
                              void* cuda_stream);
 

@@ -291,6 +291,8 @@ struct nslct_plan_s {
   void* scratch = nullptr;
   void* h_in = nullptr;   // device staging for exec_host
   void* h_out = nullptr;
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;   // exec_host copy streams (H2D, D2H)
+  std::vector<cudaEvent_t> cev;                     // exec_host: 2 events per chunk + 1
   PassArgs args[5];
   int n_passes = 5;
   int mode[5] = {0, 1, 2, 1, 3};   // HA schedule; LC (y-axis H) uses 3 passes
@@ -330,6 +332,10 @@ void free_plan(nslct_plan_s* pl) {
   if (pl->counters) cudaFree(pl->counters);
   if (pl->h_in) cudaFree(pl->h_in);
   if (pl->h_out) cudaFree(pl->h_out);
+  if (pl->cs_in) cudaStreamDestroy(pl->cs_in);
+  if (pl->cs_out) cudaStreamDestroy(pl->cs_out);
+  for (auto e : pl->cev)
+    if (e) cudaEventDestroy(e);
   for (auto& set : pl->ev)
     for (auto& e : set.e)
       if (e) cudaEventDestroy(e);
@@ -642,17 +648,12 @@ static nslct_status launch_pipe_pass(nslct_plan_t pl, int k, const PassArgs& a, 
   return NSLCT_OK;
 }
 
-nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream) {
-  if (!pl) return fail(NSLCT_E_ARG, "null plan");
-  if (!in || !out) return fail(NSLCT_E_ARG, "null in/out pointer");
-  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
-    return fail(NSLCT_E_ARG, "in/out must be 16-byte aligned");
-  if (pl->slab) return fail(NSLCT_E_ARG, "slab plans run pass by pass: nslct_exec_pass");
-  DeviceGuard guard(pl->device);
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+// The passes of `nimg` consecutive images (in/out/scratch already offset to the first).
+static nslct_status run_images(nslct_plan_t pl, const void* in, void* out, void* scratch, int64_t nimg,
+                               cudaStream_t s, bool profile) {
   const int ti = (pl->dtype == NSLCT_C64) ? 0 : 1;
   cudaEvent_t* ev = nullptr;
-  if (pl->profile) {
+  if (profile) {
     if (pl->ev_used == pl->ev.size()) {
       nslct_plan_s::EvSet set{};
       for (auto& e : set.e) CUDA_TRY(cudaEventCreate(&e));
@@ -664,6 +665,7 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
     nslct::B0Args b = pl->b0;
     b.in = in;
     b.out = out;
+    b.total = nimg * pl->n * pl->n;
     const long long blocks = (b.total + 255) / 256;
     if (in == out) return fail(NSLCT_E_ARG, "the B = 0 gather cannot run in place");
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
@@ -685,11 +687,12 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
     ia.tw = pl->tw;
     for (int k = 0; k < 5; ++k) {
       ia.pass[k] = pl->args[k];
+      ia.pass[k].n_lines = nimg * pl->n;
       ia.mode[k] = pl->mode[k];
     }
     ia.n_passes = pl->n_passes;
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
-    CUDA_TRY(table().li[ti][pl->log2n](ia, s, pl->batch));
+    CUDA_TRY(table().li[ti][pl->log2n](ia, s, nimg));
     if (ev) {
       CUDA_TRY(cudaEventRecord(ev[1], s));
       ++pl->ev_used;
@@ -702,11 +705,12 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
   const int np = pl->n_passes;
   const void* src = in;
   for (int k = 0; k < np; ++k) {
-    void* dst = (k == np - 1) ? out : ((k % 2 == 0) ? pl->scratch : out);
+    void* dst = (k == np - 1) ? out : ((k % 2 == 0) ? scratch : out);
     if (ev) CUDA_TRY(cudaEventRecord(ev[k], s));
     PassArgs a = pl->args[k];
     a.in = src;
     a.out = dst;
+    a.n_lines = nimg * pl->n;
     if (pl->pipe) {
       nslct_status st = launch_pipe_pass(pl, k, a, s);
       if (st != NSLCT_OK) return st;
@@ -720,6 +724,17 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
     ++pl->ev_used;
   }
   return NSLCT_OK;
+}
+
+nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream) {
+  if (!pl) return fail(NSLCT_E_ARG, "null plan");
+  if (!in || !out) return fail(NSLCT_E_ARG, "null in/out pointer");
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(NSLCT_E_ARG, "in/out must be 16-byte aligned");
+  if (pl->slab) return fail(NSLCT_E_ARG, "slab plans run pass by pass: nslct_exec_pass");
+  DeviceGuard guard(pl->device);
+  return run_images(pl, in, out, pl->scratch, pl->batch, reinterpret_cast<cudaStream_t>(stream),
+                    pl->profile != 0);
 }
 
 nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* out, void* stream) {
@@ -746,6 +761,21 @@ nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* ou
   return NSLCT_OK;
 }
 
+// Images per exec_host chunk: about 64 MiB per copy (NSLCT_HOST_CHUNK_MB overrides), so
+// the H2D of chunk i+1, the passes of chunk i and the D2H of chunk i-1 overlap.
+static int64_t host_chunk_images(const nslct_plan_s* pl) {
+  double mb = 64.0;
+  if (const char* e = std::getenv("NSLCT_HOST_CHUNK_MB")) {
+    const double v = std::atof(e);
+    if (v > 0) mb = v;
+  }
+  const double img = (double)pl->n * (double)pl->n * (double)pl->elem;
+  int64_t c = (int64_t)(mb * 1048576.0 / img);
+  if (c < 1) c = 1;
+  if (c > pl->batch) c = pl->batch;
+  return c;
+}
+
 nslct_status nslct_exec_host(nslct_plan_t pl, const void* host_in, void* host_out, void* stream) {
   if (!pl) return fail(NSLCT_E_ARG, "null plan");
   if (pl->slab) return fail(NSLCT_E_ARG, "slab plans run pass by pass: nslct_exec_pass");
@@ -754,10 +784,37 @@ nslct_status nslct_exec_host(nslct_plan_t pl, const void* host_in, void* host_ou
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (!pl->h_in) CUDA_TRY(cudaMalloc(&pl->h_in, pl->bytes));
   if (!pl->h_out) CUDA_TRY(cudaMalloc(&pl->h_out, pl->bytes));
-  CUDA_TRY(cudaMemcpyAsync(pl->h_in, host_in, pl->bytes, cudaMemcpyHostToDevice, s));
-  nslct_status st = nslct_exec(pl, pl->h_in, pl->h_out, stream);
-  if (st != NSLCT_OK) return st;
-  CUDA_TRY(cudaMemcpyAsync(host_out, pl->h_out, pl->bytes, cudaMemcpyDeviceToHost, s));
+  if (!pl->cs_in) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cs_in, cudaStreamNonBlocking));
+  if (!pl->cs_out) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cs_out, cudaStreamNonBlocking));
+  const int64_t c = host_chunk_images(pl);
+  const int64_t nch = (pl->batch + c - 1) / c;
+  while ((int64_t)pl->cev.size() < 2 * nch + 1) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    pl->cev.push_back(e);
+  }
+  const size_t img_bytes = (size_t)pl->n * (size_t)pl->n * pl->elem;
+  // copies start after whatever the caller queued on `stream` before this call
+  CUDA_TRY(cudaEventRecord(pl->cev[2 * nch], s));
+  CUDA_TRY(cudaStreamWaitEvent(pl->cs_in, pl->cev[2 * nch], 0));
+  for (int64_t i = 0; i < nch; ++i) {
+    const int64_t i0 = i * c, ni = (i0 + c <= pl->batch) ? c : pl->batch - i0;
+    const size_t off = (size_t)i0 * img_bytes, len = (size_t)ni * img_bytes;
+    unsigned char* din = static_cast<unsigned char*>(pl->h_in) + off;
+    unsigned char* dout = static_cast<unsigned char*>(pl->h_out) + off;
+    void* dscr = pl->scratch ? static_cast<void*>(static_cast<unsigned char*>(pl->scratch) + off) : nullptr;
+    CUDA_TRY(cudaMemcpyAsync(din, static_cast<const unsigned char*>(host_in) + off, len,
+                             cudaMemcpyHostToDevice, pl->cs_in));
+    CUDA_TRY(cudaEventRecord(pl->cev[2 * i], pl->cs_in));
+    CUDA_TRY(cudaStreamWaitEvent(s, pl->cev[2 * i], 0));
+    nslct_status st = run_images(pl, din, dout, dscr, ni, s, false);
+    if (st != NSLCT_OK) return st;
+    CUDA_TRY(cudaEventRecord(pl->cev[2 * i + 1], s));
+    CUDA_TRY(cudaStreamWaitEvent(pl->cs_out, pl->cev[2 * i + 1], 0));
+    CUDA_TRY(cudaMemcpyAsync(static_cast<unsigned char*>(host_out) + off, dout, len, cudaMemcpyDeviceToHost,
+                             pl->cs_out));
+  }
+  CUDA_TRY(cudaStreamSynchronize(pl->cs_out));
   CUDA_TRY(cudaStreamSynchronize(s));
   return NSLCT_OK;
 }
