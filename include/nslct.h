@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define NSLCT_ABI_VERSION 2
+#define NSLCT_ABI_VERSION 3
 
 typedef enum { NSLCT_C64 = 0, NSLCT_C128 = 1 } nslct_dtype;
 
@@ -46,7 +46,8 @@ typedef enum {
   NSLCT_E_ARG = 1,             /* null/misaligned pointer, bad batch/dtype/option            */
   NSLCT_E_NOT_SYMPLECTIC = 2,  /* an Eq. Intro12 residual exceeds 1e-10                       */
   NSLCT_E_NO_DECOMP = 3,       /* no feasible H with |det B'| > 1e-8 max(1,|B'|^2) (reading R5) */
-  NSLCT_E_UNSUPPORTED_N = 4,   /* N must be a power of two, 32 <= N <= 16384                  */
+  NSLCT_E_UNSUPPORTED_N = 4,   /* N outside [2, 4096] and not a power of two <= 16384 (c128:
+                                  8192); or no on-chip kernel for NSLCT_SCHEDULE_ON_CHIP     */
   NSLCT_E_CUDA = 5,            /* a CUDA launch/copy/allocation call failed (see last_error)  */
   NSLCT_E_NCCL = 6,            /* reserved for the slab-sharded mode                          */
   NSLCT_E_OOM = 7              /* device allocation of the plan's scratch failed              */
@@ -73,7 +74,14 @@ typedef struct {
   int device;         /* CUDA device ordinal for the plan's buffers; -1 = current       */
   int profile;        /* 1: record per-pass CUDA events in nslct_exec (nslct_pass_ms)   */
   int schedule;       /* NSLCT_SCHEDULE_*: how a batched plan's passes are launched      */
-  int reserved[5];
+  int n_in;           /* fused zero-padding:
+                         0 = none; else 1 <= n_in <= n is the side of the INPUT images,
+                         [batch][n_in][n_in], placed on the n x n grid with every sample
+                         keeping its centred coordinate (rows/columns [n/2 - n_in/2,
+                         n/2 - n_in/2 + n_in)), zeros elsewhere; same dx; the output is
+                         [batch][n][n].  Padded plans cannot run in place and have no
+                         row-slab form.                                                    */
+  int reserved[4];
 } nslct_opts;
 /* schedules of a batched plan (all compute the same operator) */
 enum { NSLCT_SCHEDULE_AUTO = 0,        /* the on-chip kernel for N <= 64 (measured faster at
@@ -92,15 +100,20 @@ void nslct_opts_default(nslct_opts* opts);
  * 4x4: [[a11 a12 b11 b12],[a21 a22 b21 b22],[c11 c12 d11 d12],[c21 c22 d21 d22]],
  * PAPER.md:46-51).  Host-side planning (validation, dispatch, H search) plus device
  * allocation of twiddle tables and one scratch buffer of batch*n*n complex elements on
- * the selected device.  The plan owns everything it allocates; free with nslct_destroy. */
+ * the selected device.  The plan owns everything it allocates; free with nslct_destroy.
+ * n: a power of two in [32, 16384] (c128: <= 8192) runs the radix-16 line FFTs; any
+ * other n in [2, 4096] (odd n included: the paper's N = 165 + dN) runs
+ * every line DFT by Bluestein's identity with power-of-two FFTs of length
+ * 2^ceil(log2(2n-1)), same operator, same layouts (nslct_plan_desc.fft_len). */
 nslct_status nslct_plan(nslct_plan_t* plan, int64_t n, const double abcd[16], int64_t batch,
                         nslct_dtype dtype);
 nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16], int64_t batch,
                            nslct_dtype dtype, const nslct_opts* opts);
 
 /* Enqueue the transform of `batch` images on `cuda_stream` (a cudaStream_t; NULL = the
- * legacy default stream).  in/out: DEVICE pointers to [batch][n][n] interleaved complex,
- * 16-byte aligned, owned by the caller; in == out is allowed.  Asynchronous and
+ * legacy default stream).  in/out: DEVICE pointers to [batch][n][n] interleaved complex
+ * (in: [batch][n_in][n_in] for a zero-padding plan), 16-byte aligned, owned by the
+ * caller; in == out is allowed (not for a padding plan).  Asynchronous and
  * stream-ordered: no host synchronisation, no allocation.  At most one exec per plan in
  * flight (the plan's scratch is shared).  Errors: E_ARG (null/misaligned), E_CUDA. */
 nslct_status nslct_exec(nslct_plan_t plan, const void* in, void* out, void* cuda_stream);
@@ -112,7 +125,8 @@ nslct_status nslct_exec(nslct_plan_t plan, const void* in, void* out, void* cuda
  * passes of chunk i (on cuda_stream) and the device->host copy of chunk i-1 (a second
  * plan-owned copy stream) overlap, so a large batch costs about one PCIe direction, not
  * both plus the compute.  The copies start after the work already queued on cuda_stream.
- * host buffers [batch][n][n] complex (pinned memory gives full copy speed and overlap).
+ * host buffers [batch][n][n] complex (host_in [batch][n_in][n_in] for a padding plan;
+ * pinned memory gives full copy speed and overlap).
  * Device staging buffers, copy streams and events are created on the first call and
  * owned by the plan.  Errors: E_ARG (null pointers, slab plan), E_CUDA, E_OOM. */
 nslct_status nslct_exec_host(nslct_plan_t plan, const void* host_in, void* host_out,
@@ -162,6 +176,10 @@ typedef struct {
   int on_chip;                 /* 1: the whole transform runs in one kernel per image, the
                                   image held in shared memory (see
                                   NSLCT_SCHEDULE_*); nslct_exec_pass still runs line passes  */
+  int fft_len;                 /* FFT length per line: N for a power-of-two N; for any other
+                                  N the line DFTs run by Bluestein's chirp-z identity with
+                                  FFTs of length 2^ceil(log2(2N-1)) (>= 32); 0 for B = 0   */
+  int n_in;                    /* input side (== n unless the plan zero-pads)                 */
 } nslct_plan_desc;
 
 nslct_status nslct_plan_info(nslct_plan_t plan, nslct_plan_desc* out);

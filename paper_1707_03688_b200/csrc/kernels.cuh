@@ -319,6 +319,7 @@ struct FftShape {
 template <typename T, int LOG2N>
 struct TwSet {
   static constexpr bool kFft64 = false;
+  static constexpr bool kBluestein = false;
   using Sh = FftShape<LOG2N>;
   static constexpr int NBMAX = 16 / Sh::template R<Sh::NS - 1>() > 1 ? 16 / Sh::template R<Sh::NS - 1>() : 1;
   cpx<T> w[Sh::NS][NBMAX];
@@ -365,6 +366,7 @@ __device__ __forceinline__ int padw(int i) { return i + PW * (i >> 4); }
 template <typename T, int LOG2N>
 struct TwTab {
   static constexpr bool kFft64 = false;
+  static constexpr bool kBluestein = false;
   using Sh = FftShape<LOG2N>;
   template <int S>
   __host__ __device__ static constexpr int off() {
@@ -444,6 +446,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t ta, const float (&f)[16]) {
 template <int LOG2N>
 struct TwTmem {
   static constexpr bool kFft64 = false;
+  static constexpr bool kBluestein = false;
   using Sh = FftShape<LOG2N>;
   uint32_t ta;   // this thread's TMEM address: lane quadrant + its warp's column base
   // stage S (>= 1) uses columns (S-1)*32 .. +31: complex index b*(R-1) + (r-1)
@@ -548,6 +551,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t ta, float (&f)[32]) {
 
 struct TwFft64 {
   static constexpr bool kFft64 = true;
+  static constexpr bool kBluestein = false;
   uint32_t tcol;   // lane quadrant << 16 | this warp's 64 constant columns
   uint32_t xcol;   // lane quadrant << 16 | column 256 (two 128-column exchange buffers)
   int m;           // j / 64 (warp-uniform)
@@ -804,10 +808,56 @@ struct FftInfo {
   static constexpr int NX = NS - 1;            // exchanges per FFT
 };
 
+// ---------------------------------------------------------------------------------
+// Arbitrary N: the centered length-N DFT of Eq. BasicDFT16 along a
+// line, by Bluestein's identity p m = (p^2 + m^2 - (p - m)^2) / 2 on centered p, m:
+//     X[p] = bq[p] sum_m (x[m] bq[m]) b[p - m],   b[k] = exp(+j pi k^2 / N),  bq = conj(b),
+// a linear convolution over |p - m| < N evaluated as a circular one of length
+// M = 2^LOG2M >= 2N - 1 with the radix-16 line FFT above (two FFTs of length M per DFT).
+// The line sits in the M-element register line at array index i = m + floor(N/2) < N,
+// zeros above.  Plan-owned tables (fp64-accurate, stored at the run precision):
+//     bq[i]   = exp(-j pi (i - floor(N/2))^2 / N),  i < N;
+//     bhat[k] = (1/M) FFT_M(c)[k],  c[k mod M] = b[k] for |k| < N, 0 elsewhere.
+// No centring checkerboard is involved (the identity holds for centered indices of any N).
+// ---------------------------------------------------------------------------------
+template <typename T, int LOG2M>
+struct TwBluestein {
+  static constexpr bool kFft64 = false;
+  static constexpr bool kBluestein = true;
+  TwSet<T, LOG2M> inner;   // twiddles of the length-M FFT
+  const cpx<T>* __restrict__ bq;
+  const cpx<T>* __restrict__ bhat;
+  int n;
+};
+
+template <typename T, int LOG2M, int X0, class E, class TW>
+__device__ __forceinline__ void bluestein_dft(cpx<T> (&v)[16], int j, const TW& tw, const E& ex) {
+  constexpr int TL = (1 << LOG2M) / 16;
+  constexpr int NS = FftInfo<LOG2M>::NS;
+  using In = TwSet<T, LOG2M>;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int i = j + TL * e;
+    v[e] = (i < tw.n) ? cmul(v[e], tw.bq[i]) : cpx<T>{T(0), T(0)};
+  }
+  FftStages<T, LOG2M, 0, NS, X0, E, In>::run(v, j, tw.inner, ex);
+  // slot e of thread j now holds frequency j + TL e; IFFT(Y) = conj(FFT(conj(Y)))
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] = cconj(cmul(v[e], tw.bhat[j + TL * e]));
+  FftStages<T, LOG2M, 0, NS, X0, E, In>::run(v, j, tw.inner, ex);
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int i = j + TL * e;
+    v[e] = (i < tw.n) ? cmul(cconj(v[e]), tw.bq[i]) : cpx<T>{T(0), T(0)};
+  }
+}
+
 // FFT of the thread's line; X0 = index of its first exchange within the pass.
 template <typename T, int LOG2N, int X0, class E, class TW>
 __device__ __forceinline__ void line_fft(cpx<T> (&v)[16], int j, const TW& tw, const E& ex) {
-  if constexpr (TW::kFft64) {
+  if constexpr (TW::kBluestein) {
+    bluestein_dft<T, LOG2N, X0>(v, j, tw, ex);
+  } else if constexpr (TW::kFft64) {
     static_assert(LOG2N == 12, "the 64x64 FFT is for N = 4096");
     fft64x64<X0>(v, tw, ex);
   } else {
@@ -916,6 +966,11 @@ struct PassArgs {
   int line_offset;     // global index of local line 0 (chirps use global indices)
   int in_chunk;        // C: input line = N/C chunks of C contiguous elements ...
   long long in_chunk_stride;  // ... CS elements apart (slab: C = L, CS = L*L)
+  // Fused zero-padding (row F3): the first pass reads [n_in][n_in]
+  // images placed at rows/columns [in_off, in_off + n_in) of the N x N grid, zeros
+  // elsewhere.  n_in = 0: no padding.  (line_pass_kernel and bl_pass_kernel only.)
+  int n_in;
+  int in_off;
 };
 
 // The per-line work of one pass (registers v hold elements j + TL*e of line l).
@@ -1023,7 +1078,16 @@ line_pass_kernel(PassArgs a) {
   const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in) + img * img_elems;
 
   cpx<T> v[16];
-  if (a.in_chunk == N) {
+  if (ModeIO<MODE>::kUserIn && a.n_in) {   // fused zero-padding (first pass only)
+    const long long nin = a.n_in;
+    const cpx<T>* src = reinterpret_cast<const cpx<T>*>(a.in) + img * nin * nin;
+    const int r = ll - a.in_off;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int c = j + TL * e - a.in_off;
+      v[e] = (r >= 0 && r < nin && c >= 0 && c < nin) ? src[r * nin + c] : cpx<T>{T(0), T(0)};
+    }
+  } else if (a.in_chunk == N) {
     const cpx<T>* src = in + (long long)ll * N + j;
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = src[TL * e];
@@ -1500,6 +1564,8 @@ struct B0Args {
   double d11, d12, d21, d22;
   double amp_re, amp_im;
   Phase ph;           // chirp polynomial in (i, j) array indices
+  int n_in;           // input side (fused zero-padding, row F3); == n: none
+  int in_off;         // input sample (r, c) sits at (r + in_off, c + in_off) of the grid
 };
 
 template <typename T>
@@ -1516,11 +1582,12 @@ __global__ void __launch_bounds__(256) b0_kernel(B0Args a) {
   const double q1 = __dadd_rn(__dmul_rn(a.d12, p), __dmul_rn(a.d22, q));
   const double p2 = floor(p1), q2 = floor(q1);
   const double kk = p1 - p2, lw = q1 - q2;
-  const cpx<T>* __restrict__ g = reinterpret_cast<const cpx<T>*>(a.in) + img * nn;
-  const long long ia = (long long)p2 + h, ja = (long long)q2 + h;
+  const long long nin = a.n_in;
+  const cpx<T>* __restrict__ g = reinterpret_cast<const cpx<T>*>(a.in) + img * nin * nin;
+  const long long ia = (long long)p2 + h - a.in_off, ja = (long long)q2 + h - a.in_off;
   auto tap = [&](long long r, long long c) -> cpx<T> {
-    if (r < 0 || r >= n || c < 0 || c >= n) return {T(0), T(0)};
-    return g[r * n + c];
+    if (r < 0 || r >= nin || c < 0 || c >= nin) return {T(0), T(0)};
+    return g[r * nin + c];
   };
   const cpx<T> g00 = tap(ia, ja), g01 = tap(ia, ja + 1), g10 = tap(ia + 1, ja), g11 = tap(ia + 1, ja + 1);
   const T w00 = (T)((1.0 - kk) * (1.0 - lw)), w01 = (T)((1.0 - kk) * lw);
@@ -1534,6 +1601,87 @@ __global__ void __launch_bounds__(256) b0_kernel(B0Args a) {
   const cpx<T> c = chirp_of<T>(t, T(1));
   const cpx<T> amp = {(T)a.amp_re, (T)a.amp_im};
   reinterpret_cast<cpx<T>*>(a.out)[idx] = cmul(amp, cmul(c, s));
+}
+
+// ---------------------------------------------------------------------------------
+// Line pass for arbitrary N (row F3): the pass_body of the power-of-two kernels with
+// every line DFT replaced by the Bluestein DFT above (TwBluestein), lines of N elements
+// in HBM held in M-element register lines.  One CTA takes G = LineCfg<LOG2M>::G lines
+// of ONE image (grid = batch * ceil(N / G)); the transposed store is staged through
+// shared memory like line_pass_kernel's.  Plain per-thread loads/stores: this is the
+// accuracy path of the paper's padding experiments (E3), not the headline C4 path.
+// ---------------------------------------------------------------------------------
+struct BlArgs {
+  const void* bq;     // [N] complex, see TwBluestein
+  const void* bhat;   // [M] complex
+  int n;              // line length N (2 <= N, 2N - 1 <= M)
+};
+
+template <typename T, int LOG2M, int MODE>
+__global__ void __launch_bounds__(LineCfg<LOG2M>::THREADS)
+bl_pass_kernel(PassArgs a, BlArgs b) {
+  using Cfg = LineCfg<LOG2M>;
+  constexpr int TL = Cfg::TL, G = Cfg::G, LS = Cfg::LS, THREADS = Cfg::THREADS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cpx<T>* smem = reinterpret_cast<cpx<T>*>(smem_raw);
+  const int n = b.n;
+  const int tid = threadIdx.x;
+  const int j = tid % TL;
+  const int gl = tid / TL;
+  const int bpi = (n + G - 1) / G;                      // CTAs per image
+  const long long img = blockIdx.x / bpi;
+  const int l0 = (int)(blockIdx.x % bpi) * G;           // first line of this CTA
+  const int ll = l0 + gl;
+  const bool live = ll < n;
+  const long long img_elems = (long long)n * n;
+  cpx<T>* buf = smem + gl * LS;
+
+  cpx<T> v[16];
+  if (ModeIO<MODE>::kUserIn && a.n_in) {   // fused zero-padding
+    const long long nin = a.n_in;
+    const cpx<T>* src = reinterpret_cast<const cpx<T>*>(a.in) + img * nin * nin;
+    const int r = ll - a.in_off;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int c = j + TL * e - a.in_off;
+      v[e] = (live && r >= 0 && r < nin && c >= 0 && c < nin) ? src[r * nin + c] : cpx<T>{T(0), T(0)};
+    }
+  } else {
+    const cpx<T>* src = reinterpret_cast<const cpx<T>*>(a.in) + img * img_elems + (long long)ll * n;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int i = j + TL * e;
+      v[e] = (live && i < n) ? src[i] : cpx<T>{T(0), T(0)};
+    }
+  }
+  TwBluestein<T, LOG2M> tw;
+  tw.inner.load(reinterpret_cast<const cpx<T>*>(a.tw), j);
+  tw.bq = reinterpret_cast<const cpx<T>*>(b.bq);
+  tw.bhat = reinterpret_cast<const cpx<T>*>(b.bhat);
+  tw.n = n;
+  pass_body<T, LOG2M, MODE>(v, j, tw, a, (uint64_t)ll, ExPad<T>{buf});
+
+  cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * img_elems;
+  if constexpr (ModeIO<MODE>::kStraightOut) {
+    if (live) {
+      cpx<T>* dst = out + (long long)ll * n;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int i = j + TL * e;
+        if (i < n) dst[i] = v[e];
+      }
+    }
+  } else {
+    // transposed store out[img][i][ll], consecutive threads -> consecutive lines
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) buf[pad16(j + TL * e)] = v[e];
+    __syncthreads();
+    for (int f = tid; f < G * n; f += THREADS) {
+      const int gg = f % G, e = f / G;
+      if (l0 + gg < n) out[(long long)e * n + l0 + gg] = smem[gg * LS + pad16(e)];
+    }
+  }
 }
 
 }  // namespace nslct

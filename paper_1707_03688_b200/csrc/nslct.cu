@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/nslct.h"
+#include "bluestein.h"
 #include "kernels.cuh"
 #include "planner.h"
 
@@ -280,7 +281,12 @@ Phase to_phase(const Poly& P, bool line_is_x) {
 
 struct nslct_plan_s {
   int64_t n = 0, batch = 0;
-  int log2n = 0;
+  int log2n = 0;       // power-of-two plans: log2 N; Bluestein plans: log2 M (FFT length)
+  bool bluestein = false;   // arbitrary N (row F3): every line DFT by Bluestein, length M
+  int64_t n_in = 0;         // input side (fused zero-padding when < n)
+  size_t in_img_bytes = 0;  // bytes of one input image (n_in^2 elements)
+  void* bq = nullptr;       // Bluestein tables (kernels.cuh TwBluestein)
+  void* bhat = nullptr;
   nslct_dtype dtype = NSLCT_C64;
   int device = 0;
   int profile = 0;
@@ -328,6 +334,8 @@ void free_plan(nslct_plan_s* pl) {
   if (!pl) return;
   DeviceGuard g(pl->device);
   if (pl->tw) cudaFree(pl->tw);
+  if (pl->bq) cudaFree(pl->bq);
+  if (pl->bhat) cudaFree(pl->bhat);
   if (pl->scratch) cudaFree(pl->scratch);
   if (pl->counters) cudaFree(pl->counters);
   if (pl->h_in) cudaFree(pl->h_in);
@@ -340,6 +348,91 @@ void free_plan(nslct_plan_s* pl) {
     for (auto& e : set.e)
       if (e) cudaEventDestroy(e);
   delete pl;
+}
+}  // namespace
+
+namespace {
+constexpr int64_t kBlMaxN = 4096;   // Bluestein FFT length M <= 2^kBlMaxLog
+
+// (cos, sin) of 2 pi num/den, the argument reduced exactly to [-1/8, 1/8] turn around
+// the nearest quarter turn before the fp64 cos/sin.
+void cis_turns(int64_t num, int64_t den, double* c, double* s) {
+  num %= den;
+  if (num < 0) num += den;
+  const int64_t q4 = (4 * num + den / 2) / den;
+  const double r = 2.0 * M_PI * ((double)(4 * num - q4 * den) / (4.0 * (double)den));
+  const double cr = std::cos(r), sr = std::sin(r);
+  switch (q4 & 3) {
+    case 0: *c = cr; *s = sr; break;
+    case 1: *c = -sr; *s = cr; break;
+    case 2: *c = -cr; *s = -sr; break;
+    default: *c = sr; *s = -cr; break;
+  }
+}
+
+// In-place fp64 radix-2 FFT (forward, e^{-2 pi i jk/M}) of the host table builder.
+void host_fft(std::vector<double>& re, std::vector<double>& im) {
+  const int64_t m = (int64_t)re.size();
+  for (int64_t i = 1, j = 0; i < m; ++i) {
+    int64_t bit = m >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) {
+      std::swap(re[i], re[j]);
+      std::swap(im[i], im[j]);
+    }
+  }
+  for (int64_t len = 2; len <= m; len <<= 1) {
+    for (int64_t k = 0; k < len / 2; ++k) {
+      double c, sn;
+      cis_turns(-k, len, &c, &sn);
+      for (int64_t i = k; i < m; i += len) {
+        const int64_t u = i, v = i + len / 2;
+        const double tr = re[v] * c - im[v] * sn, ti = re[v] * sn + im[v] * c;
+        re[v] = re[u] - tr;
+        im[v] = im[u] - ti;
+        re[u] += tr;
+        im[u] += ti;
+      }
+    }
+  }
+}
+
+// Bluestein tables of kernels.cuh TwBluestein for a plan of side n and FFT length
+// M = 2^log2n:  bq[i] = exp(-j pi (i-h)^2/N), bhat = FFT_M(c)/M with
+// c[k mod M] = exp(+j pi k^2/N) for |k| < N.  Phases reduced exactly: k^2 mod 2N.
+nslct_status bluestein_tables(nslct_plan_s* pl) {
+  const int64_t n = pl->n, m = int64_t(1) << pl->log2n, h = n / 2;
+  std::vector<double> bre(n), bim(n), cre(m, 0.0), cim(m, 0.0);
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t d = i - h;
+    cis_turns(-((d * d) % (2 * n)), 2 * n, &bre[i], &bim[i]);
+  }
+  for (int64_t k = -(n - 1); k <= n - 1; ++k) {
+    const int64_t pos = (k + m) % m;
+    cis_turns((k * k) % (2 * n), 2 * n, &cre[pos], &cim[pos]);
+  }
+  host_fft(cre, cim);
+  const size_t e = pl->elem;
+  std::vector<unsigned char> hb(n * e), hh(m * e);
+  auto put = [&](unsigned char* dst, int64_t i, double re, double im) {
+    if (e == 8) {
+      float* f = reinterpret_cast<float*>(dst);
+      f[2 * i] = (float)re;
+      f[2 * i + 1] = (float)im;
+    } else {
+      double* f = reinterpret_cast<double*>(dst);
+      f[2 * i] = re;
+      f[2 * i + 1] = im;
+    }
+  };
+  for (int64_t i = 0; i < n; ++i) put(hb.data(), i, bre[i], bim[i]);
+  for (int64_t k = 0; k < m; ++k) put(hh.data(), k, cre[k] / (double)m, cim[k] / (double)m);
+  CUDA_TRY(cudaMalloc(&pl->bq, n * e));
+  CUDA_TRY(cudaMalloc(&pl->bhat, m * e));
+  CUDA_TRY(cudaMemcpy(pl->bq, hb.data(), n * e, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(pl->bhat, hh.data(), m * e, cudaMemcpyHostToDevice));
+  return NSLCT_OK;
 }
 }  // namespace
 
@@ -402,9 +495,17 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
     return fail(NSLCT_E_ARG, "bad variant/dispatch option");
   int lg = 0;
   while ((int64_t(1) << lg) < n && lg < 62) ++lg;
-  if (n < 1 || (int64_t(1) << lg) != n || lg < kMinLog || lg > kMaxLog ||
-      (dtype == NSLCT_C128 && lg > kMaxLog128))
-    return fail(NSLCT_E_UNSUPPORTED_N, "N must be a power of two in [32, 16384] (c128: <= 8192)");
+  const bool pow2 = n >= 1 && (int64_t(1) << lg) == n && lg >= kMinLog && lg <= kMaxLog &&
+                    !(dtype == NSLCT_C128 && lg > kMaxLog128);
+  if (!pow2) {   // arbitrary N: Bluestein line DFTs of length M = 2^lg >= 2N - 1 (row F3)
+    if (n < 2 || n > kBlMaxN)
+      return fail(NSLCT_E_UNSUPPORTED_N,
+                  "N must be a power of two in [32, 16384] (c128: <= 8192) or any N in [2, 4096]");
+    lg = nslct::kBlMinLog;
+    while ((int64_t(1) << lg) < 2 * n - 1) ++lg;
+  }
+  const int64_t n_in = (o.n_in > 0) ? o.n_in : n;
+  if (n_in > n) return fail(NSLCT_E_ARG, "n_in must be <= n");
   if (!(std::isfinite(o.dx)) || (o.dx > 0 && !(o.dx < 1e30)))
     return fail(NSLCT_E_ARG, "bad dx");
 
@@ -423,18 +524,22 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
   int st = nslct::make_plan(abcd, o.variant, o.dispatch, o.h_fixed, &p, &err);
   if (st) return fail((nslct_status)st, err);
   if (slab && p.kind == 0) return fail(NSLCT_E_ARG, "B = 0 has no row-slab form");
+  if (slab && (!pow2 || n_in != n)) return fail(NSLCT_E_ARG, "row-slab plans need a power-of-two N and no padding");
 
   nslct_plan_s* pl = new (std::nothrow) nslct_plan_s();
   if (!pl) return fail(NSLCT_E_OOM, "host allocation failed");
   pl->n = n;
   pl->batch = batch;
   pl->log2n = lg;
+  pl->bluestein = !pow2;
+  pl->n_in = n_in;
   pl->dtype = dtype;
   pl->p = p;
   pl->profile = o.profile;
   pl->dx = (o.dx > 0) ? o.dx : std::sqrt(2.0 * M_PI / (double)n);
   pl->elem = (dtype == NSLCT_C64) ? 8 : 16;
   pl->bytes = (size_t)batch * (size_t)n * (size_t)n * pl->elem;
+  pl->in_img_bytes = (size_t)n_in * (size_t)n_in * pl->elem;
   pl->slab = slab;
   pl->nranks = slab ? nranks : 1;
   pl->rank = slab ? rank : 0;
@@ -468,18 +573,25 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       b.amp_re = detD >= 0 ? std::sqrt(detD) : 0.0;
       b.amp_im = detD >= 0 ? 0.0 : std::sqrt(-detD);
       b.ph = to_phase(P, true);
+      b.n_in = (int)n_in;
+      b.in_off = (int)(n / 2 - n_in / 2);
       break;
     }
-    // twiddles exp(-2 pi i k/N) in fp64, stored at the run precision
+    // twiddles exp(-2 pi i k/N) in fp64, stored at the run precision (N = M for Bluestein)
+    if (pl->bluestein) {
+      nslct_status st = bluestein_tables(pl);
+      if (st != NSLCT_OK) { result = st; break; }
+    }
     {
-      const size_t tw_bytes = (size_t)n * pl->elem;
+      const int64_t nt = int64_t(1) << lg;
+      const size_t tw_bytes = (size_t)nt * pl->elem;
       unsigned char* host = new (std::nothrow) unsigned char[tw_bytes];
       if (!host) { result = fail(NSLCT_E_OOM, "host twiddles"); break; }
-      for (int64_t k = 0; k < n; ++k) {
+      for (int64_t k = 0; k < nt; ++k) {
         // reduce k/N to [-1/8, 1/8] turns around the nearest quarter for accuracy
         double s, c;
-        const int64_t q4 = (4 * k + n / 2) / n;           // nearest quarter turn
-        const double r = 2.0 * M_PI * ((double)(4 * k - q4 * n) / (4.0 * (double)n));
+        const int64_t q4 = (4 * k + nt / 2) / nt;         // nearest quarter turn
+        const double r = 2.0 * M_PI * ((double)(4 * k - q4 * nt) / (4.0 * (double)nt));
         const double cr = std::cos(r), sr = std::sin(r);
         switch (q4 & 3) {
           case 0: c = cr; s = sr; break;
@@ -518,16 +630,20 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
     const double invn = 1.0 / (double)n;
     // K1: CM_r(Q0) + checkerboard;  K2: CM_w(Q1)/N;  K3: CM_r(Q2)/N;  K4: CM_w(Q3)/N;
     // K5: CM_r(Q4)/N + checkerboard.
-    Poly P0 = chirp_poly(p.q_active[0] ? p.Q[0] : zero, dx, (int)n, true);
+    // power-of-two plans: the centred DFT is S W S (kernels.cuh header); the outer
+    // checkerboards S ride on the first and last chirps.  Bluestein DFTs are centred
+    // by construction: no checkerboard.
+    const bool ck = !pl->bluestein;
+    Poly P0 = chirp_poly(p.q_active[0] ? p.Q[0] : zero, dx, (int)n, ck);
     Poly P1 = chirp_poly(p.Q[1], dw, (int)n, false);
     Poly P2 = chirp_poly(p.Q[2], dx, (int)n, false);
     Poly P3 = chirp_poly(p.Q[3], dw, (int)n, false);
-    Poly P4 = chirp_poly(p.q_active[4] ? p.Q[4] : zero, dx, (int)n, true);
+    Poly P4 = chirp_poly(p.q_active[4] ? p.Q[4] : zero, dx, (int)n, ck);
     const Phase ph[5] = {to_phase(P0, true), to_phase(P1, false), to_phase(P2, true),
                          to_phase(P3, false), to_phase(P4, true)};
     // inverse FFTs are unnormalised; the last pass applies 1/N^4 (two 2D inverses)
     const double sc[5] = {1.0, 1.0, 1.0, 1.0, invn * invn * invn * invn};
-    const int sign_only[5] = {p.q_active[0] ? 0 : 1, 0, 0, 0, p.q_active[4] ? 0 : 1};
+    const int sign_only[5] = {(p.q_active[0] || !ck) ? 0 : 1, 0, 0, 0, (p.q_active[4] || !ck) ? 0 : 1};
     for (int k = 0; k < 5; ++k) {
       pl->args[k] = PassArgs{};
       pl->args[k].tw = pl->tw;
@@ -536,7 +652,7 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       pl->args[k].scale = sc[k];
       pl->args[k].sign_only = sign_only[k];
     }
-    if (lc_y(p)) {
+    if (lc_y(p) && !pl->bluestein) {
       // LC-NsDLCT with H = (0,0;0,h) (Eq. LC12 with F_y): the 1D CC along y merges with
       // the neighbouring y-axis FFTs, 3 passes.  S_x / S_y are the
       // one-axis centring checkerboards left over when a 1D and a 2D DFT meet.
@@ -576,16 +692,19 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       pl->args[k].in_chunk = (slab && k > 0) ? (int)L : (int)n;
       pl->args[k].in_chunk_stride = (slab && k > 0) ? L * L : n * n;
       pl->args[k].n_lines = slab ? L : batch * n;
+      pl->args[k].n_in = (k == 0 && n_in != n) ? (int)n_in : 0;
+      pl->args[k].in_off = (k == 0 && n_in != n) ? (int)(n / 2 - n_in / 2) : 0;
     }
     {
       int sms = 0;
       if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device) == cudaSuccess && sms > 0)
         pl->num_sms = sms;
       const char* np = std::getenv("NSLCT_NO_PIPE");
-      pl->pipe = (!slab && ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
+      const bool plain = pow2 && n_in == n;   // neither Bluestein nor padded
+      pl->pipe = (plain && !slab && ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
       const char* f64 = std::getenv("NSLCT_FFT64");
       pl->fft64 = pl->pipe && lg == 12 && f64 && f64[0] == '1';
-      const bool have = !slab && table().li[ti][lg] != nullptr;
+      const bool have = plain && !slab && table().li[ti][lg] != nullptr;
       if (o.schedule == NSLCT_SCHEDULE_ON_CHIP && !have && pl->p.kind != 0) {
         result = fail(NSLCT_E_UNSUPPORTED_N, "no on-chip kernel for this N / dtype (c64 N <= 256, c128 N <= 128)");
         break;
@@ -615,7 +734,14 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       }
     }
     if (result != NSLCT_OK) break;
-    for (int m = 0; m < kModes; ++m) {
+    for (int m = 0; m < 4 && pl->bluestein; ++m) {
+      cudaError_t e = nslct::bl_attr(ti, lg, m)();
+      if (e != cudaSuccess) {
+        result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(bluestein): ") + cudaGetErrorString(e));
+        break;
+      }
+    }
+    for (int m = 0; m < kModes && !pl->bluestein; ++m) {
       cudaError_t e = table().at[ti][lg][m]();
       if (e != cudaSuccess) {
         result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
@@ -699,6 +825,26 @@ static nslct_status run_images(nslct_plan_t pl, const void* in, void* out, void*
     }
     return NSLCT_OK;
   }
+  if (pl->bluestein) {   // arbitrary N: Bluestein line passes (kernels.cuh bl_pass_kernel)
+    nslct::BlArgs bl{pl->bq, pl->bhat, (int)pl->n};
+    const int np = pl->n_passes;
+    const void* src = in;
+    for (int k = 0; k < np; ++k) {
+      void* dst = (k == np - 1) ? out : ((k % 2 == 0) ? scratch : out);
+      if (ev) CUDA_TRY(cudaEventRecord(ev[k], s));
+      PassArgs a = pl->args[k];
+      a.in = src;
+      a.out = dst;
+      a.n_lines = nimg * pl->n;
+      CUDA_TRY(nslct::bl_launcher(ti, pl->log2n, pl->mode[k])(a, bl, nimg, s));
+      src = dst;
+    }
+    if (ev) {
+      CUDA_TRY(cudaEventRecord(ev[np], s));
+      ++pl->ev_used;
+    }
+    return NSLCT_OK;
+  }
   if (pl->pipe) CUDA_TRY(cudaMemsetAsync(pl->counters, 0, 5 * sizeof(unsigned long long), s));
   // pass k writes the scratch (k even) or out (k odd); the last pass writes out in place.
   // HA: K1 in->S, K2 S->out, K3 out->S, K4 S->out, K5 out->out; LC-y: in->S, S->out, out->out
@@ -732,6 +878,7 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
   if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(NSLCT_E_ARG, "in/out must be 16-byte aligned");
   if (pl->slab) return fail(NSLCT_E_ARG, "slab plans run pass by pass: nslct_exec_pass");
+  if (pl->n_in != pl->n && in == out) return fail(NSLCT_E_ARG, "a padded plan cannot run in place");
   DeviceGuard guard(pl->device);
   return run_images(pl, in, out, pl->scratch, pl->batch, reinterpret_cast<cudaStream_t>(stream),
                     pl->profile != 0);
@@ -751,7 +898,10 @@ nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* ou
   PassArgs a = pl->args[pass];
   a.in = in;
   a.out = out;
-  if (pl->pipe) {
+  if (pl->bluestein) {
+    nslct::BlArgs bl{pl->bq, pl->bhat, (int)pl->n};
+    CUDA_TRY(nslct::bl_launcher(ti, pl->log2n, pl->mode[pass])(a, bl, pl->batch, s));
+  } else if (pl->pipe) {
     CUDA_TRY(cudaMemsetAsync(pl->counters + pass, 0, sizeof(unsigned long long), s));
     nslct_status st = launch_pipe_pass(pl, pass, a, s);
     if (st != NSLCT_OK) return st;
@@ -782,7 +932,7 @@ nslct_status nslct_exec_host(nslct_plan_t pl, const void* host_in, void* host_ou
   if (!host_in || !host_out) return fail(NSLCT_E_ARG, "null host pointer");
   DeviceGuard guard(pl->device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (!pl->h_in) CUDA_TRY(cudaMalloc(&pl->h_in, pl->bytes));
+  if (!pl->h_in) CUDA_TRY(cudaMalloc(&pl->h_in, pl->in_img_bytes * (size_t)pl->batch));
   if (!pl->h_out) CUDA_TRY(cudaMalloc(&pl->h_out, pl->bytes));
   if (!pl->cs_in) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cs_in, cudaStreamNonBlocking));
   if (!pl->cs_out) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cs_out, cudaStreamNonBlocking));
@@ -800,10 +950,11 @@ nslct_status nslct_exec_host(nslct_plan_t pl, const void* host_in, void* host_ou
   for (int64_t i = 0; i < nch; ++i) {
     const int64_t i0 = i * c, ni = (i0 + c <= pl->batch) ? c : pl->batch - i0;
     const size_t off = (size_t)i0 * img_bytes, len = (size_t)ni * img_bytes;
-    unsigned char* din = static_cast<unsigned char*>(pl->h_in) + off;
+    const size_t off_in = (size_t)i0 * pl->in_img_bytes, len_in = (size_t)ni * pl->in_img_bytes;
+    unsigned char* din = static_cast<unsigned char*>(pl->h_in) + off_in;
     unsigned char* dout = static_cast<unsigned char*>(pl->h_out) + off;
     void* dscr = pl->scratch ? static_cast<void*>(static_cast<unsigned char*>(pl->scratch) + off) : nullptr;
-    CUDA_TRY(cudaMemcpyAsync(din, static_cast<const unsigned char*>(host_in) + off, len,
+    CUDA_TRY(cudaMemcpyAsync(din, static_cast<const unsigned char*>(host_in) + off_in, len_in,
                              cudaMemcpyHostToDevice, pl->cs_in));
     CUDA_TRY(cudaEventRecord(pl->cev[2 * i], pl->cs_in));
     CUDA_TRY(cudaStreamWaitEvent(s, pl->cev[2 * i], 0));
@@ -850,6 +1001,8 @@ nslct_status nslct_plan_info(nslct_plan_t pl, nslct_plan_desc* d) {
   if (pl->p.kind != 0) d->n_passes = pl->n_passes;
   d->on_chip = (pl->p.kind != 0 && pl->image) ? 1 : 0;
   d->n_launches = (pl->p.kind == 0 || pl->image) ? 1 : pl->n_passes;
+  d->fft_len = (pl->p.kind == 0) ? 0 : (1 << pl->log2n);
+  d->n_in = (int)pl->n_in;
   return NSLCT_OK;
 }
 

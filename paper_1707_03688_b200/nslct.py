@@ -36,7 +36,7 @@ class NslctError(RuntimeError):
 class nslct_opts(ctypes.Structure):
     _fields_ = [("dx", ctypes.c_double), ("variant", ctypes.c_int), ("dispatch", ctypes.c_int),
                 ("h_fixed", ctypes.c_double * 3), ("device", ctypes.c_int), ("profile", ctypes.c_int),
-                ("schedule", ctypes.c_int), ("reserved", ctypes.c_int * 5)]
+                ("schedule", ctypes.c_int), ("n_in", ctypes.c_int), ("reserved", ctypes.c_int * 4)]
 
 
 class nslct_plan_desc(ctypes.Structure):
@@ -46,7 +46,8 @@ class nslct_plan_desc(ctypes.Structure):
                 ("P4", ctypes.c_double * 3), ("Q", (ctypes.c_double * 3) * 5),
                 ("dx", ctypes.c_double), ("objective", ctypes.c_double),
                 ("sym_residual", ctypes.c_double), ("recomposition_residual", ctypes.c_double),
-                ("dispatch_key", ctypes.c_double), ("n_launches", ctypes.c_int), ("on_chip", ctypes.c_int)]
+                ("dispatch_key", ctypes.c_double), ("n_launches", ctypes.c_int), ("on_chip", ctypes.c_int),
+                ("fft_len", ctypes.c_int), ("n_in", ctypes.c_int)]
 
 
 _LIB = None
@@ -97,7 +98,7 @@ SCHEDULES = {"auto": 0, "line_passes": 1, "on_chip": 2}
 
 
 def make_opts(dx=None, variant="HA", dispatch="reversible", h_fixed=None, device=None, profile=False,
-              schedule="auto"):
+              schedule="auto", n_in=None):
     o = nslct_opts()
     lib().nslct_opts_default(ctypes.byref(o))
     o.dx = float(dx) if dx else 0.0
@@ -110,6 +111,7 @@ def make_opts(dx=None, variant="HA", dispatch="reversible", h_fixed=None, device
     o.device = -1 if device is None else int(device)
     o.profile = 1 if profile else 0
     o.schedule = SCHEDULES[schedule]
+    o.n_in = 0 if n_in is None else int(n_in)
     return o
 
 
@@ -120,7 +122,8 @@ def _desc_dict(d):
                 h=np.array(list(d.H)), H=s(d.H), Bp=s(d.Bp), P2=s(d.P2), P4=s(d.P4),
                 Q=[s(d.Q[i]) for i in range(5)], dx=d.dx, objective=d.objective,
                 sym_residual=d.sym_residual, recomposition_residual=d.recomposition_residual,
-                dispatch_key=d.dispatch_key, n_launches=d.n_launches, on_chip=bool(d.on_chip))
+                dispatch_key=d.dispatch_key, n_launches=d.n_launches, on_chip=bool(d.on_chip),
+                fft_len=d.fft_len, n_in=d.n_in)
 
 
 def nslct_plan_describe(n, M, **kw):
@@ -133,14 +136,16 @@ def nslct_plan_describe(n, M, **kw):
 
 
 class Plan:
-    """RAII wrapper of nslct_plan_t.  exec() takes torch CUDA tensors (complex64/128)."""
+    """RAII wrapper of nslct_plan_t.  exec() takes torch CUDA tensors (complex64/128).
+    n_in (< n): fused zero-padding -- inputs are [batch, n_in, n_in], outputs [batch, n, n]."""
 
     def __init__(self, n, M, batch, dtype="c64", dx=None, variant="HA", dispatch="reversible",
-                 h_fixed=None, device=None, profile=False, schedule="auto"):
+                 h_fixed=None, device=None, profile=False, schedule="auto", n_in=None):
         self.n, self.batch = int(n), int(batch)
+        self.n_in = self.n if n_in is None else int(n_in)
         self.dtype = dtype
         a, ap = _abcd(M)
-        o = make_opts(dx, variant, dispatch, h_fixed, device, profile, schedule)
+        o = make_opts(dx, variant, dispatch, h_fixed, device, profile, schedule, n_in)
         h = ctypes.c_void_p()
         _check(lib().nslct_plan_ex(ctypes.byref(h), self.n, ap, self.batch,
                                    C64 if dtype == "c64" else C128, ctypes.byref(o)))
@@ -174,15 +179,16 @@ class Plan:
                                 ctypes.c_void_p(stream_ptr)))
 
     def exec(self, x, out=None, stream=None):
-        """x: torch CUDA tensor [batch, n, n] of complex64 (c64) / complex128 (c128)."""
+        """x: torch CUDA tensor [batch, n_in, n_in] of complex64 (c64) / complex128 (c128)."""
         import torch
         want = torch.complex64 if self.dtype == "c64" else torch.complex128
+        ni = self.n_in
         if not (x.is_cuda and x.dtype == want and x.is_contiguous()
-                and tuple(x.shape[-2:]) == (self.n, self.n) and x.numel() == self.batch * self.n * self.n):
+                and tuple(x.shape[-2:]) == (ni, ni) and x.numel() == self.batch * ni * ni):
             raise ValueError("exec expects a contiguous CUDA %s tensor of %d x %d x %d"
-                             % (want, self.batch, self.n, self.n))
+                             % (want, self.batch, ni, ni))
         if out is None:
-            out = torch.empty_like(x)
+            out = torch.empty((self.batch, self.n, self.n), dtype=want, device=x.device)
         s = stream if stream is not None else torch.cuda.current_stream(x.device)
         self.exec_ptr(x.data_ptr(), out.data_ptr(), s.cuda_stream)
         return out

@@ -428,10 +428,18 @@ def test_exec_host_chunked(monkeypatch, n, batch, chunk_mb, kind):
 def test_argument_errors():
     """Error codes of the ABI: unsupported N, bad batch, misaligned pointers, B0 in place."""
     M = synth.dft_matrix4()
-    for n in (16, 48, 100, 32768):
+    for n in (1, 4097, 5000, 32768):
         with pytest.raises(nslct.NslctError) as e:
             nslct.Plan(n, M, 1)
         assert e.value.name == "E_UNSUPPORTED_N"
+    with pytest.raises(nslct.NslctError) as e:
+        nslct.Plan(64, M, 1, n_in=65)
+    assert e.value.name == "E_ARG"
+    with nslct.Plan(64, M, 1, n_in=48) as p:
+        buf = torch.zeros(64 * 64, dtype=torch.complex64, device="cuda")
+        with pytest.raises(nslct.NslctError) as e:
+            p.exec_ptr(buf.data_ptr(), buf.data_ptr(), 0)
+        assert e.value.name == "E_ARG"
     with pytest.raises(nslct.NslctError) as e:
         nslct.Plan(16384, M, 1, dtype="c128")
     assert e.value.name == "E_UNSUPPORTED_N"
@@ -508,3 +516,110 @@ def test_slab_errors():
         nslct.SlabPlan(256, np.eye(4), 2, 0)  # B = 0 has no slab form
     with pytest.raises(nslct.NslctError):
         nslct.SlabPlan(256, M, 2, 2)          # rank out of range
+
+
+# ------------------------------------------------------------------ row F3: any N, zero-padding
+def fft_len(n):
+    if n >= 32 and (n & (n - 1)) == 0:
+        return n
+    m = 32
+    while m < 2 * n - 1:
+        m *= 2
+    return m
+
+
+@pytest.mark.parametrize("n", [2, 3, 6, 16, 30, 33, 48, 100, 165, 215, 1000])
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_arbitrary_n_bluestein(n, dtype):
+    """Any N: every line DFT by Bluestein's identity with power-of-two
+    FFTs of length >= 2N - 1; same operator as the oracle (which builds the centred DFT
+    matrix of Eq. BasicDFT16 for any N), both dispatch forms across the sweep."""
+    mr, ir = synth.config_streams(300 + n)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (2, n, n)).astype(NDT[dtype])
+    err, info, _ = parity(x, M, dtype)
+    assert err <= TOL[dtype], (n, dtype, err)
+    assert info["fft_len"] == fft_len(n)
+    assert info["n_launches"] == 5 and not info["on_chip"]
+
+
+@pytest.mark.parametrize("n", [2047, 4095])
+def test_arbitrary_n_large(n):
+    """Largest Bluestein FFT lengths (M = 4096, 8192; one or two lines per CTA): oracle
+    parity at 2047; at 4095 (oracle out of reach in test time) Parseval (P4) and
+    reversibility exec(M^-1) exec(M) = I (P5)."""
+    mr, ir = synth.config_streams(400 + n)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (1, n, n)).astype(np.complex64)
+    if n == 2047:
+        err, info, _ = parity(x, M, "c64")
+        assert err <= TOL["c64"], err
+        return
+    xt = torch.from_numpy(x).cuda()
+    with nslct.Plan(n, M, 1) as p, nslct.Plan(n, sy.inverse(M), 1) as pi:
+        assert p.info()["fft_len"] == 8192
+        G = p.exec(xt)
+        back = pi.exec(G)
+        torch.cuda.synchronize()
+        e_in = float(torch.sum(torch.abs(xt.to(torch.complex128)) ** 2))
+        e_out = float(torch.sum(torch.abs(G.to(torch.complex128)) ** 2))
+        assert abs(e_out / e_in - 1) < 1e-5
+        rel = float(torch.linalg.vector_norm((back - xt).to(torch.complex128)) /
+                    torch.linalg.vector_norm(xt.to(torch.complex128)))
+        assert rel < 1e-5, rel
+
+
+@pytest.mark.parametrize("n", [34, 100, 250])
+def test_arbitrary_n_special_cases(n):
+    """Even non-power-of-two N: the DFT matrix gives Eq. BasicDFT16 exactly (pin P1 via
+    numpy.fft); LC plans (y- and x-axis H run through the 5-pass schedule); B = 0."""
+    mr, ir = synth.config_streams(500 + n)
+    x = synth.iid_cn(ir, (2, n, n)).astype(np.complex64)
+    G, info = run_gpu(x, synth.dft_matrix4(), "c64")
+    dx = math.sqrt(2 * math.pi / n)
+    g = x.astype(np.complex128)
+    ref = dx * dx / (2j * math.pi) * np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(g, axes=(-2, -1))),
+                                                     axes=(-2, -1))
+    assert me.rel_l2(G, ref) <= 1e-5
+    M = synth.random_symplectic(mr)
+    err, info, _ = parity(x, M, "c64", variant="LC")
+    assert err <= TOL["c64"]
+    Mb = synth.b0_matrix4([[1.1, 0.4], [-0.3, 0.8]], [[0.3, -0.5], [-0.5, 0.9]])
+    err, info, _ = parity(x, Mb, "c64")
+    assert err <= TOL["c64"] and info["kind"] == "B0"
+
+
+@pytest.mark.parametrize("n_in,n,dtype,kind", [
+    (165, 256, "c64", "ha"),    # padded to a power of two: radix-16 line passes
+    (165, 215, "c64", "ha"),    # the paper's N = 165, dN = 50 (Bluestein)
+    (33, 64, "c128", "ha"),
+    (100, 128, "c64", "b0"),
+    (4096 - 96, 4096, "c64", "ha"),
+])
+def test_zero_padding_fused(n_in, n, dtype, kind):
+    """Fused zero-padding: the first pass reads the n_in x
+    n_in input as the centred window of the n x n grid; equals the oracle on
+    oracle.operators.zero_pad(x, n)."""
+    mr, ir = synth.config_streams(600 + n_in)
+    M = (synth.random_symplectic(mr) if kind == "ha"
+         else synth.b0_matrix4([[0.9, 0.2], [0.1, 1.2]], [[0.4, 0.1], [0.1, -0.6]]))
+    b = 1 if n >= 4096 else 2
+    x = synth.iid_cn(ir, (b, n_in, n_in)).astype(NDT[dtype])
+    dx = math.sqrt(2 * math.pi / n)
+    pl = opl.plan(M)
+    kw = dict(n_in=n_in)
+    if pl["kind"] != "B0":
+        kw["h_fixed"] = pl["h"]
+    xt = torch.from_numpy(x).cuda()
+    with nslct.Plan(n, M, b, dtype=dtype, **kw) as p:
+        G = p.exec(xt).cpu().numpy()
+        info = p.info()
+        if n < 4096:   # host path: input chunks are n_in^2 images
+            hin = torch.from_numpy(x).pin_memory()
+            hout = torch.zeros((b, n, n), dtype=TDT[dtype]).pin_memory()
+            p.exec_host(hin, hout)
+            assert np.array_equal(hout.numpy(), G)
+    assert info["n_in"] == n_in
+    for i in range(b):
+        ref, _ = op.nsdlct(op.zero_pad(x[i].astype(np.complex128), n), M, dx=dx, pl=pl)
+        assert me.rel_l2(G[i], ref) <= TOL[dtype], (n_in, n, i)
