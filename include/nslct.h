@@ -58,8 +58,17 @@ typedef struct nslct_plan_s* nslct_plan_t;
 /* plan variants */
 enum { NSLCT_VARIANT_HA = 0,       /* H by the HA objective of Eq. HA24, search of reading R5     */
        NSLCT_VARIANT_LC = 1,       /* H = (h,0;0,0) or (0,0;0,h) of Eq. LC08/LC10, HA fallback     */
-       NSLCT_VARIANT_FIXED_H = 2   /* H given in nslct_opts.h_fixed (form I: H of M; form II:
+       NSLCT_VARIANT_FIXED_H = 2,  /* H given in nslct_opts.h_fixed (form I: H of M; form II:
                                       H~ = the form-I H of M^-1), e.g. to reproduce another plan */
+       NSLCT_VARIANT_DING = 3      /* Ding's method, the paper's comparison system (Eq. Ding12,
+                                      PAPER.md:556-568): CM(B^-1 A), the 2D DFT
+                                      of the input zero-padded to 2N x 2N ("two-times
+                                      upsampling"), bilinear affine B^-T from that frequency grid
+                                      to the output grid, CM(D B^-1); kind 3, 3 launches.  Needs
+                                      det B != 0 (B = 0 takes the Eq. Intro20 path as for every
+                                      variant); 2N a power of two <= 16384 (c128: 8192) or
+                                      2N <= 4096; no slab or padded form.  Not unitary: an
+                                      approximation of the continuous NsLCT, like the paper's. */
 };
 /* dispatch policies */
 enum { NSLCT_DISPATCH_REVERSIBLE = 0,  /* Eq. Reversible08 + odd tie key (reading R7) */
@@ -156,7 +165,8 @@ nslct_status nslct_exec_pass(nslct_plan_t plan, int pass, const void* in, void* 
                              void* cuda_stream);
 
 typedef struct {
-  int kind;                    /* 0 = B=0 (Eq. Intro20), 1 = form I (Eq. HA28), 2 = form II  */
+  int kind;                    /* 0 = B=0 (Eq. Intro20), 1 = form I (Eq. HA28), 2 = form II,
+                                  3 = Ding (Eq. Ding12; Q[0] = B^-1 A, Q[4] = D B^-1)          */
   int variant;                 /* variant actually used (LC falls back to HA: PAPER.md:840)  */
   int lc_axis;                 /* 0 none, 1 = H=(h,0;0,0) (x), 2 = H=(0,0;0,h) (y)            */
   int n_passes;                /* device passes per transform: 5 (HA, LC with x-axis H),      */

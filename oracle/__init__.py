@@ -20,9 +20,10 @@ Modules
   closed_form -- Hermite-Gaussian inputs (Eq. Acc12/16) and the Gaussian-beam
                  closed form of the continuous NsLCT (derived from Eq. Intro08).
   metrics     -- NMSE (Eq. Acc04 / Add16 / Rev08), relative L2, PSNR.
+  ding        -- Ding's NsDLCT (Eq. Ding12), the paper's comparison system (row F4).
 
 Parity status: every function is pinned by a `-m "not gpu"` test in
 tests/test_oracle_*.py except where its docstring says "parity unpinned"
 (see DESIGN.md "Oracle pins").
 """
-from . import symplectic, planner, operators, direct, closed_form, metrics  # noqa: F401
+from . import symplectic, planner, operators, direct, closed_form, metrics, ding  # noqa: F401

@@ -1684,4 +1684,62 @@ bl_pass_kernel(PassArgs a, BlArgs b) {
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Ding's method (Eq. Ding12), last stage: the
+// bilinear affine transform O_Affine^{B^-T} (Eq. BasicAffine12/16) from the 2N x 2N DFT
+// grid (spacing dw = 2 pi/(2N dx), two-times upsampling) to the N x N
+// output grid (spacing dx), times sqrt(det B^-T) dx^2/(j 2 pi) (the constant of Eq.
+// BasicDFT16) and the output chirp O_CM^{D B^-1}.  The two line passes before it left
+// W (the plain DFT along array indices) of the checkerboarded, chirped, padded input;
+// `checker` = 1 applies the output-side centring checkerboard (-1)^(k + l) per tap
+// (power-of-two grids; the Bluestein DFT is centred already).  Taps outside the grid
+// read 0 (reading R10).  Coordinates in fp64, as in b0_kernel.
+// ---------------------------------------------------------------------------------
+struct DingArgs {
+  const void* in;     // [batch][n2][n2], row index = p (x), column = q (y)
+  void* out;          // [batch][n][n]
+  long long total;    // batch * n * n
+  int n, n2;          // output side, DFT grid side (2n)
+  double d11, d12, d21, d22;   // B^-T
+  double ratio;       // dx / dw
+  double amp_re, amp_im;
+  Phase ph;           // output chirp CM(D B^-1) in (i, j) array indices
+  int checker;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) ding_gather_kernel(DingArgs a) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= a.total) return;
+  const int n = a.n, h = n / 2, n2 = a.n2, h2 = n2 / 2;
+  const long long nn = (long long)n * n, nn2 = (long long)n2 * n2;
+  const long long img = idx / nn;
+  const int i = (int)((idx % nn) / n);
+  const int jj = (int)(idx % n);
+  const double p = (double)(i - h), q = (double)(jj - h);
+  const double p1 = __dmul_rn(__dadd_rn(__dmul_rn(a.d11, p), __dmul_rn(a.d21, q)), a.ratio);
+  const double q1 = __dmul_rn(__dadd_rn(__dmul_rn(a.d12, p), __dmul_rn(a.d22, q)), a.ratio);
+  const double p2 = floor(p1), q2 = floor(q1);
+  const double kk = p1 - p2, lw = q1 - q2;
+  const cpx<T>* __restrict__ g = reinterpret_cast<const cpx<T>*>(a.in) + img * nn2;
+  const long long ia = (long long)p2 + h2, ja = (long long)q2 + h2;
+  auto tap = [&](long long r, long long c) -> cpx<T> {
+    if (r < 0 || r >= n2 || c < 0 || c >= n2) return {T(0), T(0)};
+    const cpx<T> v = g[r * n2 + c];
+    return (a.checker && ((r + c) & 1)) ? cpx<T>{-v.x, -v.y} : v;
+  };
+  const cpx<T> g00 = tap(ia, ja), g01 = tap(ia, ja + 1), g10 = tap(ia + 1, ja), g11 = tap(ia + 1, ja + 1);
+  const T w00 = (T)((1.0 - kk) * (1.0 - lw)), w01 = (T)((1.0 - kk) * lw);
+  const T w10 = (T)(kk * (1.0 - lw)), w11 = (T)(kk * lw);
+  cpx<T> s;
+  s.x = w00 * g00.x + w01 * g01.x + w10 * g10.x + w11 * g11.x;
+  s.y = w00 * g00.y + w01 * g01.y + w10 * g10.y + w11 * g11.y;
+  const uint64_t ui = (uint64_t)i, uj = (uint64_t)jj;
+  const uint64_t t = a.ph.cA * ui * ui + a.ph.cB * ui * uj + a.ph.cC * uj * uj + a.ph.cL * ui +
+                     a.ph.cE * uj + a.ph.cK;
+  const cpx<T> c = chirp_of<T>(t, T(1));
+  const cpx<T> amp = {(T)a.amp_re, (T)a.amp_im};
+  reinterpret_cast<cpx<T>*>(a.out)[idx] = cmul(amp, cmul(c, s));
+}
+
 }  // namespace nslct

@@ -282,6 +282,7 @@ Phase to_phase(const Poly& P, bool line_is_x) {
 struct nslct_plan_s {
   int64_t n = 0, batch = 0;
   int log2n = 0;       // power-of-two plans: log2 N; Bluestein plans: log2 M (FFT length)
+  int64_t nl = 0;      // line length of the passes: N, or 2N for Ding plans
   bool bluestein = false;   // arbitrary N (row F3): every line DFT by Bluestein, length M
   int64_t n_in = 0;         // input side (fused zero-padding when < n)
   size_t in_img_bytes = 0;  // bytes of one input image (n_in^2 elements)
@@ -310,6 +311,7 @@ struct nslct_plan_s {
   unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
   int num_sms = 148;
   nslct::B0Args b0{};
+  nslct::DingArgs ding{};
   struct EvSet {
     cudaEvent_t e[6];
   };
@@ -402,7 +404,7 @@ void host_fft(std::vector<double>& re, std::vector<double>& im) {
 // M = 2^log2n:  bq[i] = exp(-j pi (i-h)^2/N), bhat = FFT_M(c)/M with
 // c[k mod M] = exp(+j pi k^2/N) for |k| < N.  Phases reduced exactly: k^2 mod 2N.
 nslct_status bluestein_tables(nslct_plan_s* pl) {
-  const int64_t n = pl->n, m = int64_t(1) << pl->log2n, h = n / 2;
+  const int64_t n = pl->nl, m = int64_t(1) << pl->log2n, h = n / 2;
   std::vector<double> bre(n), bim(n), cre(m, 0.0), cim(m, 0.0);
   for (int64_t i = 0; i < n; ++i) {
     const int64_t d = i - h;
@@ -491,7 +493,7 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
     nslct_opts_default(&o);
   if (dtype != NSLCT_C64 && dtype != NSLCT_C128) return fail(NSLCT_E_ARG, "bad dtype");
   if (batch < 1) return fail(NSLCT_E_ARG, "batch must be >= 1");
-  if (o.variant < 0 || o.variant > 2 || o.dispatch < 0 || o.dispatch > 1 || o.schedule < 0 || o.schedule > 2)
+  if (o.variant < 0 || o.variant > 3 || o.dispatch < 0 || o.dispatch > 1 || o.schedule < 0 || o.schedule > 2)
     return fail(NSLCT_E_ARG, "bad variant/dispatch option");
   int lg = 0;
   while ((int64_t(1) << lg) < n && lg < 62) ++lg;
@@ -525,13 +527,29 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
   if (st) return fail((nslct_status)st, err);
   if (slab && p.kind == 0) return fail(NSLCT_E_ARG, "B = 0 has no row-slab form");
   if (slab && (!pow2 || n_in != n)) return fail(NSLCT_E_ARG, "row-slab plans need a power-of-two N and no padding");
+  if (p.kind == 3 && (slab || n_in != n)) return fail(NSLCT_E_ARG, "Ding plans have no row-slab or padded form");
+  // line length of the passes: n, or 2n for Ding's two-times upsampled DFT
+  const int64_t nl = (p.kind == 3) ? 2 * n : n;
+  bool pow2l = pow2;
+  if (p.kind == 3) {
+    lg = 0;
+    while ((int64_t(1) << lg) < nl && lg < 62) ++lg;
+    pow2l = (int64_t(1) << lg) == nl && lg >= kMinLog && lg <= kMaxLog && !(dtype == NSLCT_C128 && lg > kMaxLog128);
+    if (!pow2l) {
+      if (nl > kBlMaxN)
+        return fail(NSLCT_E_UNSUPPORTED_N, "Ding plans: 2N must be a power of two <= 16384 (c128: 8192) or <= 4096");
+      lg = nslct::kBlMinLog;
+      while ((int64_t(1) << lg) < 2 * nl - 1) ++lg;
+    }
+  }
 
   nslct_plan_s* pl = new (std::nothrow) nslct_plan_s();
   if (!pl) return fail(NSLCT_E_OOM, "host allocation failed");
   pl->n = n;
   pl->batch = batch;
   pl->log2n = lg;
-  pl->bluestein = !pow2;
+  pl->nl = nl;
+  pl->bluestein = !pow2l;
   pl->n_in = n_in;
   pl->dtype = dtype;
   pl->p = p;
@@ -619,7 +637,8 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       }
     }
     if (!slab) {
-      cudaError_t e = cudaMalloc(&pl->scratch, pl->bytes);
+      const size_t sb = (p.kind == 3) ? 2 * (size_t)batch * (size_t)nl * (size_t)nl * pl->elem : pl->bytes;
+      cudaError_t e = cudaMalloc(&pl->scratch, sb);
       if (e != cudaSuccess) {
         result = fail(e == cudaErrorMemoryAllocation ? NSLCT_E_OOM : NSLCT_E_CUDA,
                       std::string("scratch: ") + cudaGetErrorString(e));
@@ -695,12 +714,47 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       pl->args[k].n_in = (k == 0 && n_in != n) ? (int)n_in : 0;
       pl->args[k].in_off = (k == 0 && n_in != n) ? (int)(n / 2 - n_in / 2) : 0;
     }
+    if (p.kind == 3) {
+      // Ding (Eq. Ding12): pass 0 = CM(B^-1 A) on the input zero-padded to 2N x 2N (+ the
+      // input-side centring checkerboard on power-of-two grids), W_y; pass 1 = W_x; then
+      // the gather (kernels.cuh ding_gather_kernel) from the 2N grid to the N x N output.
+      Poly Pa = chirp_poly(p.Q[0], dx, (int)nl, ck);
+      for (int k = 0; k < 2; ++k) {
+        PassArgs& a = pl->args[k];
+        a = PassArgs{};
+        a.tw = pl->tw;
+        a.ph = (k == 0) ? to_phase(Pa, true) : Phase{};
+        a.scale = 1.0;
+        a.sign_only = 0;
+        a.lines_per_img = (int)nl;
+        a.in_chunk = (int)nl;
+        a.in_chunk_stride = nl * nl;
+        a.n_lines = batch * nl;
+        a.n_in = (k == 0) ? (int)n : 0;
+        a.in_off = (k == 0) ? (int)(nl / 2 - n / 2) : 0;
+      }
+      pl->n_passes = 3;   // two line passes + the gather
+      pl->mode[0] = pl->mode[1] = 0;
+      nslct::DingArgs& d = pl->ding;
+      d.n = (int)n;
+      d.n2 = (int)nl;
+      d.d11 = p.Db.a; d.d12 = p.Db.b; d.d21 = p.Db.c; d.d22 = p.Db.d;
+      const double dwl = 2.0 * M_PI / ((double)nl * dx);   // DFT grid of the upsampled F
+      d.ratio = dx / dwl;
+      const double detD = p.Db.a * p.Db.d - p.Db.b * p.Db.c;
+      const double sr = detD >= 0 ? std::sqrt(detD) : 0.0, si = detD >= 0 ? 0.0 : std::sqrt(-detD);
+      const double c = dx * dx / (2.0 * M_PI);                // dx dy / (j 2 pi) = -j c
+      d.amp_re = si * c;
+      d.amp_im = -sr * c;
+      d.ph = to_phase(chirp_poly(p.Q[4], dx, (int)n, false), true);
+      d.checker = ck ? 1 : 0;
+    }
     {
       int sms = 0;
       if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device) == cudaSuccess && sms > 0)
         pl->num_sms = sms;
       const char* np = std::getenv("NSLCT_NO_PIPE");
-      const bool plain = pow2 && n_in == n;   // neither Bluestein nor padded
+      const bool plain = pow2 && n_in == n && p.kind != 3;   // neither Bluestein, padded nor Ding
       pl->pipe = (plain && !slab && ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
       const char* f64 = std::getenv("NSLCT_FFT64");
       pl->fft64 = pl->pipe && lg == 12 && f64 && f64[0] == '1';
@@ -774,10 +828,13 @@ static nslct_status launch_pipe_pass(nslct_plan_t pl, int k, const PassArgs& a, 
   return NSLCT_OK;
 }
 
-// The passes of `nimg` consecutive images (in/out/scratch already offset to the first).
-static nslct_status run_images(nslct_plan_t pl, const void* in, void* out, void* scratch, int64_t nimg,
+// The passes of `nimg` consecutive images starting at image img0 of the plan's batch
+// (in/out already offset to image img0; the scratch is offset here).
+static nslct_status run_images(nslct_plan_t pl, const void* in, void* out, int64_t img0, int64_t nimg,
                                cudaStream_t s, bool profile) {
   const int ti = (pl->dtype == NSLCT_C64) ? 0 : 1;
+  unsigned char* sbase = static_cast<unsigned char*>(pl->scratch);
+  void* scratch = sbase ? sbase + (size_t)img0 * (size_t)pl->nl * (size_t)pl->nl * pl->elem : nullptr;
   cudaEvent_t* ev = nullptr;
   if (profile) {
     if (pl->ev_used == pl->ev.size()) {
@@ -821,6 +878,42 @@ static nslct_status run_images(nslct_plan_t pl, const void* in, void* out, void*
     CUDA_TRY(table().li[ti][pl->log2n](ia, s, nimg));
     if (ev) {
       CUDA_TRY(cudaEventRecord(ev[1], s));
+      ++pl->ev_used;
+    }
+    return NSLCT_OK;
+  }
+  if (pl->p.kind == 3) {   // Ding: two line passes of length 2N, then the affine gather
+    const size_t img2 = (size_t)pl->nl * (size_t)pl->nl * pl->elem;
+    void* s1 = scratch;
+    void* s2 = sbase + (size_t)pl->batch * img2 + (size_t)img0 * img2;
+    nslct::BlArgs bl{pl->bq, pl->bhat, (int)pl->nl};
+    const void* src = in;
+    for (int k = 0; k < 2; ++k) {
+      void* dst = (k == 0) ? s1 : s2;
+      if (ev) CUDA_TRY(cudaEventRecord(ev[k], s));
+      PassArgs a = pl->args[k];
+      a.in = src;
+      a.out = dst;
+      a.n_lines = nimg * pl->nl;
+      if (pl->bluestein)
+        CUDA_TRY(nslct::bl_launcher(ti, pl->log2n, 0)(a, bl, nimg, s));
+      else
+        CUDA_TRY(table().l[ti][pl->log2n][0](a, s));
+      src = dst;
+    }
+    nslct::DingArgs d = pl->ding;
+    d.in = s2;
+    d.out = out;
+    d.total = nimg * pl->n * pl->n;
+    const long long blocks = (d.total + 255) / 256;
+    if (ev) CUDA_TRY(cudaEventRecord(ev[2], s));
+    if (ti == 0)
+      nslct::ding_gather_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(d);
+    else
+      nslct::ding_gather_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(d);
+    CUDA_TRY(cudaGetLastError());
+    if (ev) {
+      CUDA_TRY(cudaEventRecord(ev[3], s));
       ++pl->ev_used;
     }
     return NSLCT_OK;
@@ -880,7 +973,7 @@ nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream
   if (pl->slab) return fail(NSLCT_E_ARG, "slab plans run pass by pass: nslct_exec_pass");
   if (pl->n_in != pl->n && in == out) return fail(NSLCT_E_ARG, "a padded plan cannot run in place");
   DeviceGuard guard(pl->device);
-  return run_images(pl, in, out, pl->scratch, pl->batch, reinterpret_cast<cudaStream_t>(stream),
+  return run_images(pl, in, out, 0, pl->batch, reinterpret_cast<cudaStream_t>(stream),
                     pl->profile != 0);
 }
 
@@ -890,6 +983,7 @@ nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* ou
   if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(NSLCT_E_ARG, "in/out must be 16-byte aligned");
   if (pl->p.kind == 0) return fail(NSLCT_E_ARG, "the B = 0 plan has a single pass: use nslct_exec");
+  if (pl->p.kind == 3) return fail(NSLCT_E_ARG, "Ding plans run through nslct_exec");
   if (pass < 0 || pass >= pl->n_passes) return fail(NSLCT_E_ARG, "pass out of range");
   if (pass < pl->n_passes - 1 && in == out) return fail(NSLCT_E_ARG, "transposing passes cannot run in place");
   DeviceGuard guard(pl->device);
@@ -953,12 +1047,11 @@ nslct_status nslct_exec_host(nslct_plan_t pl, const void* host_in, void* host_ou
     const size_t off_in = (size_t)i0 * pl->in_img_bytes, len_in = (size_t)ni * pl->in_img_bytes;
     unsigned char* din = static_cast<unsigned char*>(pl->h_in) + off_in;
     unsigned char* dout = static_cast<unsigned char*>(pl->h_out) + off;
-    void* dscr = pl->scratch ? static_cast<void*>(static_cast<unsigned char*>(pl->scratch) + off) : nullptr;
     CUDA_TRY(cudaMemcpyAsync(din, static_cast<const unsigned char*>(host_in) + off_in, len_in,
                              cudaMemcpyHostToDevice, pl->cs_in));
     CUDA_TRY(cudaEventRecord(pl->cev[2 * i], pl->cs_in));
     CUDA_TRY(cudaStreamWaitEvent(s, pl->cev[2 * i], 0));
-    nslct_status st = run_images(pl, din, dout, dscr, ni, s, false);
+    nslct_status st = run_images(pl, din, dout, i0, ni, s, false);
     if (st != NSLCT_OK) return st;
     CUDA_TRY(cudaEventRecord(pl->cev[2 * i + 1], s));
     CUDA_TRY(cudaStreamWaitEvent(pl->cs_out, pl->cev[2 * i + 1], 0));
@@ -975,7 +1068,7 @@ static void describe(const nslct::Plan& p, double dx, nslct_plan_desc* d) {
   d->kind = p.kind;
   d->variant = p.variant;
   d->lc_axis = p.lc_axis;
-  d->n_passes = (p.kind == 0) ? 1 : lc_y(p) ? 3 : 5;
+  d->n_passes = (p.kind == 0) ? 1 : (p.kind == 3 || lc_y(p)) ? 3 : 5;
   auto put = [](double* o, const nslct::Sym& s) {
     o[0] = s.q11;
     o[1] = s.q22;
@@ -1016,7 +1109,7 @@ nslct_status nslct_plan_describe(int64_t n, const double abcd[16], const nslct_o
   else
     nslct_opts_default(&o);
   if (n < 2) return fail(NSLCT_E_ARG, "n must be >= 2");
-  if (o.variant < 0 || o.variant > 2 || o.dispatch < 0 || o.dispatch > 1 || o.schedule < 0 || o.schedule > 2)
+  if (o.variant < 0 || o.variant > 3 || o.dispatch < 0 || o.dispatch > 1 || o.schedule < 0 || o.schedule > 2)
     return fail(NSLCT_E_ARG, "bad variant/dispatch option");
   std::string err;
   nslct::Plan p;

@@ -452,6 +452,41 @@ int make_plan(const double m[16], int variant, int dispatch, const double h_fixe
     *out = p;
     return 0;
   }
+  if (variant == 3) {
+    // Ding's method (Eq. Ding04/Ding12):
+    //   M = (I, 0; D B^-1, I) (B, 0; 0, B^-T) (0, I; -I, 0) (I, 0; B^-1 A, I)
+    // Q[0] = B^-1 A (input CM), Q[4] = D B^-1 (output CM), Db = B^-T (affine matrix).
+    const double dB = det(b.B);
+    if (!(std::fabs(dB) > 1e-12 * std::max(1.0, maxabs(b.B) * maxabs(b.B)))) {
+      *err = "Ding's method needs det B != 0";
+      return 3;
+    }
+    const M2 Bi = inv(b.B);
+    p.kind = 3;
+    p.Q[0] = symm(mul(Bi, b.A));
+    p.Q[4] = symm(mul(b.D, Bi));
+    p.q_active[0] = p.q_active[4] = true;
+    p.Db = tr(Bi);
+    p.Cb = b.C;
+    // recomposition: (B Q0, B; Q4 B Q0 - B^-T, Q4 B)
+    const M2 Q0 = of(p.Q[0]), Q4 = of(p.Q[4]);
+    Blocks r;
+    r.A = mul(b.B, Q0);
+    r.B = b.B;
+    r.C = sub(mul(Q4, mul(b.B, Q0)), tr(Bi));
+    r.D = mul(Q4, b.B);
+    double R[16];
+    unblocks(r, R);
+    double res = 0;
+    for (int i = 0; i < 16; ++i) res = std::max(res, std::fabs(R[i] - m[i]));
+    p.recomposition_residual = res;
+    if (!(res <= 1e-9 * std::max(1.0, mmax))) {
+      *err = "Ding recomposition check failed (residual " + std::to_string(res) + ")";
+      return 3;
+    }
+    *out = p;
+    return 0;
+  }
   p.key = dispatch_key(m);
   bool form1_ = (dispatch == 1) || (p.key >= 0.0);
   double mt[16];

@@ -14,13 +14,13 @@ struct Sym {  // symmetric 2x2 (q11, q22, q12)
 };
 
 struct Plan {
-  int kind = 0;           // 0 = B0, 1 = form I, 2 = form II
-  int variant = 0;        // 0 HA, 1 LC, 2 fixed H
+  int kind = 0;           // 0 = B0, 1 = form I, 2 = form II, 3 = Ding (Eq. Ding12)
+  int variant = 0;        // 0 HA, 1 LC, 2 fixed H, 3 Ding
   int lc_axis = 0;        // 0 none, 1 x, 2 y
   Sym H{}, Bp{}, P2{}, P4{};
   Sym Q[5]{};             // chirps in application order (see nslct.h)
   bool q_active[5]{};     // Q0 / Q4 may be absent
-  M2 Cb{}, Db{};          // B = 0: C and D
+  M2 Cb{}, Db{};          // B = 0: C and D; Ding: Db = B^-T
   double objective = 0, sym_residual = 0, recomposition_residual = 0, key = 0;
 };
 

@@ -14,11 +14,11 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libnslct.so")
 
 C64, C128 = 0, 1
-VARIANTS = {"HA": 0, "LC": 1, "FIXED_H": 2}
+VARIANTS = {"HA": 0, "LC": 1, "FIXED_H": 2, "DING": 3}
 DISPATCH = {"reversible": 0, "formI": 1}
 STATUS = {0: "OK", 1: "E_ARG", 2: "E_NOT_SYMPLECTIC", 3: "E_NO_DECOMP", 4: "E_UNSUPPORTED_N",
           5: "E_CUDA", 6: "E_NCCL", 7: "E_OOM"}
-KINDS = {0: "B0", 1: "I", 2: "II"}
+KINDS = {0: "B0", 1: "I", 2: "II", 3: "DING"}
 
 # every symbol include/nslct.h declares
 EXPORTS = ("nslct_opts_default", "nslct_plan", "nslct_plan_ex", "nslct_exec", "nslct_exec_host",
@@ -117,7 +117,7 @@ def make_opts(dx=None, variant="HA", dispatch="reversible", h_fixed=None, device
 
 def _desc_dict(d):
     s = lambda a: np.array([[a[0], a[2]], [a[2], a[1]]])
-    return dict(kind=KINDS[d.kind], variant={0: "HA", 1: "LC", 2: "FIXED_H"}[d.variant],
+    return dict(kind=KINDS[d.kind], variant={0: "HA", 1: "LC", 2: "FIXED_H", 3: "DING"}[d.variant],
                 lc_axis={0: None, 1: "x", 2: "y"}[d.lc_axis], n_passes=d.n_passes,
                 h=np.array(list(d.H)), H=s(d.H), Bp=s(d.Bp), P2=s(d.P2), P4=s(d.P4),
                 Q=[s(d.Q[i]) for i in range(5)], dx=d.dx, objective=d.objective,

@@ -623,3 +623,48 @@ def test_zero_padding_fused(n_in, n, dtype, kind):
     for i in range(b):
         ref, _ = op.nsdlct(op.zero_pad(x[i].astype(np.complex128), n), M, dx=dx, pl=pl)
         assert me.rel_l2(G[i], ref) <= TOL[dtype], (n_in, n, i)
+
+
+# ------------------------------------------------------------------ row F4: Ding's method
+from oracle import ding as odg  # noqa: E402
+
+
+@pytest.mark.parametrize("n,dtype", [(16, "c64"), (32, "c128"), (50, "c64"), (100, "c128"), (256, "c64"),
+                                     (1024, "c64")])
+def test_ding_method(n, dtype):
+    """Ding's NsDLCT (Eq. Ding12) through the C ABI (VARIANT_DING: two
+    line passes of length 2N -- radix-16 for power-of-two 2N, Bluestein otherwise -- and
+    the bilinear affine gather) against oracle.ding on the same inputs."""
+    mr, ir = synth.config_streams(700 + n)
+    M = synth.random_symplectic(mr)
+    b = 2
+    x = synth.iid_cn(ir, (b, n, n)).astype(NDT[dtype])
+    xt = torch.from_numpy(x).cuda()
+    with nslct.Plan(n, M, b, dtype=dtype, variant="DING") as p:
+        G = p.exec(xt).cpu().numpy()
+        info = p.info()
+        hin = torch.from_numpy(x).pin_memory()
+        hout = torch.zeros_like(hin).pin_memory()
+        p.exec_host(hin, hout)
+        assert np.array_equal(hout.numpy(), G)
+    assert info["kind"] == "DING" and info["n_launches"] == 3
+    for i in range(b):
+        ref = odg.ding(x[i].astype(np.complex128), M)
+        assert me.rel_l2(G[i], ref) <= TOL[dtype], (n, dtype, i, me.rel_l2(G[i], ref))
+
+
+def test_ding_dft_and_errors():
+    """Ding on the DFT matrix equals Eq. BasicDFT16 (numpy.fft); B = 0 takes the B0 path;
+    Ding has no padded form."""
+    n = 64
+    x = synth.iid_cn(np.random.default_rng(5), (1, n, n)).astype(np.complex64)
+    G, info = run_gpu(x, synth.dft_matrix4(), "c64", variant="DING")
+    dx = math.sqrt(2 * math.pi / n)
+    g = x[0].astype(np.complex128)
+    ref = dx * dx / (2j * math.pi) * np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(g)))
+    assert me.rel_l2(G[0], ref) <= 1e-5
+    with nslct.Plan(n, np.eye(4), 1, variant="DING") as p:
+        assert p.info()["kind"] == "B0"
+    with pytest.raises(nslct.NslctError) as e:
+        nslct.Plan(n, synth.dft_matrix4(), 1, variant="DING", n_in=32)
+    assert e.value.name == "E_ARG"
