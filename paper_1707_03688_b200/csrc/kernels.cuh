@@ -898,10 +898,23 @@ __device__ __forceinline__ cpx<double> chirp_of<double>(uint64_t t, double scale
 //   t = cA l^2 + cB l e + cC e^2 + cL l + cE e + cK
 struct Phase {
   uint64_t cA, cB, cC, cL, cE, cK;
+  // complex64 "rotation" evaluation (rec = 1, set by the host per pass): with
+  // t_k = t0 + k d0 + k(k-1)/2 dd along the thread's elements e = j + TL k, the chirp is
+  // exp(2 pi j t0) w^k Z_k, w = exp(2 pi j d0), Z_k = exp(2 pi j k(k-1)/2 dd) -- Z a
+  // per-pass constant (dd = 2 cC TL^2 does not depend on the line or thread) -- evaluated
+  // from two anchors (k = 0 and 8) with 7-step power recurrences: 8 MUFU per thread and
+  // line instead of 32, the rest on the FMA pipe; phases stay exact in fixed point up to
+  // the anchors, the recurrence adds <= 14 fp32 roundings.
+  float zr[8], zi[8];
+  int rec;
 };
 // conj(chirp of t) = chirp of -t
 __device__ __forceinline__ Phase neg_phase(Phase p) {
-  return {0 - p.cA, 0 - p.cB, 0 - p.cC, 0 - p.cL, 0 - p.cE, 0 - p.cK};
+  Phase q = p;
+  q.cA = 0 - p.cA; q.cB = 0 - p.cB; q.cC = 0 - p.cC; q.cL = 0 - p.cL; q.cE = 0 - p.cE; q.cK = 0 - p.cK;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) q.zi[m] = -p.zi[m];
+  return q;
 }
 
 // Multiply the thread's 16 elements (e = j + TL*k) of line l by the chirp.
@@ -931,6 +944,26 @@ __device__ __forceinline__ void apply_chirp(cpx<T> (&v)[16], const Phase& ph, ui
   uint64_t t = alpha + gamma * j + ph.cC * j * j;
   const uint64_t dd = 2ull * ph.cC * (uint64_t)TL * (uint64_t)TL;  // second difference
   uint64_t d = gamma * (uint64_t)TL + 2ull * ph.cC * j * (uint64_t)TL + ph.cC * (uint64_t)TL * (uint64_t)TL;
+  if constexpr (sizeof(T) == 4) {
+    if (ph.rec) {   // anchors k = 0, 8; recurrences P <- P w (see struct Phase)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        cpx<T> P = chirp_of<T>(t, SCALE ? scale : T(1));
+        const cpx<T> w = chirp_of<T>(d, T(1));
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const cpx<T> c = cmul(P, cpx<T>{ph.zr[m], ph.zi[m]});
+          cpx<T> x = v[8 * h + m];
+          if (CONJ_IN) x = cconj(x);
+          v[8 * h + m] = cmul(x, c);
+          if (m < 7) P = cmul(P, w);
+        }
+        t += 8ull * d + 28ull * dd;   // t_8 = t_0 + 8 d_0 + 28 dd
+        d += 8ull * dd;               // d_8 = d_0 + 8 dd
+      }
+      return;
+    }
+  }
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     cpx<T> c = chirp_of<T>(t, SCALE ? scale : T(1));
@@ -971,6 +1004,9 @@ struct PassArgs {
   // elsewhere.  n_in = 0: no padding.  (line_pass_kernel and bl_pass_kernel only.)
   int n_in;
   int in_off;
+  // persistent pipe kernels: when claiming group g, also prefetch group g + l2_ahead into
+  // L2 (the group this CTA will most likely claim next; 0 = off)
+  int l2_ahead;
 };
 
 // The per-line work of one pass (registers v hold elements j + TL*e of line l).
@@ -1178,6 +1214,10 @@ __device__ __forceinline__ void tensor_s2g_4d(const CUtensorMap* map, const void
       "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+// L2 prefetch of a contiguous global range (no shared memory, no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -1368,10 +1408,13 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
       const cpx<T>* in;
       uint64_t* bar;
       long long* s_next;
+      int ahead;
       __device__ __forceinline__ void run() const {
         if (tid == 0) {   // claim and prefetch the next group
           const long long gn = (long long)atomicAdd(counter, 1ull);
           s_next[bn] = gn;
+          if (ahead && gn + ahead < n_groups)   // the group after next, into L2 only
+            bulk_prefetch_l2(in + (gn + ahead) * GE, (uint32_t)(GE * sizeof(cpx<T>)));
           bulk_wait_read0();
           if (gn < n_groups) {
             fence_proxy_async_smem();    // order the generic-proxy uses of the buffer before TMA
@@ -1382,7 +1425,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
         }
       }
     };
-    const Prefetch pf{tid, bn, counter, n_groups, bufs + bn * BE, in, bar, s_next};
+    const Prefetch pf{tid, bn, counter, n_groups, bufs + bn * BE, in, bar, s_next, a.l2_ahead};
     const ExPad2<T, Prefetch> ex{xb + gl * LS, sb + gl * LS, &pf};
     pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ex);
 

@@ -266,9 +266,21 @@ Poly chirp_poly(const nslct::Sym& q, double d, int n, bool checker) {
   }
   return P;
 }
+// Z_m = exp(2 pi j m(m-1)/2 dd), dd = 2 cC TL^2 (mod 2^64), for the rotation evaluation
+// of complex64 chirps (kernels.cuh struct Phase).
+void set_rec(Phase* ph, int tl) {
+  const uint64_t dd = 2ull * ph->cC * (uint64_t)tl * (uint64_t)tl;
+  for (int m = 0; m < 8; ++m) {
+    const uint64_t t = (uint64_t)(m * (m - 1) / 2) * dd;
+    const double ang = 2.0 * M_PI * ((double)(int64_t)t * 5.42101086242752217e-20);   // 2^-64 turns
+    ph->zr[m] = (float)std::cos(ang);
+    ph->zi[m] = (float)std::sin(ang);
+  }
+  ph->rec = 1;
+}
 // roles: line index = i (x) or j (y)
 Phase to_phase(const Poly& P, bool line_is_x) {
-  Phase ph;
+  Phase ph{};
   if (line_is_x) {
     ph.cA = P.A; ph.cB = P.B; ph.cC = P.C; ph.cL = P.Li; ph.cE = P.Lj; ph.cK = P.K;
   } else {
@@ -756,6 +768,36 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       const char* np = std::getenv("NSLCT_NO_PIPE");
       const bool plain = pow2 && n_in == n && p.kind != 3;   // neither Bluestein, padded nor Ding
       pl->pipe = (plain && !slab && ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
+      // L2 prefetch one claim ahead in the persistent kernels: one grid of groups ahead
+      // (the group this CTA most likely claims next).  Measured on the C4 bench (DESIGN.md
+      // §6.6): K1 1.51 -> 1.32 ms, K2-K5 +0.5-1% -- so by default on the first pass only.
+      // NSLCT_L2_AHEAD (groups ahead, 0 = off) and NSLCT_L2_PASSES (bit mask of passes)
+      // override for experiments.
+      if (pl->pipe) {
+        const char* la = std::getenv("NSLCT_L2_AHEAD");
+        const char* lp = std::getenv("NSLCT_L2_PASSES");
+        const int ahead = la ? std::atoi(la) : pl->num_sms;
+        const int mask = lp ? std::atoi(lp) : 1;
+        for (int k = 0; k < 5; ++k) pl->args[k].l2_ahead = ((mask >> k) & 1) ? ahead : 0;
+      }
+      // complex64 chirps by anchored rotation recurrences (kernels.cuh struct Phase):
+      // by default on the one-FFT passes (modes 0, 3), where they measured K5 1.71 ->
+      // 1.66 ms on the C4 bench (the two-FFT passes: +-0.5%); the bit
+      // mask of passes NSLCT_CHIRP_REC overrides.
+      if (ti == 0) {
+        const char* cr = std::getenv("NSLCT_CHIRP_REC");
+        int mask = 0;
+        for (int k = 0; k < 5; ++k)
+          if (pl->mode[k] == 0 || pl->mode[k] == 3) mask |= 1 << k;
+        if (cr) mask = std::atoi(cr);
+        const int tl = (1 << lg) / 16;
+        for (int k = 0; k < 5; ++k)
+          if ((mask >> k) & 1) {
+            set_rec(&pl->args[k].ph, tl);
+            set_rec(&pl->args[k].ph_b, tl);
+            set_rec(&pl->args[k].ph_c, tl);
+          }
+      }
       const char* f64 = std::getenv("NSLCT_FFT64");
       pl->fft64 = pl->pipe && lg == 12 && f64 && f64[0] == '1';
       const bool have = plain && !slab && table().li[ti][lg] != nullptr;
