@@ -11,7 +11,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnslct.so")
+# NSLCT_LIB: an alternative in-tree build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("NSLCT_LIB") or os.path.join(_HERE, "libnslct.so")
 
 C64, C128 = 0, 1
 VARIANTS = {"HA": 0, "LC": 1, "FIXED_H": 2, "DING": 3}

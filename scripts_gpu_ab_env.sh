@@ -5,7 +5,7 @@ cd $GRAFT_REPO_ROOT
 TAG=$1; shift
 for rep in 1 2; do
 for setting in "$@"; do
-  env $setting timeout 300 python bench.py --steps 30 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ab_${TAG}.tmp 2>&1
+  env $setting timeout 300 python bench.py --steps ${STEPS:-30} --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ab_${TAG}.tmp 2>&1
   grep '^{' gpurun_out/ab_${TAG}.tmp | python -c "
 import json,sys
 d=json.loads(sys.stdin.read())
