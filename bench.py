@@ -424,10 +424,21 @@ def run_slab(args, n, M, dtype, desc, world, rank, local, dev):
     x = torch.randn((L, n), dtype=torch.complex64, device=dev, generator=gen)
     out = torch.empty_like(x)
     plan = nslct.SlabPlan(n, M, world, rank, device=local)
-    exchange = nslct.torch_all_to_all()
     stream = torch.cuda.current_stream(dev)
+    if args.exchange == "peer":
+        # the all-to-all fused into the transposing passes' stores (nslct_exec_pass_peer)
+        # into torch symmetric-memory receive buffers over NVLink
+        recv, ptrs, sbar = nslct.symm_mem_exchange(L, n)
+
+        def step():
+            plan.run_peer(x, recv, ptrs, sbar, out, stream)
+    else:
+        exchange = nslct.torch_all_to_all()
+
+        def step():
+            plan.run(x, exchange, out, stream)
     for _ in range(args.warmup):
-        plan.run(x, exchange, out, stream)
+        step()
     torch.cuda.synchronize()
     dist.barrier()
     clocks = ClockSampler(local)
@@ -435,7 +446,7 @@ def run_slab(args, n, M, dtype, desc, world, rank, local, dev):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        plan.run(x, exchange, out, stream)
+        step()
     e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
@@ -452,7 +463,9 @@ def run_slab(args, n, M, dtype, desc, world, rank, local, dev):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": {"workload": desc + ", row slabs of %d x %d per GPU" % (L, n), "n": n, "global_batch": 1,
-                       "parallelism": "row-slab x%d, NCCL all-to-all between passes" % world},
+                       "parallelism": "row-slab x%d, %s" % (world, "all-to-all fused into the pass stores "
+                                                            "(NVLink peer memory)" if args.exchange == "peer"
+                                                            else "NCCL all-to-all between passes")},
             "roofline": {"bound": "nvlink", "achieved": a2a_bytes_gpu / (ms * 1e-3) / 1e9, "peak": nvlink_gbs,
                          "unit": "GB/s", "frac": a2a_bytes_gpu / (ms * 1e-3) / 1e9 / nvlink_gbs, "traffic": None,
                          "hbm_alg_bytes_per_gpu": hbm_bytes_gpu, "alltoall_bytes_per_gpu_per_dir": a2a_bytes_gpu,
@@ -473,6 +486,9 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", choices=("nccl", "peer"), default="nccl",
+                    help="config 5 under torchrun: NCCL all-to-all between passes, or the exchange "
+                         "fused into the transposing passes' stores to peer memory")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--schedule", default="auto", choices=["auto", "line_passes", "on_chip"],
                     help="on-chip kernel where available (auto) or one launch per pass")

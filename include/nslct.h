@@ -164,6 +164,19 @@ nslct_status nslct_plan_slab(nslct_plan_t* plan, int64_t n, const double abcd[16
 nslct_status nslct_exec_pass(nslct_plan_t plan, int pass, const void* in, void* out,
                              void* cuda_stream);
 
+/* Row-slab pass with the all-to-all FUSED into its store (SURVEY.md §8(e) stretch): pass
+ * `pass` (a transposing pass, 0 <= pass < n_passes - 1) of this rank's slab writes
+ * row-block s of its [n][L] output straight into peer_out[s] -- a device buffer of rank s
+ * (CUDA peer / NVLink memory, e.g. a torch symmetric-memory buffer), n*L elements -- at
+ * element offset rank*L*L: exactly what the all_to_all_single of nslct_exec_pass would have
+ * left in rank s's receive buffer, so the next pass reads it unchanged.  n_peers must equal
+ * nranks (<= 8).  The CALLER orders the exchange: every rank's pass k must have finished
+ * reading the buffers it is about to overwrite (double-buffer the receive buffers across
+ * passes) and a cross-rank barrier must separate pass k's stores from pass k+1's reads.
+ * Asynchronous on cuda_stream; no allocation.  Errors: E_ARG, E_CUDA. */
+nslct_status nslct_exec_pass_peer(nslct_plan_t plan, int pass, const void* in, void* const* peer_out,
+                                  int n_peers, void* cuda_stream);
+
 typedef struct {
   int kind;                    /* 0 = B=0 (Eq. Intro20), 1 = form I (Eq. HA28), 2 = form II,
                                   3 = Ding (Eq. Ding12; Q[0] = B^-1 A, Q[4] = D B^-1)          */

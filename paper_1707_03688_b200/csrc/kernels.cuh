@@ -1007,6 +1007,12 @@ struct PassArgs {
   // persistent pipe kernels: when claiming group g, also prefetch group g + l2_ahead into
   // L2 (the group this CTA will most likely claim next; 0 = off)
   int l2_ahead;
+  // Row-slab mode with the exchange fused into the store (SURVEY.md §8(e) stretch): when
+  // peer_on != 0 the transposing store sends row-block s of its [N][L] output straight
+  // to peer_out[s] (a buffer of rank s, NVLink peer memory across GPUs) at block offset
+  // peer_rank * L * L -- the layout all_to_all_single would have produced there.
+  void* peer_out[8];
+  int peer_on, peer_rank;
 };
 
 // The per-line work of one pass (registers v hold elements j + TL*e of line l).
@@ -1154,12 +1160,24 @@ line_pass_kernel(PassArgs a) {
     for (int e = 0; e < 16; ++e) buf[pad16(j + TL * e)] = v[e];
     __syncthreads();
     const int l0 = (int)(line0 % L);
+    if (a.peer_on) {   // fused exchange: block e / L goes to rank e / L
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const int f = tid + k * THREADS;
-      const int gg = f % G;
-      const int e = f / G;
-      out[(long long)e * L + l0 + gg] = smem[gg * LS + pad16(e)];
+      for (int k = 0; k < 16; ++k) {
+        const int f = tid + k * THREADS;
+        const int gg = f % G;
+        const int e = f / G;
+        const int sblk = e / L;
+        cpx<T>* dst = reinterpret_cast<cpx<T>*>(a.peer_out[sblk]) + (long long)a.peer_rank * L * L;
+        dst[(long long)(e - sblk * L) * L + l0 + gg] = smem[gg * LS + pad16(e)];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int f = tid + k * THREADS;
+        const int gg = f % G;
+        const int e = f / G;
+        out[(long long)e * L + l0 + gg] = smem[gg * LS + pad16(e)];
+      }
     }
   }
 }

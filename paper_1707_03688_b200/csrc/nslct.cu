@@ -1062,6 +1062,31 @@ static int64_t host_chunk_images(const nslct_plan_s* pl) {
   return c;
 }
 
+nslct_status nslct_exec_pass_peer(nslct_plan_t pl, int pass, const void* in, void* const* peer_out, int n_peers,
+                                  void* stream) {
+  if (!pl) return fail(NSLCT_E_ARG, "null plan");
+  if (!pl->slab) return fail(NSLCT_E_ARG, "peer-store passes exist for row-slab plans only");
+  if (!in || !peer_out) return fail(NSLCT_E_ARG, "null pointer");
+  if (n_peers != pl->nranks || n_peers > 8) return fail(NSLCT_E_ARG, "n_peers must equal nranks (<= 8)");
+  if (pass < 0 || pass >= pl->n_passes - 1)
+    return fail(NSLCT_E_ARG, "only the transposing passes (0 .. n_passes-2) exchange");
+  for (int s = 0; s < n_peers; ++s)
+    if (!peer_out[s] || (reinterpret_cast<uintptr_t>(peer_out[s]) & 15))
+      return fail(NSLCT_E_ARG, "peer buffers must be non-null and 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(in) & 15) return fail(NSLCT_E_ARG, "in must be 16-byte aligned");
+  DeviceGuard guard(pl->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int ti = (pl->dtype == NSLCT_C64) ? 0 : 1;
+  PassArgs a = pl->args[pass];
+  a.in = in;
+  a.out = peer_out[pl->rank];
+  a.peer_on = 1;
+  a.peer_rank = pl->rank;
+  for (int r = 0; r < n_peers; ++r) a.peer_out[r] = peer_out[r];
+  CUDA_TRY(table().l[ti][pl->log2n][pl->mode[pass]](a, s));
+  return NSLCT_OK;
+}
+
 nslct_status nslct_exec_host(nslct_plan_t pl, const void* host_in, void* host_out, void* stream) {
   if (!pl) return fail(NSLCT_E_ARG, "null plan");
   if (pl->slab) return fail(NSLCT_E_ARG, "slab plans run pass by pass: nslct_exec_pass");

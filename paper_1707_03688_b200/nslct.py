@@ -24,7 +24,8 @@ KINDS = {0: "B0", 1: "I", 2: "II", 3: "DING"}
 # every symbol include/nslct.h declares
 EXPORTS = ("nslct_opts_default", "nslct_plan", "nslct_plan_ex", "nslct_exec", "nslct_exec_host",
            "nslct_plan_info", "nslct_plan_describe", "nslct_pass_ms", "nslct_destroy",
-           "nslct_last_error", "nslct_abi_version", "nslct_plan_slab", "nslct_exec_pass")
+           "nslct_last_error", "nslct_abi_version", "nslct_plan_slab", "nslct_exec_pass",
+           "nslct_exec_pass_peer")
 
 
 class NslctError(RuntimeError):
@@ -70,6 +71,7 @@ def lib():
         L.nslct_plan_slab.argtypes = [ctypes.POINTER(vp), i64, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(nslct_opts)]
         L.nslct_exec_pass.argtypes = [vp, ctypes.c_int, vp, vp, vp]
+        L.nslct_exec_pass_peer.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(vp), ctypes.c_int, vp]
         L.nslct_exec_host.argtypes = [vp, vp, vp, vp]
         L.nslct_plan_info.argtypes = [vp, ctypes.POINTER(nslct_plan_desc)]
         L.nslct_plan_describe.argtypes = [i64, dp, ctypes.POINTER(nslct_opts), ctypes.POINTER(nslct_plan_desc)]
@@ -79,7 +81,7 @@ def lib():
         L.nslct_abi_version.restype = ctypes.c_int
         for f in ("nslct_plan", "nslct_plan_ex", "nslct_exec", "nslct_exec_host", "nslct_plan_info",
                   "nslct_plan_describe", "nslct_pass_ms", "nslct_destroy", "nslct_plan_slab",
-                  "nslct_exec_pass"):
+                  "nslct_exec_pass", "nslct_exec_pass_peer"):
             getattr(L, f).restype = ctypes.c_int
         _LIB = L
     return _LIB
@@ -240,6 +242,30 @@ class SlabPlan(Plan):
                                      ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(s.cuda_stream)))
         return out
 
+    def exec_pass_peer(self, k, x, peer_ptrs, stream=None):
+        """Transposing pass k with the exchange fused into its store: row-block s goes to
+        peer_ptrs[s] (device pointers, one per rank) at block offset rank*L*L."""
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream(x.device)
+        arr = (ctypes.c_void_p * len(peer_ptrs))(*[int(p) for p in peer_ptrs])
+        _check(lib().nslct_exec_pass_peer(self._h, int(k), ctypes.c_void_p(x.data_ptr()), arr,
+                                          len(peer_ptrs), ctypes.c_void_p(s.cuda_stream)))
+
+    def run_peer(self, x_slab, recv, peer_ptrs, barrier, out=None, stream=None):
+        """The slab transform with every all-to-all fused into the producing pass's store
+        (nslct_exec_pass_peer).  recv: this rank's two receive buffers [L, n] (double
+        buffering across passes); peer_ptrs[b][s]: rank s's receive buffer b; barrier():
+        a stream-ordered cross-rank barrier run after each transposing pass."""
+        import torch
+        out = torch.empty_like(x_slab) if out is None else out
+        cur = x_slab
+        for k in range(self.n_passes - 1):
+            self.exec_pass_peer(k, cur, peer_ptrs[k % 2], stream)
+            barrier()
+            cur = recv[k % 2]
+        self.exec_pass(self.n_passes - 1, cur, out, stream)
+        return out
+
     def run(self, x_slab, exchange, out=None, stream=None):
         """x_slab: contiguous CUDA tensor [L, n] (this rank's rows).  Returns [L, n]."""
         import torch
@@ -269,6 +295,49 @@ def torch_all_to_all(group=None):
     def exchange(send, recv):
         dist.all_to_all_single(recv.view(-1), send.view(-1), group=group)
     return exchange
+
+
+def symm_mem_exchange(L, n, dtype="c64", group=None):
+    """Receive buffers for SlabPlan.run_peer in torch symmetric memory (CUDA peer memory
+    over NVLink on a multi-GPU node): returns (recv, peer_ptrs, barrier).  Multi-GPU only;
+    not exercised by this round's single-GPU tests (the kernel path is, through
+    emulate_slabs_peer)."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+    want = torch.complex64 if dtype == "c64" else torch.complex128
+    grp = group if group is not None else dist.group.WORLD
+    recv, handles = [], []
+    for _ in range(2):
+        b = symm.empty((L, n), dtype=want, device=torch.device("cuda", torch.cuda.current_device()))
+        handles.append(symm.rendezvous(b, grp.group_name))
+        recv.append(b)
+    peer_ptrs = [list(h.buffer_ptrs) for h in handles]
+    return recv, peer_ptrs, (lambda: handles[0].barrier())
+
+
+def emulate_slabs_peer(n, M, x_full, nranks, dtype="c64", **kw):
+    """Single-GPU emulation of the fused peer-store exchange: nranks slab plans run one
+    after another, each transposing pass storing its row-blocks straight into the other
+    "ranks'" receive buffers (all on this GPU; no kernel waits on another).  Returns the
+    assembled [n, n] output."""
+    import torch
+    L = n // nranks
+    plans = [SlabPlan(n, M, nranks, r, dtype=dtype, **kw) for r in range(nranks)]
+    cur = [x_full[r * L:(r + 1) * L].contiguous() for r in range(nranks)]
+    recv = [[torch.empty_like(cur[0]) for _ in range(nranks)] for _ in range(2)]
+    np_ = plans[0].n_passes
+    for k in range(np_ - 1):
+        ptrs = [t.data_ptr() for t in recv[k % 2]]
+        for r in range(nranks):
+            plans[r].exec_pass_peer(k, cur[r], ptrs)
+        cur = recv[k % 2]
+    outs = [torch.empty_like(c) for c in cur]
+    for r in range(nranks):
+        plans[r].exec_pass(np_ - 1, cur[r], outs[r])
+    for p in plans:
+        p.close()
+    return torch.cat(outs, dim=0)
 
 
 def emulate_slabs(n, M, x_full, nranks, dtype="c64", **kw):

@@ -508,6 +508,35 @@ def test_slab_mode_c5_16384_emulated_8_ranks():
     assert rel <= 1e-6, rel
 
 
+@pytest.mark.parametrize("n,nranks,dtype,variant", [(256, 2, "c64", "HA"), (1024, 8, "c128", "HA"),
+                                                     (4096, 4, "c64", "HA"), (1024, 4, "c64", "LC"),
+                                                     (16384, 8, "c64", "HA")])
+def test_slab_fused_peer_exchange_emulated(n, nranks, dtype, variant):
+    """§8(e) stretch: the all-to-all fused into the transposing pass's store
+    (nslct_exec_pass_peer: row-block s written straight into rank s's receive buffer at
+    block offset rank*L*L), emulated on one GPU with every "rank's" receive buffers local.
+    Equals the NCCL-style exchange (emulate_slabs) exactly -- same kernels, same arithmetic,
+    only the store address differs -- and the single-plan transform."""
+    mr, ir = synth.config_streams(80 + n)
+    M = synth.random_symplectic(mr)
+    pl = opl.plan(M, variant=variant)
+    kw = dict(h_fixed=pl["h"]) if variant == "HA" else dict(variant="LC")
+    if n >= 16384:
+        g = torch.Generator(device="cuda")
+        g.manual_seed(7)
+        xt = torch.randn((n, n), dtype=torch.complex64, device="cuda", generator=g)
+    else:
+        xt = torch.from_numpy(synth.iid_cn(ir, (n, n)).astype(NDT[dtype])).cuda()
+    G_peer = nslct.emulate_slabs_peer(n, M, xt, nranks, dtype=dtype, **kw)
+    G_a2a = nslct.emulate_slabs(n, M, xt, nranks, dtype=dtype, **kw)
+    assert torch.equal(G_peer, G_a2a)
+    with nslct.Plan(n, M, 1, dtype=dtype, **kw) as p:
+        G_one = p.exec(xt.view(1, n, n))[0]
+    rel = float(torch.linalg.vector_norm((G_peer - G_one).to(torch.complex128)) /
+                torch.linalg.vector_norm(G_one.to(torch.complex128)))
+    assert rel <= (1e-6 if dtype == "c64" else 1e-13), rel
+
+
 def test_slab_errors():
     M = synth.dft_matrix4()
     with pytest.raises(nslct.NslctError):
