@@ -1509,6 +1509,87 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
 }
 
 // ---------------------------------------------------------------------------------
+// Large-N line pass (N = 8192, 16384; complex64, batched plans): a line is 64-128 KB, so
+// one CTA holds ONE line (G = 1) and the persistent pipe kernels' group of two lines per
+// CTA does not fit.  A CLUSTER of two CTAs takes the two lines of a pair-interleaved
+// group instead (same intermediate layout as the pipe kernels: element mu of line
+// lambda at (lambda/2) 2N + 2 mu + lambda%2):
+//   * input: CTA c reads its line with coalesced per-thread loads (the user's rows in
+//     the first pass; in the others every 8 B of 16, the partner CTA reading the other 8 B
+//     of the same sectors at the same time, so DRAM moves each byte once);
+//   * output: each CTA stages its line in shared memory and, after a cluster barrier,
+//     writes the 32-byte segments [line 0: lambda, lambda+1 | line 1: lambda, lambda+1] of
+//     its half of the lambda pairs, reading the partner's two elements through DSMEM --
+//     full-sector writes, as the pipe kernels' TMA tensor stores (the G = 1
+//     line_pass_kernel wrote scattered 8-byte elements: 1.4 TB/s at N = 16384).
+// ---------------------------------------------------------------------------------
+template <typename T, int LOG2N, int MODE>
+__global__ void __launch_bounds__(LineCfg<LOG2N>::THREADS)
+line_pass_pair_kernel(PassArgs a) {
+  using Cfg = LineCfg<LOG2N>;
+  constexpr int N = Cfg::N, TL = Cfg::TL, LS = Cfg::LS, THREADS = Cfg::THREADS;
+  static_assert(Cfg::G == 1, "one line per CTA");
+  static_assert(sizeof(T) == 4, "complex64 (the 32-byte segments are 2 x float4)");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cpx<T>* buf = reinterpret_cast<cpx<T>*>(smem_raw);
+  uint32_t c;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c));
+  const int tid = threadIdx.x;
+  const int j = tid;
+  const long long line = blockIdx.x;                 // over the batch
+  const long long img = line / N;
+  const int l = (int)(line % N);
+  const long long img_elems = (long long)N * N;
+  const cpx<T>* __restrict__ tw = reinterpret_cast<const cpx<T>*>(a.tw);
+
+  cpx<T> v[16];
+  if constexpr (ModeIO<MODE>::kUserIn) {   // the user's row-major line
+    const cpx<T>* src = reinterpret_cast<const cpx<T>*>(a.in) + img * img_elems + (long long)l * N + j;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = src[TL * e];
+  } else {                                  // pair-interleaved intermediate
+    const cpx<T>* src = reinterpret_cast<const cpx<T>*>(a.in) + img * img_elems + (long long)(l / 2) * 2 * N +
+                        (l % 2) + 2 * j;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = src[2 * TL * e];
+  }
+  TwSet<T, LOG2N> tws;
+  tws.load(tw, j);
+  pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ExPad<T>{buf});
+
+  cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * img_elems;
+  if constexpr (ModeIO<MODE>::kStraightOut) {
+    cpx<T>* dst = out + (long long)l * N;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
+  } else {
+    __syncthreads();   // the FFT's last reads of buf are done
+#pragma unroll
+    for (int e = 0; e < 16; ++e) buf[pad16(j + TL * e)] = v[e];
+    // both CTAs' lines staged (release/acquire across the cluster)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    uint64_t ra[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      asm volatile("mapa.u64 %0, %1, %2;" : "=l"(ra[r]) : "l"(reinterpret_cast<uint64_t>(buf)), "r"(r));
+    const cpx<T>* b0 = reinterpret_cast<const cpx<T>*>(ra[0]);
+    const cpx<T>* b1 = reinterpret_cast<const cpx<T>*>(ra[1]);
+    const int lp = l & ~1;   // line 0 of the pair
+    // lambda pairs q in this CTA's half: segment at (q) 2N + 2 lp, 4 elements
+    for (int q = (int)c * (N / 4) + tid; q < ((int)c + 1) * (N / 4); q += THREADS) {
+      const int e0 = 2 * q;
+      const cpx<T> a0 = b0[pad16(e0)], a1 = b0[pad16(e0 + 1)];
+      const cpx<T> c0 = b1[pad16(e0)], c1 = b1[pad16(e0 + 1)];
+      cpx<T>* d = out + (long long)q * 2 * N + 2 * lp;
+      reinterpret_cast<float4*>(d)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
+      reinterpret_cast<float4*>(d)[1] = make_float4(c0.x, c0.y, c1.x, c1.y);
+    }
+    // the partner may still read this CTA's buffer
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // Fully on-chip small-N transform.  One CTA -- or a thread-block
 // cluster of C CTAs sharing their shared memory (DSMEM) -- holds one image and runs every
 // pass of the schedule on it, so the image crosses HBM once each way instead of once per

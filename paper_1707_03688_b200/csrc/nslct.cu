@@ -57,6 +57,40 @@ cudaError_t set_attr() {
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
+// large-N pair kernels (N = 8192, 16384, complex64): a 2-CTA cluster per line pair
+template <int LOG2N, int MODE>
+cudaError_t launch_pair(const PassArgs& a, cudaStream_t s) {
+  using Cfg = nslct::LineCfg<LOG2N>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)a.n_lines);
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = (size_t)Cfg::LS * sizeof(nslct::cpx<float>);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair_kernel<float, LOG2N, MODE>, a);
+}
+template <int LOG2N, int MODE>
+cudaError_t set_attr_pair() {
+  using Cfg = nslct::LineCfg<LOG2N>;
+  return cudaFuncSetAttribute(nslct::line_pass_pair_kernel<float, LOG2N, MODE>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Cfg::LS * sizeof(nslct::cpx<float>)));
+}
+template <int LOG2N>
+struct PairRow {
+  static void fill(launch_fn* l, attr_fn* at) {
+    l[0] = launch_pair<LOG2N, 0>; l[1] = launch_pair<LOG2N, 1>; l[2] = launch_pair<LOG2N, 2>;
+    l[3] = launch_pair<LOG2N, 3>; l[4] = launch_pair<LOG2N, 4>; l[5] = launch_pair<LOG2N, 5>;
+    at[0] = set_attr_pair<LOG2N, 0>; at[1] = set_attr_pair<LOG2N, 1>; at[2] = set_attr_pair<LOG2N, 2>;
+    at[3] = set_attr_pair<LOG2N, 3>; at[4] = set_attr_pair<LOG2N, 4>; at[5] = set_attr_pair<LOG2N, 5>;
+  }
+};
+
 // persistent TMA-pipelined variant: grid = #SMs (one CTA per SM)
 constexpr size_t kPipeExtra = 64;   // 3 mbarriers + 3 claimed-group slots + TMEM base
 template <typename T, int LOG2N, int MODE, bool F64 = false>
@@ -186,6 +220,8 @@ struct Table {
   attr_fn ati[2][kMaxLog + 1] = {};
   launch_fn l[2][kMaxLog + 1][kModes] = {};
   attr_fn at[2][kMaxLog + 1][kModes] = {};
+  launch_fn lpair[kMaxLog + 1][kModes] = {};   // c64 N = 8192, 16384 (cluster pairs)
+  attr_fn atpair[kMaxLog + 1][kModes] = {};
   pipe_fn lp[kMaxLog + 1][kModes] = {};   // c64 only
   attr_fn atp[kMaxLog + 1][kModes] = {};
   pipe_fn lp64[kModes] = {launch_pipe<float, 12, 0, true>, launch_pipe<float, 12, 1, true>,
@@ -202,6 +238,8 @@ struct Table {
     li[1][5] = launch_img<double, 5, 1>, ati[1][5] = set_attr_img<double, 5, 1>;
     li[1][6] = launch_img<double, 6, 1>, ati[1][6] = set_attr_img<double, 6, 1>;
     li[1][7] = launch_img<double, 7, 4>, ati[1][7] = set_attr_img<double, 7, 4>;
+    PairRow<13>::fill(lpair[13], atpair[13]);
+    PairRow<14>::fill(lpair[14], atpair[14]);
     PipeRow<float, 10>::fill(lp[10], atp[10]);
     PipeRow<float, 11>::fill(lp[11], atp[11]);
     PipeRow<float, 12>::fill(lp[12], atp[12]);
@@ -320,6 +358,7 @@ struct nslct_plan_s {
   bool pipe = false;   // persistent TMA-pipelined kernels
   bool image = false;  // fully on-chip kernel (one launch per exec)
   bool fft64 = false;  // pipe kernels with the 64x64 TMEM-exchange FFT (N = 4096, opt-in)
+  bool pair = false;   // large-N cluster-pair line passes (N = 8192, 16384, complex64)
   unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
   int num_sms = 148;
   nslct::B0Args b0{};
@@ -798,6 +837,16 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
             set_rec(&pl->args[k].ph_c, tl);
           }
       }
+      const char* npair = std::getenv("NSLCT_NO_PAIR");
+      pl->pair = plain && !slab && ti == 0 && (lg == 13 || lg == 14) && !(npair && npair[0] == '1');
+      for (int m = 0; m < kModes && pl->pair; ++m) {
+        cudaError_t e = table().atpair[lg][m]();
+        if (e != cudaSuccess) {
+          result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(pair): ") + cudaGetErrorString(e));
+          break;
+        }
+      }
+      if (result != NSLCT_OK) break;
       const char* f64 = std::getenv("NSLCT_FFT64");
       pl->fft64 = pl->pipe && lg == 12 && f64 && f64[0] == '1';
       const bool have = plain && !slab && table().li[ti][lg] != nullptr;
@@ -995,6 +1044,8 @@ static nslct_status run_images(nslct_plan_t pl, const void* in, void* out, int64
     if (pl->pipe) {
       nslct_status st = launch_pipe_pass(pl, k, a, s);
       if (st != NSLCT_OK) return st;
+    } else if (pl->pair) {
+      CUDA_TRY(table().lpair[pl->log2n][pl->mode[k]](a, s));
     } else {
       CUDA_TRY(table().l[ti][pl->log2n][pl->mode[k]](a, s));
     }
@@ -1041,6 +1092,8 @@ nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* ou
     CUDA_TRY(cudaMemsetAsync(pl->counters + pass, 0, sizeof(unsigned long long), s));
     nslct_status st = launch_pipe_pass(pl, pass, a, s);
     if (st != NSLCT_OK) return st;
+  } else if (pl->pair) {
+    CUDA_TRY(table().lpair[pl->log2n][pl->mode[pass]](a, s));
   } else {
     CUDA_TRY(table().l[ti][pl->log2n][pl->mode[pass]](a, s));
   }

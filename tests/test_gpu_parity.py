@@ -167,6 +167,32 @@ def test_config5_n16384_properties():
         assert abs(got - ref) <= 1e-4
 
 
+@pytest.mark.parametrize("n,batch,variant", [(8192, 2, "HA"), (16384, 1, "HA"), (8192, 1, "LC")])
+def test_large_n_cluster_pair_kernels(monkeypatch, n, batch, variant):
+    """N = 8192, 16384 (complex64, batched): the 2-CTA cluster-pair line passes (pair-
+    interleaved intermediates, 32-byte segment stores through DSMEM) compute exactly what
+    the one-line-per-CTA passes compute -- same butterflies and chirps, only the
+    intermediate layout differs -- so the results are bit-identical; the plan with the
+    inverse matrix brings the input back (P5)."""
+    mr, ir = synth.config_streams(900 + n)
+    M = synth.random_symplectic(mr)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n)
+    xt = torch.randn((batch, n, n), dtype=torch.complex64, device="cuda", generator=g)
+    kw = dict(variant=variant)
+    with nslct.Plan(n, M, batch, **kw) as p, nslct.Plan(n, sy.inverse(M), batch, **kw) as pi:
+        G = p.exec(xt)
+        back = pi.exec(G)
+    rel = float(torch.linalg.vector_norm((back - xt).to(torch.complex128)) /
+                torch.linalg.vector_norm(xt.to(torch.complex128)))
+    assert rel < 1e-5, rel
+    monkeypatch.setenv("NSLCT_NO_PAIR", "1")
+    with nslct.Plan(n, M, batch, **kw) as p:
+        G_line = p.exec(xt)
+    torch.cuda.synchronize()
+    assert torch.equal(G, G_line)
+
+
 # ------------------------------------------------------------------ sweeps and edge cases
 @pytest.mark.parametrize("n", [32, 64, 128, 256, 512, 1024, 2048])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
