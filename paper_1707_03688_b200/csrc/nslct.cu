@@ -819,15 +819,12 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
         const int mask = lp ? std::atoi(lp) : 1;
         for (int k = 0; k < 5; ++k) pl->args[k].l2_ahead = ((mask >> k) & 1) ? ahead : 0;
       }
-      // complex64 chirps by anchored rotation recurrences (kernels.cuh struct Phase):
-      // by default on the one-FFT passes (modes 0, 3), where they measured K5 1.71 ->
-      // 1.66 ms on the C4 bench (the two-FFT passes: +-0.5%); the bit
-      // mask of passes NSLCT_CHIRP_REC overrides.
+      // complex64 chirps by anchored rotation recurrences (kernels.cuh struct Phase) on
+      // every pass: measured K5 1.71 -> 1.66 ms, K2-K4 -1.4..-2% on the C4 bench (DESIGN.md
+      // §6.3); the bit mask of passes NSLCT_CHIRP_REC overrides.
       if (ti == 0) {
         const char* cr = std::getenv("NSLCT_CHIRP_REC");
-        int mask = 0;
-        for (int k = 0; k < 5; ++k)
-          if (pl->mode[k] == 0 || pl->mode[k] == 3) mask |= 1 << k;
+        int mask = 31;
         if (cr) mask = std::atoi(cr);
         const int tl = (1 << lg) / 16;
         for (int k = 0; k < 5; ++k)
