@@ -358,52 +358,6 @@ __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
 template <int PW>
 __device__ __forceinline__ int padw(int i) { return i + PW * (i >> 4); }
 
-// Twiddle powers from shared-memory tables: stage S (>= 1) holds, for every residue
-// m = jp % Ns and r = 1..R-1, exp(-2 pi i m r / (Ns R)) at [S-offset + (r-1) Ns + m]
-// (the entries come from the fp64-accurate global table, so they are exact to rounding).
-// Consecutive lanes read consecutive m: conflict-free.  Used by the persistent kernels,
-// which fill the tables once; it saves the 14 power-generation products per butterfly.
-template <typename T, int LOG2N>
-struct TwTab {
-  static constexpr bool kFft64 = false;
-  static constexpr bool kBluestein = false;
-  using Sh = FftShape<LOG2N>;
-  template <int S>
-  __host__ __device__ static constexpr int off() {
-    if constexpr (S <= 1) {
-      return 0;
-    } else {
-      return off<S - 1>() + Sh::template Ns<S - 1>() * (Sh::template R<S - 1>() - 1);
-    }
-  }
-  __host__ __device__ static constexpr int elems() { return off<Sh::NS>(); }
-  const cpx<T>* tab;
-  template <int S>
-  __device__ __forceinline__ void prefetch() const {}
-  template <int S, int R>
-  __device__ __forceinline__ void apply(cpx<T>* u, int /*b*/, int jp) const {
-    constexpr int Ns = Sh::template Ns<S>();
-    const cpx<T>* t = tab + off<S>() + (jp % Ns);
-#pragma unroll
-    for (int r = 1; r < R; ++r) u[r] = cmul(u[r], t[(r - 1) * Ns]);
-  }
-  // all threads of the CTA: tab[...] = tw[m * r * N/(Ns R)]
-  __device__ static void fill(cpx<T>* tab, const cpx<T>* __restrict__ tw, int tid, int nthreads) {
-    fill_stage<1>(tab, tw, tid, nthreads);
-  }
-  template <int S>
-  __device__ static void fill_stage(cpx<T>* tab, const cpx<T>* __restrict__ tw, int tid, int nthreads) {
-    if constexpr (S < Sh::NS) {
-      constexpr int Ns = Sh::template Ns<S>(), R = Sh::template R<S>();
-      for (int i = tid; i < Ns * (R - 1); i += nthreads) {
-        const int r = i / Ns + 1, m = i % Ns;
-        tab[off<S>() + i] = tw[m * r * (Sh::N / (Ns * R))];
-      }
-      fill_stage<S + 1>(tab, tw, tid, nthreads);
-    }
-  }
-};
-
 // Twiddle powers cached in TENSOR MEMORY (sm_100a).  The persistent c64 kernels issue no
 // MMAs, so TMEM (512 columns x 128 lanes x 32 bit per SM) is free: each thread parks its
 // stage twiddles w^r = exp(-2 pi i k0 r / N) (up to 15 complex = 30 columns per stage, from
@@ -658,11 +612,9 @@ __device__ __forceinline__ void fft64x64(cpx<float> (&v)[16], const TwFft64& t, 
 // memory).  X is the compile-time index of the exchange within the pass.
 //  ExPad: one padded buffer (index i + i/16, N + N/16 per line); write, barrier, read,
 //         barrier.
-//  ExSwz: two unpadded buffers used alternately (exchange X uses buffer X & 1) with an
-//         XOR swizzle of each 16-element group: write, barrier, read -- the next write
-//         goes to the other buffer, so the trailing barrier is not needed.  c is a
-//         per-line constant so the G lines read together by the transposed store hit
-//         distinct banks.  Buffer 0 is the TMA staging buffer of the current group.
+//  ExPad2: two padded buffers used alternately (exchange X uses buffer X & 1): write,
+//         barrier, read -- the next write goes to the other buffer, so the trailing
+//         barrier is not needed.
 template <typename T>
 struct ExPad {
   static constexpr bool kDouble = false;
@@ -695,25 +647,6 @@ struct ExPad2 {   // two padded buffers used alternately: write, barrier, read
     if constexpr (X == 0) hook->run();
   }
 };
-template <typename T, class Hook>
-struct ExSwz {   // two unpadded XOR-swizzled buffers used alternately (see above)
-  static constexpr bool kDouble = true;
-  static constexpr bool kPadded = false;
-  static constexpr int kPadW = 0;
-  cpx<T>* buf0;   // exchanges 0, 2, ...
-  cpx<T>* buf1;   // exchanges 1, 3, ...
-  int c;          // per-line swizzle constant
-  const Hook* hook;
-  template <int X>
-  __device__ __forceinline__ void sync() const { __syncthreads(); }
-  template <int X>
-  __device__ __forceinline__ cpx<T>* b() const { return (X & 1) ? buf1 : buf0; }
-  __device__ __forceinline__ int idx(int i) const { return i ^ (((i >> 4) + c) & 15); }
-  template <int X>
-  __device__ __forceinline__ void after_barrier() const {
-    if constexpr (X == 0) hook->run();
-  }
-};
 
 template <typename T, int LOG2N, int STAGE, int NS, int X, class E, class TW>
 __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TW& tw, const E& ex) {
@@ -729,7 +662,6 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TW& tw, 
   // or i is a multiple of 16 and k < 16 -- so one base per butterfly/thread plus
   // compile-time offsets (the compiler cannot prove j < TL by itself).
   constexpr bool FAST = E::kPadded && (TL % 16 == 0);
-  constexpr bool FAST_SWZ = !E::kPadded && (TL % 16 == 0);
   constexpr int PW = E::kPadW;
   constexpr int WSTEP = (Ns >= 16) ? Ns + PW * Ns / 16 : Ns;
   constexpr int RSTEP = TL + PW * TL / 16;
@@ -755,20 +687,6 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TW& tw, 
           const int r = (R == 16) ? ((q & 3) * 4 + (q >> 2)) : q;
           wb[r * WSTEP] = u[r];
         }
-      } else if constexpr (FAST_SWZ) {
-        // element idxD + r*Ns; its 16-group index is (idxD >> 4) + r*Ns/16 (Ns >= 16) or
-        // idxD >> 4 (Ns == 1, r < 16); the low 4 bits are (jp & 15) or r.
-        if constexpr (Ns == 1) {
-          cpx<T>* wb = buf + idxD;
-          const int x = ((idxD >> 4) + ex.c) & 15;
-#pragma unroll
-          for (int r = 0; r < R; ++r) wb[r ^ x] = u[r];
-        } else {
-          cpx<T>* wb = buf + (idxD & ~15);
-          const int y = (idxD >> 4) + ex.c, lo = jp & 15;
-#pragma unroll
-          for (int r = 0; r < R; ++r) wb[r * Ns + (lo ^ ((y + r * (Ns / 16)) & 15))] = u[r];
-        }
       } else {
 #pragma unroll
         for (int r = 0; r < R; ++r) buf[ex.idx(idxD + r * Ns)] = u[r];
@@ -786,11 +704,6 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TW& tw, 
         const int e = (q & 3) * 4 + (q >> 2);   // first-layer DFT4 order {n1, n1+4, n1+8, n1+12}
         v[e] = rb[e * RSTEP];
       }
-    } else if constexpr (FAST_SWZ) {
-      // element j + TL e (j < TL): group (j >> 4) + (TL/16) e, low bits j & 15
-      const int y = (j >> 4) + ex.c, lo = j & 15;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = buf[TL * e + (j & ~15) + (lo ^ ((y + (TL / 16) * e) & 15))];
     } else {
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = buf[ex.idx(j + TL * e)];

@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of runtime env settings on the C4 bench: prints value + per-pass ms per setting
-# usage: scripts_gpu_ab_env.sh TAG "VAR=a" "VAR=b" ...
+# usage: tools/gpu/gpu_ab_env.sh TAG "VAR=a" "VAR=b" ...
 cd $GRAFT_REPO_ROOT
 TAG=$1; shift
 for rep in 1 2; do
