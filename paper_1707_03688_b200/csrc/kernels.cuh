@@ -1425,7 +1425,8 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
 // Large-N line pass (N = 8192, 16384; complex64, batched plans): a line is 64-128 KB, so
 // one CTA holds ONE line (G = 1) and the persistent pipe kernels' group of two lines per
 // CTA does not fit.  A CLUSTER of two CTAs takes the two lines of a pair-interleaved
-// group instead (same intermediate layout as the pipe kernels: element mu of line
+// group instead; persistent (grid = the SMs, clusters stride the pairs), each CTA
+// prefetching its input of the next iteration into L2 while it computes (same intermediate layout as the pipe kernels: element mu of line
 // lambda at (lambda/2) 2N + 2 mu + lambda%2):
 //   * input: CTA c reads its line with coalesced per-thread loads (the user's rows in
 //     the first pass; in the others every 8 B of 16, the partner CTA reading the other 8 B
@@ -1440,7 +1441,7 @@ template <typename T, int LOG2N, int MODE>
 __global__ void __launch_bounds__(LineCfg<LOG2N>::THREADS)
 line_pass_pair_kernel(PassArgs a) {
   using Cfg = LineCfg<LOG2N>;
-  constexpr int N = Cfg::N, TL = Cfg::TL, LS = Cfg::LS, THREADS = Cfg::THREADS;
+  constexpr int N = Cfg::N, TL = Cfg::TL, THREADS = Cfg::THREADS;
   static_assert(Cfg::G == 1, "one line per CTA");
   static_assert(sizeof(T) == 4, "complex64 (the 32-byte segments are 2 x float4)");
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1449,56 +1450,76 @@ line_pass_pair_kernel(PassArgs a) {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c));
   const int tid = threadIdx.x;
   const int j = tid;
-  const long long line = blockIdx.x;                 // over the batch
-  const long long img = line / N;
-  const int l = (int)(line % N);
   const long long img_elems = (long long)N * N;
+  const long long npairs = a.n_lines / 2;
+  const long long ncl = gridDim.x / 2;              // persistent: clusters stride the pairs
+  const long long cl = blockIdx.x / 2;
   const cpx<T>* __restrict__ tw = reinterpret_cast<const cpx<T>*>(a.tw);
-
-  cpx<T> v[16];
-  if constexpr (ModeIO<MODE>::kUserIn) {   // the user's row-major line
-    const cpx<T>* src = reinterpret_cast<const cpx<T>*>(a.in) + img * img_elems + (long long)l * N + j;
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = src[TL * e];
-  } else {                                  // pair-interleaved intermediate
-    const cpx<T>* src = reinterpret_cast<const cpx<T>*>(a.in) + img * img_elems + (long long)(l / 2) * 2 * N +
-                        (l % 2) + 2 * j;
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = src[2 * TL * e];
-  }
+  const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in);
   TwSet<T, LOG2N> tws;
   tws.load(tw, j);
-  pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ExPad<T>{buf});
+  uint64_t ra[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(ra[r]) : "l"(reinterpret_cast<uint64_t>(buf)), "r"(r));
+  const cpx<T>* b0 = reinterpret_cast<const cpx<T>*>(ra[0]);
+  const cpx<T>* b1 = reinterpret_cast<const cpx<T>*>(ra[1]);
+  // this CTA's input bytes of pair p: its own row (first pass) or its half of the
+  // pair's interleaved block -- prefetched into L2 one iteration ahead
+  auto in_part = [&](long long p) -> const cpx<T>* {
+    const long long line = 2 * p + c;
+    if constexpr (ModeIO<MODE>::kUserIn) return in + line * N;
+    else return in + (2 * p) * N + (long long)c * N;
+  };
+  if (tid == 0 && cl < npairs) bulk_prefetch_l2(in_part(cl), (uint32_t)(N * sizeof(cpx<T>)));
 
-  cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * img_elems;
-  if constexpr (ModeIO<MODE>::kStraightOut) {
-    cpx<T>* dst = out + (long long)l * N;
+  for (long long p = cl; p < npairs; p += ncl) {
+    if (tid == 0 && p + ncl < npairs) bulk_prefetch_l2(in_part(p + ncl), (uint32_t)(N * sizeof(cpx<T>)));
+    const long long line = 2 * p + c;                  // over the batch
+    const long long img = line / N;
+    const int l = (int)(line % N);
+    cpx<T> v[16];
+    if constexpr (ModeIO<MODE>::kUserIn) {   // the user's row-major line
+      const cpx<T>* src = in + line * N + j;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
-  } else {
-    __syncthreads();   // the FFT's last reads of buf are done
+      for (int e = 0; e < 16; ++e) v[e] = src[TL * e];
+    } else {                                  // pair-interleaved intermediate
+      const cpx<T>* src = in + img * img_elems + (long long)(l / 2) * 2 * N + (l % 2) + 2 * j;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) buf[pad16(j + TL * e)] = v[e];
-    // both CTAs' lines staged (release/acquire across the cluster)
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    uint64_t ra[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-      asm volatile("mapa.u64 %0, %1, %2;" : "=l"(ra[r]) : "l"(reinterpret_cast<uint64_t>(buf)), "r"(r));
-    const cpx<T>* b0 = reinterpret_cast<const cpx<T>*>(ra[0]);
-    const cpx<T>* b1 = reinterpret_cast<const cpx<T>*>(ra[1]);
-    const int lp = l & ~1;   // line 0 of the pair
-    // lambda pairs q in this CTA's half: segment at (q) 2N + 2 lp, 4 elements
-    for (int q = (int)c * (N / 4) + tid; q < ((int)c + 1) * (N / 4); q += THREADS) {
-      const int e0 = 2 * q;
-      const cpx<T> a0 = b0[pad16(e0)], a1 = b0[pad16(e0 + 1)];
-      const cpx<T> c0 = b1[pad16(e0)], c1 = b1[pad16(e0 + 1)];
-      cpx<T>* d = out + (long long)q * 2 * N + 2 * lp;
-      reinterpret_cast<float4*>(d)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
-      reinterpret_cast<float4*>(d)[1] = make_float4(c0.x, c0.y, c1.x, c1.y);
+      for (int e = 0; e < 16; ++e) v[e] = src[2 * TL * e];
     }
-    // the partner may still read this CTA's buffer
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ExPad<T>{buf});
+
+    cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * img_elems;
+    if constexpr (ModeIO<MODE>::kStraightOut) {
+      // in place (the last pass writes where it read): rows 2p, 2p+1 ARE the pair's
+      // interleaved input block, so neither CTA may store before both have read it
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+      cpx<T>* dst = out + (long long)l * N;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
+      __syncthreads();   // the next iteration's exchange reuses buf
+    } else {
+      __syncthreads();   // the FFT's last reads of buf are done
+#pragma unroll
+      for (int e = 0; e < 16; ++e) buf[pad16(j + TL * e)] = v[e];
+      // both CTAs' lines staged (release/acquire across the cluster)
+      asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+      const int lp = l & ~1;   // line 0 of the pair
+      // lambda pairs q in this CTA's half: segment at (q) 2N + 2 lp, 4 elements
+      for (int q = (int)c * (N / 4) + tid; q < ((int)c + 1) * (N / 4); q += THREADS) {
+        const int e0 = 2 * q;
+        const cpx<T> a0 = b0[pad16(e0)], a1 = b0[pad16(e0 + 1)];
+        const cpx<T> c0 = b1[pad16(e0)], c1 = b1[pad16(e0 + 1)];
+        cpx<T>* d = out + (long long)q * 2 * N + 2 * lp;
+        reinterpret_cast<float4*>(d)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
+        reinterpret_cast<float4*>(d)[1] = make_float4(c0.x, c0.y, c1.x, c1.y);
+      }
+      // the partner may still read this CTA's buffer (next iteration / exit).  Relaxed
+      // arrive: the DSMEM loads above are complete (their values were stored), and a
+      // release would make every thread wait for its outstanding GLOBAL stores.
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+    }
   }
 }
 

@@ -169,11 +169,12 @@ def test_config5_n16384_properties():
 
 @pytest.mark.parametrize("n,batch,variant", [(8192, 2, "HA"), (16384, 1, "HA"), (8192, 1, "LC")])
 def test_large_n_cluster_pair_kernels(monkeypatch, n, batch, variant):
-    """N = 8192, 16384 (complex64, batched): the 2-CTA cluster-pair line passes (pair-
-    interleaved intermediates, 32-byte segment stores through DSMEM) compute exactly what
-    the one-line-per-CTA passes compute -- same butterflies and chirps, only the
-    intermediate layout differs -- so the results are bit-identical; the plan with the
-    inverse matrix brings the input back (P5)."""
+    """N = 8192, 16384 (complex64, batched): the persistent 2-CTA cluster-pair line passes
+    (pair-interleaved intermediates, 32-byte segment stores through DSMEM) compute what the
+    one-line-per-CTA passes compute -- same butterflies and chirps, only the intermediate
+    layout differs, so they agree to rounding (the two instantiations may contract
+    multiply-adds differently; a layout error would be O(1)); the plan with the inverse
+    matrix brings the input back (P5)."""
     mr, ir = synth.config_streams(900 + n)
     M = synth.random_symplectic(mr)
     g = torch.Generator(device="cuda")
@@ -190,7 +191,9 @@ def test_large_n_cluster_pair_kernels(monkeypatch, n, batch, variant):
     with nslct.Plan(n, M, batch, **kw) as p:
         G_line = p.exec(xt)
     torch.cuda.synchronize()
-    assert torch.equal(G, G_line)
+    d = float(torch.linalg.vector_norm((G - G_line).to(torch.complex128)) /
+              torch.linalg.vector_norm(G_line.to(torch.complex128)))
+    assert d <= 1e-6, d
 
 
 # ------------------------------------------------------------------ sweeps and edge cases
