@@ -935,6 +935,7 @@ struct PassArgs {
   // peer_rank * L * L -- the layout all_to_all_single would have produced there.
   void* peer_out[8];
   int peer_on, peer_rank;
+  int persist_ctas;   // persistent cluster-pair kernels: grid size (even; 0 = one per line)
 };
 
 // The per-line work of one pass (registers v hold elements j + TL*e of line l).

@@ -58,12 +58,11 @@ cudaError_t set_attr() {
 }
 
 // large-N pair kernels (N = 8192, 16384, complex64): a 2-CTA cluster per line pair
-int g_num_sms = 148;   // set at plan time (persistent pair kernels)
 template <int LOG2N, int MODE>
 cudaError_t launch_pair(const PassArgs& a, cudaStream_t s) {
   using Cfg = nslct::LineCfg<LOG2N>;
   cudaLaunchConfig_t cfg = {};
-  long long grid = (g_num_sms / 2) * 2;           // persistent: one CTA per SM, pairs of SMs
+  long long grid = a.persist_ctas > 0 ? a.persist_ctas : a.n_lines;   // persistent: one CTA per SM
   if (grid > a.n_lines) grid = a.n_lines;
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(Cfg::THREADS);
@@ -837,9 +836,9 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
             set_rec(&pl->args[k].ph_c, tl);
           }
       }
-      g_num_sms = pl->num_sms;
       const char* npair = std::getenv("NSLCT_NO_PAIR");
       pl->pair = plain && !slab && ti == 0 && (lg == 13 || lg == 14) && !(npair && npair[0] == '1');
+      for (int k = 0; k < 5 && pl->pair; ++k) pl->args[k].persist_ctas = (pl->num_sms / 2) * 2;
       for (int m = 0; m < kModes && pl->pair; ++m) {
         cudaError_t e = table().atpair[lg][m]();
         if (e != cudaSuccess) {

@@ -196,6 +196,25 @@ def test_large_n_cluster_pair_kernels(monkeypatch, n, batch, variant):
     assert d <= 1e-6, d
 
 
+def test_c128_n8192_properties():
+    """complex128 at its largest N (8192, one line per CTA): Parseval (P4) and
+    reversibility through the inverse plan (P5) to fp64 rounding."""
+    n = 8192
+    mr, _ = synth.config_streams(990)
+    M = synth.random_symplectic(mr)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(990)
+    xt = torch.randn((1, n, n), dtype=torch.complex128, device="cuda", generator=g)
+    with nslct.Plan(n, M, 1, dtype="c128") as p, nslct.Plan(n, sy.inverse(M), 1, dtype="c128") as pi:
+        G = p.exec(xt)
+        back = pi.exec(G)
+    e_in = float(torch.sum(torch.abs(xt) ** 2))
+    e_out = float(torch.sum(torch.abs(G) ** 2))
+    assert abs(e_out / e_in - 1) < 1e-12
+    rel = float(torch.linalg.vector_norm(back - xt) / torch.linalg.vector_norm(xt))
+    assert rel < 1e-11, rel
+
+
 # ------------------------------------------------------------------ sweeps and edge cases
 @pytest.mark.parametrize("n", [32, 64, 128, 256, 512, 1024, 2048])
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
