@@ -745,3 +745,61 @@ def test_ding_dft_and_errors():
     with pytest.raises(nslct.NslctError) as e:
         nslct.Plan(n, synth.dft_matrix4(), 1, variant="DING", n_in=32)
     assert e.value.name == "E_ARG"
+
+
+# ------------------------------------------------------------------ the paper's own examples on the GPU
+import json as _json  # noqa: E402
+import os as _os  # noqa: E402
+
+from oracle import closed_form as _cf  # noqa: E402
+from oracle import direct as _od  # noqa: E402
+
+_GOLD = _json.load(open(_os.path.join(_os.path.dirname(__file__), "golden", "paper_examples.json")))
+
+
+@pytest.mark.parametrize("ex,variant", [("E1", "HA"), ("E1", "LC"), ("E2", "HA"), ("E2", "LC")])
+def test_paper_accuracy_examples_on_gpu(ex, variant):
+    """The paper's accuracy experiments run on the GPU: g1 (N = 100,
+    dx = 0.25) and g2 (N = 165, dx = 0.2) -- non-power-of-two N, so the Bluestein line
+    passes -- through A1 / A2 in complex128 (form-I dispatch, reading R8).  The GPU output
+    equals the oracle to 1e-10 and its NMSE against the direct-method truth (1024^2,
+    dx = 0.078) reproduces the printed HA / LC values within x1.5."""
+    e = _GOLD[ex]
+    gi, t = _GOLD[e["input"]], _GOLD["truth"]
+    M = sy.polar_project(np.array(_GOLD[e["M"]]["M"], float))
+    g = _cf.hg2d(gi["orders"], gi["n"], gi["dx"])
+    n = gi["n"]
+    x = g[None].astype(np.complex128)
+    pl = opl.plan(M, variant=variant, policy="formI")
+    kw = dict(dx=gi["dx"], dispatch="formI", h_fixed=pl["h"])   # the oracle's H (LC: Eq. LC08/10)
+    G, info = run_gpu(x, M, "c128", **kw)
+    ref, _ = op.nsdlct(g, M, gi["dx"], variant=variant, policy="formI", pl=pl)
+    assert me.rel_l2(G[0], ref) <= 1e-10
+    truth = _od.direct(_cf.hg2d(gi["orders"], t["n"], t["dx"]), M, t["dx"], dx_out=gi["dx"], n_out=n)
+    val = me.nmse_pm(G[0], truth)
+    assert e[variant] / 1.5 <= val <= e[variant] * 1.5, (ex, variant, val)
+    assert info["fft_len"] == fft_len(n)
+
+
+@pytest.mark.parametrize("dn", [0, 24, 50])
+def test_paper_padding_sweep_on_gpu(dn):
+    """E3 on the GPU: g2 (N = 165) zero-padded by dN inside the first pass (opts.n_in) and
+    transformed at N' = 165 + dN by the Bluestein passes (complex128, A2, form I): equals
+    the oracle on the padded field, and its NMSE against the direct-method truth on the
+    N' x N' output grid falls with dN as the oracle's does (tests/test_oracle_pins.py::
+    test_f3_e3_padding_sweep_g2: 1.1e-3, 8e-7, 2e-8 at dN = 0, 24, 50)."""
+    e = _GOLD["E2"]
+    gi, t = _GOLD[e["input"]], _GOLD["truth"]
+    M = sy.polar_project(np.array(_GOLD[e["M"]]["M"], float))
+    g = _cf.hg2d(gi["orders"], gi["n"], gi["dx"])
+    n2 = gi["n"] + dn
+    pl = opl.plan(M, policy="formI")
+    with nslct.Plan(n2, M, 1, dtype="c128", dx=gi["dx"], dispatch="formI", h_fixed=pl["h"],
+                    n_in=gi["n"]) as p:
+        G = p.exec(torch.from_numpy(g[None].copy()).cuda()).cpu().numpy()[0]
+    ref, _ = op.nsdlct(op.zero_pad(g, n2), M, gi["dx"], pl=pl)
+    assert me.rel_l2(G, ref) <= 1e-10
+    truth = _od.direct(_cf.hg2d(gi["orders"], t["n"], t["dx"]), M, t["dx"], dx_out=gi["dx"], n_out=n2)
+    val = me.nmse_pm(G, truth)
+    bound = {0: 1.7e-3, 24: 2e-6, 50: 5e-8}[dn]
+    assert val <= bound, (dn, val)

@@ -557,3 +557,21 @@ def test_f4_ding_paper_accuracy(ex):
     # and worse than HA on the same example (the paper's conclusion)
     Gh, _ = op.nsdlct(g, paper_matrix(e["M"]), gi["dx"], policy="formI")
     assert me.nmse_pm(Gh, _truth(e["input"], e["M"])) < val or ex == "E2"
+
+
+def test_f3_e3_padding_sweep_g2():
+    """E3 (Figs. 2-3: curves only): zero-padding g2 (N = 165) by dN
+    makes the HA-NsDLCT of A2 converge to the direct-method truth -- NMSE 1.1e-3 at dN = 0
+    (the printed E2 value) falling monotonically by orders of magnitude by dN = 50."""
+    e = GOLD["E2"]
+    gi, t = GOLD[e["input"]], GOLD["truth"]
+    M = paper_matrix(e["M"])
+    g = cf.hg2d(gi["orders"], gi["n"], gi["dx"])
+    gt = cf.hg2d(gi["orders"], t["n"], t["dx"])
+    vals = []
+    for dn in (0, 10, 24, 50):
+        n2 = gi["n"] + dn
+        G, _ = op.nsdlct(op.zero_pad(g, n2), M, gi["dx"], policy="formI")
+        vals.append(me.nmse_pm(G, od.direct(gt, M, t["dx"], dx_out=gi["dx"], n_out=n2)))
+    assert e["HA"] / 1.5 <= vals[0] <= e["HA"] * 1.5, vals
+    assert all(b < a / 5 for a, b in zip(vals, vals[1:])), vals
