@@ -371,3 +371,49 @@ def emulate_slabs(n, M, x_full, nranks, dtype="c64", **kw):
 
 def default_dx(n):
     return math.sqrt(2.0 * math.pi / n)
+
+
+def inverse_matrix(M):
+    """M^-1 = (D^T, -B^T; -C^T, A^T) (Eq. CCCMCCCM20): the inverse transform's matrix."""
+    M = np.asarray(M, dtype=np.float64).reshape(4, 4)
+    A, B, C, D = M[:2, :2], M[:2, 2:], M[2:, :2], M[2:, 2:]
+    return np.block([[D.T, -B.T], [-C.T, A.T]])
+
+
+def nsdlct(x, M, variant="HA", dispatch="reversible", dx=None, n=None, h_fixed=None, stream=None):
+    """One-shot NsDLCT of x ([n_in, n_in] or [batch, n_in, n_in], complex64/complex128) for
+    the 4x4 ABCD matrix M: plan, execute, free.  CUDA tensors run on their device; numpy
+    arrays or CPU tensors go through nslct_exec_host (host in, host out).  n (>= n_in)
+    zero-pads the input to n x n inside the first pass.  Returns the
+    same kind of array, [.., n, n].  For repeated calls build a Plan once instead."""
+    import torch
+    is_np = isinstance(x, np.ndarray)
+    t = torch.from_numpy(np.ascontiguousarray(x)) if is_np else x
+    if t.dtype not in (torch.complex64, torch.complex128):
+        raise ValueError("nsdlct expects complex64 or complex128 input")
+    dtype = "c64" if t.dtype == torch.complex64 else "c128"
+    squeeze = t.dim() == 2
+    if squeeze:
+        t = t.unsqueeze(0)
+    b, n_in = t.shape[0], t.shape[-1]
+    n_out = n_in if n is None else int(n)
+    kw = dict(dtype=dtype, dx=dx, variant=variant, dispatch=dispatch, h_fixed=h_fixed,
+              n_in=(n_in if n_out != n_in else None))
+    if t.is_cuda:
+        with torch.cuda.device(t.device):
+            with Plan(n_out, M, b, device=t.device.index, **kw) as p:
+                out = p.exec(t.contiguous(), stream=stream)
+                (stream or torch.cuda.current_stream(t.device)).synchronize()   # before the plan is freed
+    else:
+        with Plan(n_out, M, b, **kw) as p:
+            out = torch.empty((b, n_out, n_out), dtype=t.dtype)
+            p.exec_host(t.contiguous(), out, stream)
+    if squeeze:
+        out = out[0]
+    return out.numpy() if is_np else out
+
+
+def nsdlct_inverse(G, M, **kw):
+    """The inverse NsDLCT: nsdlct on M^-1 (with the reversible dispatch the pair is exact
+    to rounding)."""
+    return nsdlct(G, inverse_matrix(M), **kw)

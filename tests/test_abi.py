@@ -109,3 +109,15 @@ def test_planner_is_fast():
     for _ in range(5):
         nslct.nslct_plan_describe(4096, M)
     assert (time.time() - t) / 5 < 0.05
+
+
+def test_inverse_matrix_matches_oracle():
+    """nslct.inverse_matrix (the user-facing M^-1 of Eq. CCCMCCCM20) equals the oracle's
+    symplectic inverse and inverts M."""
+    from oracle import symplectic as sy
+    r, _ = synth.config_streams(21)
+    for _ in range(3):
+        M = synth.random_symplectic(r)
+        Mi = nslct.inverse_matrix(M)
+        assert np.allclose(Mi, sy.inverse(M), atol=1e-14)
+        assert np.allclose(Mi @ M, np.eye(4), atol=1e-12)

@@ -821,3 +821,23 @@ def test_paper_additivity_examples_on_gpu(ex, variant):
     Gp, _ = run_gpu(g, M2 @ M1, "c128", **kw)
     val = me.nmse_pm(Gp[0], G[0])
     assert e[variant] / 1.5 <= val <= e[variant] * 1.5, (ex, variant, val)
+
+
+def test_one_shot_api():
+    """nslct.nsdlct / nsdlct_inverse (plan + exec + free): numpy in -> host path, CUDA
+    tensor in -> device path, both equal the oracle; zero-padding through n; the inverse
+    brings the input back."""
+    mr, ir = synth.config_streams(31)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (64, 64)).astype(np.complex128)
+    pl = opl.plan(M)
+    G_host = nslct.nsdlct(x, M, h_fixed=pl["h"])
+    ref, _ = op.nsdlct(x, M, pl=pl)
+    assert isinstance(G_host, np.ndarray) and me.rel_l2(G_host, ref) <= 1e-10
+    G_dev = nslct.nsdlct(torch.from_numpy(x).cuda(), M, h_fixed=pl["h"])
+    assert G_dev.is_cuda and me.rel_l2(G_dev.cpu().numpy(), ref) <= 1e-10
+    back = nslct.nsdlct_inverse(nslct.nsdlct(x, M), M)
+    assert me.rel_l2(back, x) <= 1e-10
+    Gp = nslct.nsdlct(x.astype(np.complex64), M, n=100, h_fixed=pl["h"])
+    refp, _ = op.nsdlct(op.zero_pad(x, 100), M, dx=math.sqrt(2 * math.pi / 100), pl=pl)
+    assert Gp.shape == (100, 100) and me.rel_l2(Gp, refp) <= 1e-4
