@@ -1451,7 +1451,12 @@ line_pass_pair_kernel(PassArgs a) {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c));
   const int tid = threadIdx.x;
   const int j = tid;
-  const long long img_elems = (long long)N * N;
+  // Layout (batched: L = C = N, one block per image; row slabs: L = N/P lines per rank,
+  // chunks of C = L elements, blocks of L x L -- the all-to-all's unit): element i of
+  // local line lam of image img sits at
+  //   img L N + (i / C) L C + (lam / 2) 2C + 2 (i % C) + lam % 2.
+  const int L = a.lines_per_img, C = a.in_chunk;
+  const long long slab_elems = (long long)L * N;
   const long long npairs = a.n_lines / 2;
   const long long ncl = gridDim.x / 2;              // persistent: clusters stride the pairs
   const long long cl = blockIdx.x / 2;
@@ -1465,38 +1470,45 @@ line_pass_pair_kernel(PassArgs a) {
     asm volatile("mapa.u64 %0, %1, %2;" : "=l"(ra[r]) : "l"(reinterpret_cast<uint64_t>(buf)), "r"(r));
   const cpx<T>* b0 = reinterpret_cast<const cpx<T>*>(ra[0]);
   const cpx<T>* b1 = reinterpret_cast<const cpx<T>*>(ra[1]);
-  // this CTA's input bytes of pair p: its own row (first pass) or its half of the
-  // pair's interleaved block -- prefetched into L2 one iteration ahead
+  // this CTA's input bytes of pair p when contiguous (its own row in the first pass, its
+  // half of the pair's interleaved block otherwise) -- prefetched into L2 one iteration
+  // ahead; chunked slab inputs are not prefetched
+  const bool pf = ModeIO<MODE>::kUserIn || C == N;
   auto in_part = [&](long long p) -> const cpx<T>* {
     const long long line = 2 * p + c;
     if constexpr (ModeIO<MODE>::kUserIn) return in + line * N;
     else return in + (2 * p) * N + (long long)c * N;
   };
-  if (tid == 0 && cl < npairs) bulk_prefetch_l2(in_part(cl), (uint32_t)(N * sizeof(cpx<T>)));
+  if (pf && tid == 0 && cl < npairs) bulk_prefetch_l2(in_part(cl), (uint32_t)(N * sizeof(cpx<T>)));
 
   for (long long p = cl; p < npairs; p += ncl) {
-    if (tid == 0 && p + ncl < npairs) bulk_prefetch_l2(in_part(p + ncl), (uint32_t)(N * sizeof(cpx<T>)));
+    if (pf && tid == 0 && p + ncl < npairs) bulk_prefetch_l2(in_part(p + ncl), (uint32_t)(N * sizeof(cpx<T>)));
     const long long line = 2 * p + c;                  // over the batch
-    const long long img = line / N;
-    const int l = (int)(line % N);
+    const long long img = line / L;
+    const int ll = (int)(line % L);                    // local line
+    const int l = a.line_offset + ll;                  // global line (chirps)
     cpx<T> v[16];
     if constexpr (ModeIO<MODE>::kUserIn) {   // the user's row-major line
       const cpx<T>* src = in + line * N + j;
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = src[TL * e];
-    } else {                                  // pair-interleaved intermediate
-      const cpx<T>* src = in + img * img_elems + (long long)(l / 2) * 2 * N + (l % 2) + 2 * j;
+    } else {                                  // pair-interleaved (chunked) intermediate
+      const cpx<T>* src = in + img * slab_elems + (long long)(ll / 2) * 2 * C + (ll % 2);
 #pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = src[2 * TL * e];
+      for (int e = 0; e < 16; ++e) {
+        const int i = j + TL * e;
+        v[e] = src[(long long)(i / C) * L * C + 2 * (i % C)];
+      }
     }
     pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ExPad<T>{buf});
 
-    cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * img_elems;
+    cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * slab_elems;
     if constexpr (ModeIO<MODE>::kStraightOut) {
-      // in place (the last pass writes where it read): rows 2p, 2p+1 ARE the pair's
-      // interleaved input block, so neither CTA may store before both have read it
+      // in place in the batched schedule (the last pass writes where it read): rows 2p,
+      // 2p+1 ARE the pair's interleaved input block, so neither CTA may store before both
+      // have read it
       asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
-      cpx<T>* dst = out + (long long)l * N;
+      cpx<T>* dst = out + (long long)ll * N;
 #pragma unroll
       for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
       __syncthreads();   // the next iteration's exchange reuses buf
@@ -1506,13 +1518,19 @@ line_pass_pair_kernel(PassArgs a) {
       for (int e = 0; e < 16; ++e) buf[pad16(j + TL * e)] = v[e];
       // both CTAs' lines staged (release/acquire across the cluster)
       asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-      const int lp = l & ~1;   // line 0 of the pair
-      // lambda pairs q in this CTA's half: segment at (q) 2N + 2 lp, 4 elements
+      const int lp = ll & ~1;   // local line 0 of the pair
+      // element pairs (e0, e0+1) in this CTA's half of the line: consumer lines
+      // lam = e0 % L, lam + 1 of block s = e0 / L; 32-byte segment [lp: lam, lam+1 |
+      // lp+1: lam, lam+1] at s L^2 + (lam / 2) 2L + 2 lp (in rank s's receive buffer at
+      // block offset peer_rank L^2 when the exchange is fused)
       for (int q = (int)c * (N / 4) + tid; q < ((int)c + 1) * (N / 4); q += THREADS) {
         const int e0 = 2 * q;
         const cpx<T> a0 = b0[pad16(e0)], a1 = b0[pad16(e0 + 1)];
         const cpx<T> c0 = b1[pad16(e0)], c1 = b1[pad16(e0 + 1)];
-        cpx<T>* d = out + (long long)q * 2 * N + 2 * lp;
+        const int sblk = e0 / L, lam = e0 % L;
+        cpx<T>* base = a.peer_on ? reinterpret_cast<cpx<T>*>(a.peer_out[sblk]) + (long long)a.peer_rank * L * L
+                                 : out + (long long)sblk * L * L;
+        cpx<T>* d = base + (long long)(lam / 2) * 2 * L + 2 * lp;
         reinterpret_cast<float4*>(d)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
         reinterpret_cast<float4*>(d)[1] = make_float4(c0.x, c0.y, c1.x, c1.y);
       }

@@ -837,7 +837,7 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
           }
       }
       const char* npair = std::getenv("NSLCT_NO_PAIR");
-      pl->pair = plain && !slab && ti == 0 && (lg == 13 || lg == 14) && !(npair && npair[0] == '1');
+      pl->pair = plain && ti == 0 && (lg == 13 || lg == 14) && (L % 2 == 0) && !(npair && npair[0] == '1');
       for (int k = 0; k < 5 && pl->pair; ++k) pl->args[k].persist_ctas = (pl->num_sms / 2) * 2;
       for (int m = 0; m < kModes && pl->pair; ++m) {
         cudaError_t e = table().atpair[lg][m]();
@@ -1136,7 +1136,10 @@ nslct_status nslct_exec_pass_peer(nslct_plan_t pl, int pass, const void* in, voi
   a.peer_on = 1;
   a.peer_rank = pl->rank;
   for (int r = 0; r < n_peers; ++r) a.peer_out[r] = peer_out[r];
-  CUDA_TRY(table().l[ti][pl->log2n][pl->mode[pass]](a, s));
+  if (pl->pair)
+    CUDA_TRY(table().lpair[pl->log2n][pl->mode[pass]](a, s));
+  else
+    CUDA_TRY(table().l[ti][pl->log2n][pl->mode[pass]](a, s));
   return NSLCT_OK;
 }
 

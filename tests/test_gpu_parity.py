@@ -519,7 +519,8 @@ def test_profile_pass_times():
 
 
 # ------------------------------------------------------------------ row-slab mode (a12)
-@pytest.mark.parametrize("n,nranks,dtype", [(256, 2, "c64"), (256, 4, "c128"), (1024, 8, "c64"), (4096, 4, "c64")])
+@pytest.mark.parametrize("n,nranks,dtype", [(256, 2, "c64"), (256, 4, "c128"), (1024, 8, "c64"), (4096, 4, "c64"),
+                                            (8192, 4, "c64"), (8192, 2, "c128")])
 def test_slab_mode_emulated(n, nranks, dtype):
     """§8(e): one transform as nranks row slabs with the all-to-all between passes
     (emulated on one GPU by block copies; every pass runs the real slab kernels with global
@@ -558,7 +559,7 @@ def test_slab_mode_c5_16384_emulated_8_ranks():
 
 @pytest.mark.parametrize("n,nranks,dtype,variant", [(256, 2, "c64", "HA"), (1024, 8, "c128", "HA"),
                                                      (4096, 4, "c64", "HA"), (1024, 4, "c64", "LC"),
-                                                     (16384, 8, "c64", "HA")])
+                                                     (8192, 4, "c64", "LC"), (16384, 8, "c64", "HA")])
 def test_slab_fused_peer_exchange_emulated(n, nranks, dtype, variant):
     """§8(e) stretch: the all-to-all fused into the transposing pass's store
     (nslct_exec_pass_peer: row-block s written straight into rank s's receive buffer at
