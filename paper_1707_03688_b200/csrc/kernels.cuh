@@ -1438,7 +1438,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
 //     full-sector writes, as the pipe kernels' TMA tensor stores (the G = 1
 //     line_pass_kernel wrote scattered 8-byte elements: 1.4 TB/s at N = 16384).
 // ---------------------------------------------------------------------------------
-template <typename T, int LOG2N, int MODE>
+template <typename T, int LOG2N, int MODE, bool SLAB>
 __global__ void __launch_bounds__(LineCfg<LOG2N>::THREADS)
 line_pass_pair_kernel(PassArgs a) {
   using Cfg = LineCfg<LOG2N>;
@@ -1455,7 +1455,11 @@ line_pass_pair_kernel(PassArgs a) {
   // chunks of C = L elements, blocks of L x L -- the all-to-all's unit): element i of
   // local line lam of image img sits at
   //   img L N + (i / C) L C + (lam / 2) 2C + 2 (i % C) + lam % 2.
-  const int L = a.lines_per_img, C = a.in_chunk;
+  // batched plans: L = C = N at compile time (the 1024-thread kernel has 64 registers);
+  // slab plans: powers of two from the arguments, divisions as shifts
+  const int lgL = SLAB ? __ffs(a.lines_per_img) - 1 : LOG2N;
+  const int lgC = SLAB ? __ffs(a.in_chunk) - 1 : LOG2N;
+  const int L = 1 << lgL, C = 1 << lgC;
   const long long slab_elems = (long long)L * N;
   const long long npairs = a.n_lines / 2;
   const long long ncl = gridDim.x / 2;              // persistent: clusters stride the pairs
@@ -1473,19 +1477,29 @@ line_pass_pair_kernel(PassArgs a) {
   // this CTA's input bytes of pair p when contiguous (its own row in the first pass, its
   // half of the pair's interleaved block otherwise) -- prefetched into L2 one iteration
   // ahead; chunked slab inputs are not prefetched
-  const bool pf = ModeIO<MODE>::kUserIn || C == N;
-  auto in_part = [&](long long p) -> const cpx<T>* {
-    const long long line = 2 * p + c;
-    if constexpr (ModeIO<MODE>::kUserIn) return in + line * N;
-    else return in + (2 * p) * N + (long long)c * N;
+  const bool contiguous = !SLAB || ModeIO<MODE>::kUserIn || C == N;
+  auto prefetch = [&](long long p) {
+    if (!SLAB || contiguous) {
+      const long long line = 2 * p + c;
+      const cpx<T>* src = ModeIO<MODE>::kUserIn ? in + line * N : in + (2 * p) * N + (long long)c * N;
+      bulk_prefetch_l2(src, (uint32_t)(N * sizeof(cpx<T>)));
+    } else if constexpr (SLAB) {   // chunked (slab) input: the pair's 2C-element run in every
+                                   // block, CTA c taking every other block
+      const long long line = 2 * p;
+      const long long img = line / L;
+      const int lp = (int)(line % L);
+      for (int sb = (int)c; sb < N / C; sb += 2)
+        bulk_prefetch_l2(in + img * slab_elems + (long long)sb * L * C + (long long)(lp / 2) * 2 * C,
+                         (uint32_t)(2 * C * sizeof(cpx<T>)));
+    }
   };
-  if (pf && tid == 0 && cl < npairs) bulk_prefetch_l2(in_part(cl), (uint32_t)(N * sizeof(cpx<T>)));
+  if (tid == 0 && cl < npairs) prefetch(cl);
 
   for (long long p = cl; p < npairs; p += ncl) {
-    if (pf && tid == 0 && p + ncl < npairs) bulk_prefetch_l2(in_part(p + ncl), (uint32_t)(N * sizeof(cpx<T>)));
+    if (tid == 0 && p + ncl < npairs) prefetch(p + ncl);
     const long long line = 2 * p + c;                  // over the batch
-    const long long img = line / L;
-    const int ll = (int)(line % L);                    // local line
+    const long long img = line >> lgL;
+    const int ll = (int)(line & (L - 1));              // local line
     const int l = a.line_offset + ll;                  // global line (chirps)
     cpx<T> v[16];
     if constexpr (ModeIO<MODE>::kUserIn) {   // the user's row-major line
@@ -1494,10 +1508,16 @@ line_pass_pair_kernel(PassArgs a) {
       for (int e = 0; e < 16; ++e) v[e] = src[TL * e];
     } else {                                  // pair-interleaved (chunked) intermediate
       const cpx<T>* src = in + img * slab_elems + (long long)(ll / 2) * 2 * C + (ll % 2);
+      if constexpr (SLAB) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int i = j + TL * e;
-        v[e] = src[(long long)(i / C) * L * C + 2 * (i % C)];
+        for (int e = 0; e < 16; ++e) {
+          const int i = j + TL * e;
+          v[e] = src[((long long)(i >> lgC) << (lgL + lgC)) + 2 * (i & (C - 1))];
+        }
+      } else {   // one block per image: constant offsets
+        src += 2 * j;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = src[2 * TL * e];
       }
     }
     pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ExPad<T>{buf});
@@ -1527,10 +1547,15 @@ line_pass_pair_kernel(PassArgs a) {
         const int e0 = 2 * q;
         const cpx<T> a0 = b0[pad16(e0)], a1 = b0[pad16(e0 + 1)];
         const cpx<T> c0 = b1[pad16(e0)], c1 = b1[pad16(e0 + 1)];
-        const int sblk = e0 / L, lam = e0 % L;
-        cpx<T>* base = a.peer_on ? reinterpret_cast<cpx<T>*>(a.peer_out[sblk]) + (long long)a.peer_rank * L * L
-                                 : out + (long long)sblk * L * L;
-        cpx<T>* d = base + (long long)(lam / 2) * 2 * L + 2 * lp;
+        cpx<T>* d;
+        if constexpr (SLAB) {
+          const int sblk = e0 >> lgL, lam = e0 & (L - 1);
+          cpx<T>* base = a.peer_on ? reinterpret_cast<cpx<T>*>(a.peer_out[sblk]) + (long long)a.peer_rank * L * L
+                                   : out + (long long)sblk * L * L;
+          d = base + (long long)(lam / 2) * 2 * L + 2 * lp;
+        } else {
+          d = out + (long long)q * 2 * N + 2 * lp;
+        }
         reinterpret_cast<float4*>(d)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
         reinterpret_cast<float4*>(d)[1] = make_float4(c0.x, c0.y, c1.x, c1.y);
       }

@@ -58,7 +58,7 @@ cudaError_t set_attr() {
 }
 
 // large-N pair kernels (N = 8192, 16384, complex64): a 2-CTA cluster per line pair
-template <int LOG2N, int MODE>
+template <int LOG2N, int MODE, bool SLAB>
 cudaError_t launch_pair(const PassArgs& a, cudaStream_t s) {
   using Cfg = nslct::LineCfg<LOG2N>;
   cudaLaunchConfig_t cfg = {};
@@ -75,21 +75,22 @@ cudaError_t launch_pair(const PassArgs& a, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair_kernel<float, LOG2N, MODE>, a);
+  return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair_kernel<float, LOG2N, MODE, SLAB>, a);
 }
-template <int LOG2N, int MODE>
+template <int LOG2N, int MODE, bool SLAB>
 cudaError_t set_attr_pair() {
   using Cfg = nslct::LineCfg<LOG2N>;
-  return cudaFuncSetAttribute(nslct::line_pass_pair_kernel<float, LOG2N, MODE>,
+  return cudaFuncSetAttribute(nslct::line_pass_pair_kernel<float, LOG2N, MODE, SLAB>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Cfg::LS * sizeof(nslct::cpx<float>)));
 }
-template <int LOG2N>
+template <int LOG2N, bool SLAB>
 struct PairRow {
   static void fill(launch_fn* l, attr_fn* at) {
-    l[0] = launch_pair<LOG2N, 0>; l[1] = launch_pair<LOG2N, 1>; l[2] = launch_pair<LOG2N, 2>;
-    l[3] = launch_pair<LOG2N, 3>; l[4] = launch_pair<LOG2N, 4>; l[5] = launch_pair<LOG2N, 5>;
-    at[0] = set_attr_pair<LOG2N, 0>; at[1] = set_attr_pair<LOG2N, 1>; at[2] = set_attr_pair<LOG2N, 2>;
-    at[3] = set_attr_pair<LOG2N, 3>; at[4] = set_attr_pair<LOG2N, 4>; at[5] = set_attr_pair<LOG2N, 5>;
+    l[0] = launch_pair<LOG2N, 0, SLAB>; l[1] = launch_pair<LOG2N, 1, SLAB>; l[2] = launch_pair<LOG2N, 2, SLAB>;
+    l[3] = launch_pair<LOG2N, 3, SLAB>; l[4] = launch_pair<LOG2N, 4, SLAB>; l[5] = launch_pair<LOG2N, 5, SLAB>;
+    at[0] = set_attr_pair<LOG2N, 0, SLAB>; at[1] = set_attr_pair<LOG2N, 1, SLAB>;
+    at[2] = set_attr_pair<LOG2N, 2, SLAB>; at[3] = set_attr_pair<LOG2N, 3, SLAB>;
+    at[4] = set_attr_pair<LOG2N, 4, SLAB>; at[5] = set_attr_pair<LOG2N, 5, SLAB>;
   }
 };
 
@@ -222,8 +223,8 @@ struct Table {
   attr_fn ati[2][kMaxLog + 1] = {};
   launch_fn l[2][kMaxLog + 1][kModes] = {};
   attr_fn at[2][kMaxLog + 1][kModes] = {};
-  launch_fn lpair[kMaxLog + 1][kModes] = {};   // c64 N = 8192, 16384 (cluster pairs)
-  attr_fn atpair[kMaxLog + 1][kModes] = {};
+  launch_fn lpair[2][kMaxLog + 1][kModes] = {};   // c64 N = 8192, 16384 (cluster pairs): [slab]
+  attr_fn atpair[2][kMaxLog + 1][kModes] = {};
   pipe_fn lp[kMaxLog + 1][kModes] = {};   // c64 only
   attr_fn atp[kMaxLog + 1][kModes] = {};
   pipe_fn lp64[kModes] = {launch_pipe<float, 12, 0, true>, launch_pipe<float, 12, 1, true>,
@@ -240,8 +241,10 @@ struct Table {
     li[1][5] = launch_img<double, 5, 1>, ati[1][5] = set_attr_img<double, 5, 1>;
     li[1][6] = launch_img<double, 6, 1>, ati[1][6] = set_attr_img<double, 6, 1>;
     li[1][7] = launch_img<double, 7, 4>, ati[1][7] = set_attr_img<double, 7, 4>;
-    PairRow<13>::fill(lpair[13], atpair[13]);
-    PairRow<14>::fill(lpair[14], atpair[14]);
+    PairRow<13, false>::fill(lpair[0][13], atpair[0][13]);
+    PairRow<14, false>::fill(lpair[0][14], atpair[0][14]);
+    PairRow<13, true>::fill(lpair[1][13], atpair[1][13]);
+    PairRow<14, true>::fill(lpair[1][14], atpair[1][14]);
     PipeRow<float, 10>::fill(lp[10], atp[10]);
     PipeRow<float, 11>::fill(lp[11], atp[11]);
     PipeRow<float, 12>::fill(lp[12], atp[12]);
@@ -840,7 +843,7 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       pl->pair = plain && ti == 0 && (lg == 13 || lg == 14) && (L % 2 == 0) && !(npair && npair[0] == '1');
       for (int k = 0; k < 5 && pl->pair; ++k) pl->args[k].persist_ctas = (pl->num_sms / 2) * 2;
       for (int m = 0; m < kModes && pl->pair; ++m) {
-        cudaError_t e = table().atpair[lg][m]();
+        cudaError_t e = table().atpair[slab ? 1 : 0][lg][m]();
         if (e != cudaSuccess) {
           result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(pair): ") + cudaGetErrorString(e));
           break;
@@ -1045,7 +1048,7 @@ static nslct_status run_images(nslct_plan_t pl, const void* in, void* out, int64
       nslct_status st = launch_pipe_pass(pl, k, a, s);
       if (st != NSLCT_OK) return st;
     } else if (pl->pair) {
-      CUDA_TRY(table().lpair[pl->log2n][pl->mode[k]](a, s));
+      CUDA_TRY(table().lpair[pl->slab ? 1 : 0][pl->log2n][pl->mode[k]](a, s));
     } else {
       CUDA_TRY(table().l[ti][pl->log2n][pl->mode[k]](a, s));
     }
@@ -1093,7 +1096,7 @@ nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* ou
     nslct_status st = launch_pipe_pass(pl, pass, a, s);
     if (st != NSLCT_OK) return st;
   } else if (pl->pair) {
-    CUDA_TRY(table().lpair[pl->log2n][pl->mode[pass]](a, s));
+    CUDA_TRY(table().lpair[pl->slab ? 1 : 0][pl->log2n][pl->mode[pass]](a, s));
   } else {
     CUDA_TRY(table().l[ti][pl->log2n][pl->mode[pass]](a, s));
   }
@@ -1137,7 +1140,7 @@ nslct_status nslct_exec_pass_peer(nslct_plan_t pl, int pass, const void* in, voi
   a.peer_rank = pl->rank;
   for (int r = 0; r < n_peers; ++r) a.peer_out[r] = peer_out[r];
   if (pl->pair)
-    CUDA_TRY(table().lpair[pl->log2n][pl->mode[pass]](a, s));
+    CUDA_TRY(table().lpair[pl->slab ? 1 : 0][pl->log2n][pl->mode[pass]](a, s));
   else
     CUDA_TRY(table().l[ti][pl->log2n][pl->mode[pass]](a, s));
   return NSLCT_OK;
