@@ -149,7 +149,9 @@ nslct_status nslct_exec_host(nslct_plan_t plan, const void* host_in, void* host_
  * all_to_all_single): the send buffer is the previous pass's `out`, laid out [n][L] =
  * nranks row-blocks of [L][L] (block s goes to rank s), and the receive buffer (block
  * from rank s at element offset s*L*L) is the next pass's `in`.  This exchange is the
- * distributed form of the transposes the single-GPU passes fold into their stores.
+ * distributed form of the transposes the single-GPU passes fold into their stores.  The
+ * element order INSIDE a block is the library's (plain transposed, or pair-interleaved
+ * for complex64 n >= 8192: DESIGN.md §7); the exchange must move whole blocks unchanged.
  * Requires B != 0 (the B = 0 gather has no slab form), nranks | n, and L a multiple of
  * the kernel's lines per CTA (L >= 16 suffices for n >= 4096).  The plan allocates no
  * scratch: the caller owns all buffers (each n*L complex elements).  Errors: as
@@ -183,7 +185,8 @@ typedef struct {
   int variant;                 /* variant actually used (LC falls back to HA: PAPER.md:840)  */
   int lc_axis;                 /* 0 none, 1 = H=(h,0;0,0) (x), 2 = H=(0,0;0,h) (y)            */
   int n_passes;                /* device passes per transform: 5 (HA, LC with x-axis H),      */
-                               /* 3 (LC with y-axis H), 1 (B=0)               */
+                               /* 3 (LC with y-axis H; Ding: two line passes
+                                  of length 2N + the affine gather), 1 (B=0)                  */
   double H[3], Bp[3], P2[3], P4[3];  /* form-I plan of M (form I) or of M^-1 (form II):
                                         (q11, q22, q12) of H, B', P2=B'^-1(A-I), P4=(D'-I)B'^-1 */
   double Q[5][3];              /* the executed chirps, application order:
