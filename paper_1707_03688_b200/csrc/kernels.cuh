@@ -1,4 +1,4 @@
-// Device kernels of the B200 NsDLCT (sm_100a).  Included by nslct.cu only.
+// Device kernels of the B200 NsDLCT (sm_100a).  Included by nslct.cu and bluestein.cu.
 //
 // The HA chain (Eq. HA28; form II Eq. CCCMCCCM40) is executed as
 //     G = CM_r(Q4) S W^-1 CM_w(Q3) W CM_r(Q2) W^-1 CM_w(Q1) W S CM_r(Q0) g
