@@ -1423,6 +1423,202 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
 }
 
 // ---------------------------------------------------------------------------------
+// Warp-specialised variant of the persistent pipe kernel (passes 2-5 at N = 4096): 16 compute
+// warps run pass_body exactly as line_pass_pipe_kernel does, and a 17th PRODUCER warp
+// issues every TMA operation -- the output stores of a group, the claim of the group
+// after next and its load.  In the 512-thread kernel thread 0 does that work between
+// the output barrier and the next group's first exchange, and every other warp then waits
+// for warp 0 at that barrier (the largest single stall in the ncu source view).  Compute
+// warps synchronise among themselves with named barrier 1 (512 threads) and hand each
+// staged output to the producer with a non-blocking arrive on named barrier 2.
+// ---------------------------------------------------------------------------------
+template <typename T>
+struct ExPadWS {   // as ExPad2, but the 16 compute warps only (named barrier 1), no hook
+  static constexpr bool kDouble = true;
+  static constexpr bool kPadded = true;
+  static constexpr int kPadW = 1;
+  cpx<T>* buf0;
+  cpx<T>* buf1;
+  template <int X>
+  __device__ __forceinline__ void sync() const { asm volatile("bar.sync 1, 512;" ::: "memory"); }
+  template <int X>
+  __device__ __forceinline__ cpx<T>* b() const { return (X & 1) ? buf1 : buf0; }
+  __device__ __forceinline__ int idx(int i) const { return padw<1>(i); }
+  template <int X>
+  __device__ __forceinline__ void after_barrier() const {}
+};
+
+constexpr size_t kWsExtra = 128;
+template <int LOG2N, int MODE>
+__global__ void __launch_bounds__(544, 1)
+line_pass_ws_kernel(PassArgs a, long long n_groups, unsigned long long* counter,
+                    const __grid_constant__ CUtensorMap omap) {
+  using T = float;
+  using Cfg = PipeCfg<LOG2N>;
+  constexpr int N = Cfg::N, TL = Cfg::TL, G = Cfg::G, IL = Cfg::IL;
+  constexpr int GE = Cfg::GROUP_ELEMS;
+  constexpr int BE = Cfg::BUF_ELEMS, LS = Cfg::LS;
+  constexpr int NXP = FftNX<LOG2N, TwTmem<LOG2N>>::value * PassInfo<LOG2N, MODE>::NFFT;
+  static_assert((NXP & 1) == 0, "even exchange count: the output is staged in the spare buffer");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cpx<T>* bufs = reinterpret_cast<cpx<T>*>(smem_raw);
+  // shared tail (kWsExtra bytes): 3 "loaded" mbarriers (TMA completion), 3 "staged"
+  // mbarriers (512 compute-thread arrivals: output of the group in that buffer is staged),
+  // 3 group slots, the TMEM base
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 3 * BE * sizeof(cpx<T>));
+  uint64_t* staged = bar + 3;
+  long long* s_next = reinterpret_cast<long long*>(staged + 3);
+  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(s_next + 3);
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const bool producer = warp == 16;
+  const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in);
+  cpx<T>* __restrict__ out = reinterpret_cast<cpx<T>*>(a.out);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_taddr)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&bar[i], 1);
+      mbar_init(&staged[i], 512);
+    }
+    fence_mbar_init();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  if (producer) {
+    // lane 0 issues the TMA traffic; the warp keeps uniform control flow (claimed group
+    // indices are broadcast)
+    const bool lead = (tid & 31) == 0;
+    uint32_t sphase = 0;   // parity of the next completion of staged[0..2]
+    auto claim_load = [&](int b) -> long long {
+      long long gn = 0;
+      if (lead) {
+        gn = (long long)atomicAdd(counter, 1ull);
+        s_next[b] = gn;
+        if (gn < n_groups) {
+          if (a.l2_ahead && gn + a.l2_ahead < n_groups)
+            bulk_prefetch_l2(in + (gn + a.l2_ahead) * GE, (uint32_t)(GE * sizeof(cpx<T>)));
+          load_group<T, LOG2N, MODE>(bufs + b * BE, in + gn * GE, &bar[b]);
+        } else {
+          mbar_arrive(&bar[b]);   // end marker for the compute warps
+        }
+      }
+      return __shfl_sync(0xffffffffu, gn, 0);
+    };
+    long long gq[3];
+    gq[0] = claim_load(0);
+    gq[1] = (gq[0] < n_groups) ? claim_load(1) : n_groups;   // buffer 1 is free at the start
+    gq[2] = n_groups;
+    int bs = 0, bx = 2, bn = 1;
+    for (;;) {
+      const long long g = gq[bs];
+      if (g >= n_groups) break;           // the compute warps stopped at this buffer
+      // wait until the 16 compute warps have staged group g's output in the spare buffer
+      mbar_wait(&staged[bx], (sphase >> bx) & 1u);
+      sphase ^= 1u << bx;
+      cpx<T>* ob = bufs + bx * BE;
+      if (lead) {
+        if constexpr (ModeIO<MODE>::kStraightOut) {
+          bulk_s2g(out + g * G * N, ob, (uint32_t)(GE * sizeof(cpx<T>)));
+        } else {
+          const int gi = (int)(g % (N / G)), img = (int)(g / (N / G));
+#pragma unroll 1
+          for (int r = 0; r < Cfg::ROWS; r += Cfg::BOX_ROWS) tensor_s2g_4d(&omap, ob + r * (G * IL), 0, r, gi, img);
+        }
+        bulk_commit();
+      }
+      // the spare becomes the buffer of the group after next once its store has been read
+      const int ob_i = bx, free_i = bs;
+      if (gq[bn] < n_groups) {
+        if (lead) {
+          bulk_wait_read0();
+          fence_proxy_async_smem();
+        }
+        gq[ob_i] = claim_load(ob_i);
+      } else {
+        gq[ob_i] = n_groups;
+      }
+      bs = bn;
+      bn = ob_i;
+      bx = free_i;
+    }
+    if (lead) bulk_wait0();
+    return;
+  }
+
+  // ---- the 16 compute warps
+  const int gl = tid % G;
+  const int j = tid / G;
+  const uint32_t tmem_base = *s_taddr;
+  using Maker = TwMaker<LOG2N, false>;
+  const typename Maker::type tws = Maker::make(tmem_base + ((uint32_t)(32 * (warp & 3)) << 16), warp, j,
+                                               reinterpret_cast<const cpx<T>*>(a.tw));
+  int bs = 0, bx = 2, bn = 1;
+  uint32_t phases = 0;
+  for (;;) {
+    cpx<T>* sb = bufs + bs * BE;
+    cpx<T>* xb = bufs + bx * BE;
+    mbar_wait(&bar[bs], (phases >> bs) & 1u);
+    phases ^= 1u << bs;
+    const long long g = s_next[bs];
+    if (g >= n_groups) break;
+    const long long line0 = g * G;
+    const int l = (int)((line0 + gl) % N);
+    cpx<T> v[16];
+    if constexpr (ModeIO<MODE>::kUserIn) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int e = (q & 3) * 4 + (q >> 2);
+        v[e] = sb[gl * LS + j + TL * e];
+      }
+    } else {
+      const cpx<T>* src = sb + (gl / IL) * (IL * N) + (gl % IL);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int e = (q & 3) * 4 + (q >> 2);
+        v[e] = src[(j + TL * e) * IL];
+      }
+    }
+    const ExPadWS<T> ex{xb + gl * LS, sb + gl * LS};
+    pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ex);
+    cpx<T>* ob = xb;   // even exchange count: the spare buffer is free
+    if constexpr (ModeIO<MODE>::kStraightOut) {
+      cpx<T>* o = ob + gl * N;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int e = (q & 3) * 4 + (q >> 2);
+        o[j + TL * e] = v[e];
+      }
+    } else {
+      cpx<T>* o = ob + (j / IL) * (G * IL) + gl * IL + (j % IL);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int e = (q & 3) * 4 + (q >> 2);
+        o[e * (TL / IL) * (G * IL)] = v[e];
+      }
+    }
+    fence_proxy_async_smem();
+    // every compute warp is past this group's last exchange reads (the next group's first
+    // exchange writes into this group's staging buffer) ...
+    asm volatile("bar.sync 1, 512;" ::: "memory");
+    // ... and the staged output goes to the producer
+    mbar_arrive(&staged[bx]);
+    const int ob_i = bx, free_i = bs;
+    bs = bn;
+    bn = ob_i;
+    bx = free_i;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  asm volatile("bar.sync 1, 512;" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+}
+
+// ---------------------------------------------------------------------------------
 // Large-N line pass (N = 8192, 16384; complex64, batched plans): a line is 64-128 KB, so
 // one CTA holds ONE line (G = 1) and the persistent pipe kernels' group of two lines per
 // CTA does not fit.  A CLUSTER of two CTAs takes the two lines of a pair-interleaved

@@ -116,6 +116,25 @@ cudaError_t set_attr_pipe() {
 }
 typedef cudaError_t (*pipe_fn)(const PassArgs&, cudaStream_t, int, unsigned long long*, const CUtensorMap&);
 
+// warp-specialised variant (kernels.cuh line_pass_ws_kernel, opt-in NSLCT_WS=1)
+template <int LOG2N, int MODE>
+cudaError_t launch_ws(const PassArgs& a, cudaStream_t s, int grid, unsigned long long* counter,
+                      const CUtensorMap& omap) {
+  using Cfg = nslct::PipeCfg<LOG2N>;
+  const size_t smem = (size_t)Cfg::NBUF * Cfg::BUF_ELEMS * sizeof(nslct::cpx<float>) + nslct::kWsExtra;
+  const long long n_groups = a.n_lines / Cfg::G;
+  const long long g = n_groups < grid ? n_groups : grid;
+  nslct::line_pass_ws_kernel<LOG2N, MODE><<<(unsigned)g, 544, smem, s>>>(a, n_groups, counter, omap);
+  return cudaGetLastError();
+}
+template <int LOG2N, int MODE>
+cudaError_t set_attr_ws() {
+  using Cfg = nslct::PipeCfg<LOG2N>;
+  const size_t smem = (size_t)Cfg::NBUF * Cfg::BUF_ELEMS * sizeof(nslct::cpx<float>) + nslct::kWsExtra;
+  return cudaFuncSetAttribute(nslct::line_pass_ws_kernel<LOG2N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem);
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (resolved once)
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
@@ -363,6 +382,7 @@ struct nslct_plan_s {
   bool pipe = false;   // persistent TMA-pipelined kernels
   bool image = false;  // fully on-chip kernel (one launch per exec)
   bool fft64 = false;  // pipe kernels with the 64x64 TMEM-exchange FFT (N = 4096, opt-in)
+  bool ws = false;     // warp-specialised pipe kernels for modes 1-3 (N = 4096; NSLCT_WS=0 disables)
   bool pair = false;   // large-N cluster-pair line passes (N = 8192, 16384, complex64)
   unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
   int num_sms = 148;
@@ -852,6 +872,20 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       if (result != NSLCT_OK) break;
       const char* f64 = std::getenv("NSLCT_FFT64");
       pl->fft64 = pl->pipe && lg == 12 && f64 && f64[0] == '1';
+      // warp-specialised kernels for the passes after the first (measured K2-K5 -0.6..-1.6%,
+      // K1 +2.4% -- so not for mode 0)
+      const char* wse = std::getenv("NSLCT_WS");
+      pl->ws = pl->pipe && !pl->fft64 && lg == 12 && !(wse && wse[0] == '0');
+      if (pl->ws) {
+        cudaError_t e = set_attr_ws<12, 0>();
+        if (e == cudaSuccess) e = set_attr_ws<12, 1>();
+        if (e == cudaSuccess) e = set_attr_ws<12, 2>();
+        if (e == cudaSuccess) e = set_attr_ws<12, 3>();
+        if (e != cudaSuccess) {
+          result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(ws): ") + cudaGetErrorString(e));
+          break;
+        }
+      }
       const bool have = plain && !slab && table().li[ti][lg] != nullptr;
       if (o.schedule == NSLCT_SCHEDULE_ON_CHIP && !have && pl->p.kind != 0) {
         result = fail(NSLCT_E_UNSUPPORTED_N, "no on-chip kernel for this N / dtype (c64 N <= 256, c128 N <= 128)");
@@ -915,7 +949,10 @@ static nslct_status launch_pipe_pass(nslct_plan_t pl, int k, const PassArgs& a, 
     nslct_status st = make_store_map(&map, a.out, pl->log2n, a.n_lines >> pl->log2n);
     if (st != NSLCT_OK) return st;
   }
-  if (pl->fft64)
+  if (pl->ws && m >= 1 && m <= 3) {
+    static const pipe_fn wsl[4] = {launch_ws<12, 0>, launch_ws<12, 1>, launch_ws<12, 2>, launch_ws<12, 3>};
+    CUDA_TRY(wsl[m](a, s, pl->num_sms, pl->counters + k, map));
+  } else if (pl->fft64)
     CUDA_TRY(table().lp64[m](a, s, pl->num_sms, pl->counters + k, map));
   else
     CUDA_TRY(table().lp[pl->log2n][m](a, s, pl->num_sms, pl->counters + k, map));
