@@ -121,3 +121,25 @@ def test_inverse_matrix_matches_oracle():
         Mi = nslct.inverse_matrix(M)
         assert np.allclose(Mi, sy.inverse(M), atol=1e-14)
         assert np.allclose(Mi @ M, np.eye(4), atol=1e-12)
+
+
+def test_ding_plan_describe():
+    """Ding plans on the host (no GPU): kind DING, 3 passes, Q0 = B^-1 A and Q4 = D B^-1
+    of Eq. Ding12; B = 0 takes the Eq. Intro20 path; a singular B != 0
+    has no Ding decomposition."""
+    r, _ = synth.config_streams(23)
+    M = synth.random_symplectic(r)
+    d = nslct.nslct_plan_describe(64, M, variant="DING")
+    assert d["kind"] == "DING" and d["n_passes"] == 3 and d["variant"] == "DING"
+    A, B, C, D = M[:2, :2], M[:2, 2:], M[2:, :2], M[2:, 2:]
+    Bi = np.linalg.inv(B)
+    assert np.allclose(d["Q"][0], 0.5 * (Bi @ A + (Bi @ A).T), atol=1e-12)
+    assert np.allclose(d["Q"][4], 0.5 * (D @ Bi + (D @ Bi).T), atol=1e-12)
+    assert d["recomposition_residual"] < 1e-9
+    assert nslct.nslct_plan_describe(64, np.eye(4), variant="DING")["kind"] == "B0"
+    # B = [[1, 0], [0, 0]] (rank 1): a valid matrix (free space along x, identity in y)
+    Ms = np.eye(4)
+    Ms[0, 2] = 1.0
+    with pytest.raises(nslct.NslctError) as e:
+        nslct.nslct_plan_describe(64, Ms, variant="DING")
+    assert e.value.name == "E_NO_DECOMP"
