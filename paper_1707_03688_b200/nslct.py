@@ -307,8 +307,6 @@ def symm_mem_exchange(L, n, dtype="c64", group=None):
     import torch.distributed._symmetric_memory as symm
     want = torch.complex64 if dtype == "c64" else torch.complex128
     grp = group if group is not None else dist.group.WORLD
-    if hasattr(symm, "enable_symm_mem_for_group"):   # required by older torch releases
-        symm.enable_symm_mem_for_group(grp.group_name)
     recv, handles = [], []
     for _ in range(2):
         b = symm.empty(L, n, dtype=want, device=torch.device("cuda", torch.cuda.current_device()))

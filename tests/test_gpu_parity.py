@@ -842,3 +842,36 @@ def test_one_shot_api():
     Gp = nslct.nsdlct(x.astype(np.complex64), M, n=100, h_fixed=pl["h"])
     refp, _ = op.nsdlct(op.zero_pad(x, 100), M, dx=math.sqrt(2 * math.pi / 100), pl=pl)
     assert Gp.shape == (100, 100) and me.rel_l2(Gp, refp) <= 1e-4
+
+
+@pytest.mark.parametrize("n", [1024, 8192])
+def test_symm_mem_peer_exchange_single_rank(n):
+    """The multi-GPU fused-exchange plumbing (torch symmetric memory receive buffers, their
+    peer pointers and stream-ordered barrier -- nslct.symm_mem_exchange -- driving
+    SlabPlan.run_peer) on a one-rank NCCL process group: the transform equals the
+    single-plan result.  (Real peers need more than one GPU.)"""
+    import tempfile
+
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    mr, ir = synth.config_streams(950 + n)
+    M = synth.random_symplectic(mr)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n)
+    x = torch.randn((n, n), dtype=torch.complex64, device="cuda", generator=g)
+    with tempfile.NamedTemporaryFile() as f:
+        dist.init_process_group("nccl", init_method="file://" + f.name, rank=0, world_size=1,
+                                device_id=torch.device("cuda", torch.cuda.current_device()))
+        try:
+            recv, ptrs, barrier = nslct.symm_mem_exchange(n, n)
+            with nslct.SlabPlan(n, M, 1, 0) as sp:
+                G = sp.run_peer(x, recv, ptrs, barrier)
+            torch.cuda.synchronize()
+        finally:
+            dist.destroy_process_group()
+    with nslct.Plan(n, M, 1) as p:
+        G1 = p.exec(x.view(1, n, n))[0]
+    rel = float(torch.linalg.vector_norm((G - G1).to(torch.complex128)) /
+                torch.linalg.vector_norm(G1.to(torch.complex128)))
+    assert rel <= 1e-6, rel
