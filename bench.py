@@ -170,6 +170,29 @@ def cpu_fft_sample(x_img, M):
     return time.perf_counter() - t0, cores
 
 
+def cpu_direct_sample(x_img, M, k=128):
+    """Time the direct method (Eq. Intro32, oracle/direct.py, O(N^2) per output pixel) on k
+    sampled output pixels of one image; returns the extrapolated seconds per transform
+    (x N^2 / k) and the BLAS thread count."""
+    import numpy as np
+    from oracle import direct
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    g = np.asarray(x_img, np.complex128)
+    n = g.shape[-1]
+    dx = math.sqrt(2.0 * math.pi / n)
+    rs = np.random.default_rng(0)
+    idx = rs.integers(0, n, (k, 2))
+    pts = (idx - n // 2) * dx
+    t0 = time.perf_counter()
+    direct.direct(g, M, dx, out_points=pts)
+    dt = time.perf_counter() - t0
+    return dt * n * n / k, cores
+
+
 def run_reference(args):
     """Reference arm: the fp64 oracle, as it stands, on the host cores (rank 0 only).
 
@@ -370,6 +393,7 @@ def run_ours(args):
 
     cpu = None
     cpu_fft_line = None
+    cpu_direct_line = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         img0 = x[0].cpu().numpy()
         dt, cores = cpu_oracle_sample(img0, M)
@@ -378,6 +402,9 @@ def run_ours(args):
         dtf, coresf = cpu_fft_sample(img0, M)
         cpu_fft_line = {"value": 1.0 / dtf, "unit": UNIT, "cores": coresf, "kind": "cpu_fft_decomposition",
                         "sample": "image 0 of the step, fp64, scipy.fft (workers=%d): baselines/cpu_fft.py" % coresf}
+        dtd, coresd = cpu_direct_sample(img0, M)
+        cpu_direct_line = {"value": 1.0 / dtd, "unit": UNIT, "cores": coresd, "kind": "oracle_direct_eq_intro32",
+                           "sample": "128 sampled output pixels of image 0 (O(N^2) each), extrapolated x N^2/128"}
 
     plan.close()
     if rank == 0:
@@ -400,6 +427,7 @@ def run_ours(args):
                          "pass_ms": pass_ms},
             "cpu_baseline": cpu,
             "cpu_fft_baseline": cpu_fft_line,
+            "cpu_direct_baseline": cpu_direct_line,
             "e2e": e2e,
             "gpu_launches": info["n_launches"] * args.steps,
             "clocks": clk,
