@@ -416,7 +416,8 @@ def run_ours(args):
                        "variant": info["variant"], "per_gpu_batch": batch, "global_batch": int(total_units),
                        "plan_kind": info["kind"], "parallelism": "dp%d (independent images, no collective)" % world,
                        "l2": ("L2 flushed before every step (512 MiB memset outside the step events)" if flush is not None
-                              else "inputs %.2f GiB/GPU >> 126 MB L2; no flush" % (batch * n * n * S / 2 ** 30)),
+                              else "each pass reads and writes %.2f GiB/GPU (>= 2x the 126 MB L2); no flush"
+                              % (2 * batch * n * n * S / 2 ** 30)),
                        "schedule": "on-chip (1 launch)" if info["on_chip"] else "%d line passes" % info["n_passes"], "hbm_alg_bytes_per_step": step_alg_bytes},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": names[ki],

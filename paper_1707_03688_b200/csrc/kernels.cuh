@@ -1423,7 +1423,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
 }
 
 // ---------------------------------------------------------------------------------
-// Warp-specialised variant of the persistent pipe kernel (passes 2-5 at N = 4096): 16 compute
+// Warp-specialised variant of the persistent pipe kernel (passes 2-5, N = 1024 ... 4096): 16 compute
 // warps run pass_body exactly as line_pass_pipe_kernel does, and a 17th PRODUCER warp
 // issues every TMA operation -- the output stores of a group, the claim of the group
 // after next and its load.  In the 512-thread kernel thread 0 does that work between

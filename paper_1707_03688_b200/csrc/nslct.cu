@@ -134,6 +134,20 @@ cudaError_t set_attr_ws() {
   return cudaFuncSetAttribute(nslct::line_pass_ws_kernel<LOG2N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem);
 }
+// the warp-specialised kernels for N = 2^lg (1024 ... 4096), pass modes 1 ... 3
+struct WsRow {
+  pipe_fn launch[3];
+  attr_fn attr[3];
+};
+template <int L>
+constexpr WsRow ws_row() {
+  return WsRow{{launch_ws<L, 1>, launch_ws<L, 2>, launch_ws<L, 3>},
+               {set_attr_ws<L, 1>, set_attr_ws<L, 2>, set_attr_ws<L, 3>}};
+}
+const WsRow* ws_row_of(int lg) {
+  static const WsRow rows[3] = {ws_row<10>(), ws_row<11>(), ws_row<12>()};
+  return (lg >= 10 && lg <= 12) ? &rows[lg - 10] : nullptr;
+}
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (resolved once)
 PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
@@ -382,7 +396,7 @@ struct nslct_plan_s {
   bool pipe = false;   // persistent TMA-pipelined kernels
   bool image = false;  // fully on-chip kernel (one launch per exec)
   bool fft64 = false;  // pipe kernels with the 64x64 TMEM-exchange FFT (N = 4096, opt-in)
-  bool ws = false;     // warp-specialised pipe kernels for modes 1-3 (N = 4096; NSLCT_WS=0 disables)
+  bool ws = false;     // warp-specialised pipe kernels for modes 1-3 (NSLCT_WS=0 disables)
   bool pair = false;   // large-N cluster-pair line passes (N = 8192, 16384, complex64)
   unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
   int num_sms = 148;
@@ -875,12 +889,11 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       // warp-specialised kernels for the passes after the first (measured K2-K5 -0.6..-1.6%,
       // K1 +2.4% -- so not for mode 0)
       const char* wse = std::getenv("NSLCT_WS");
-      pl->ws = pl->pipe && !pl->fft64 && lg == 12 && !(wse && wse[0] == '0');
+      pl->ws = pl->pipe && !pl->fft64 && !(wse && wse[0] == '0');
       if (pl->ws) {
-        cudaError_t e = set_attr_ws<12, 0>();
-        if (e == cudaSuccess) e = set_attr_ws<12, 1>();
-        if (e == cudaSuccess) e = set_attr_ws<12, 2>();
-        if (e == cudaSuccess) e = set_attr_ws<12, 3>();
+        const WsRow* row = ws_row_of(lg);
+        cudaError_t e = row ? cudaSuccess : cudaErrorInvalidValue;
+        for (int m = 1; m <= 3 && e == cudaSuccess; ++m) e = row->attr[m - 1]();
         if (e != cudaSuccess) {
           result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(ws): ") + cudaGetErrorString(e));
           break;
@@ -950,8 +963,7 @@ static nslct_status launch_pipe_pass(nslct_plan_t pl, int k, const PassArgs& a, 
     if (st != NSLCT_OK) return st;
   }
   if (pl->ws && m >= 1 && m <= 3) {
-    static const pipe_fn wsl[4] = {launch_ws<12, 0>, launch_ws<12, 1>, launch_ws<12, 2>, launch_ws<12, 3>};
-    CUDA_TRY(wsl[m](a, s, pl->num_sms, pl->counters + k, map));
+    CUDA_TRY(ws_row_of(pl->log2n)->launch[m - 1](a, s, pl->num_sms, pl->counters + k, map));
   } else if (pl->fft64)
     CUDA_TRY(table().lp64[m](a, s, pl->num_sms, pl->counters + k, map));
   else
