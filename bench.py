@@ -259,6 +259,9 @@ def run_ours(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     n, batch, dtype, desc = CONFIGS[args.config]
+    if args.batch:   # exploration only: the config's workload at another per-GPU batch
+        desc = desc.replace("batch %d/GPU" % batch, "batch %d/GPU" % args.batch)
+        batch = args.batch
     mr, _ = synth.config_streams(args.config)
     M = synth.random_symplectic(mr)                 # same matrix on every rank
     if args.variant == "LC":   # the first G(rng) draw whose LC plan has a y-axis H (3 passes)
@@ -522,6 +525,8 @@ def main(argv=None):
     ap.add_argument("--schedule", default="auto", choices=["auto", "line_passes", "on_chip"],
                     help="on-chip kernel where available (auto) or one launch per pass")
     ap.add_argument("--variant", default="HA", choices=["HA", "LC"], help="planner variant")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="override the config's per-GPU batch (exploration; the default run uses the config's)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
