@@ -32,6 +32,7 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # id: (n, per-GPU batch, dtype, description)
+    1: (32, 1, "c128", "C1: 32x32 complex128, 1 transform/GPU, random symplectic ABCD, iid CN(0,1)"),
     2: (256, 64, "c64", "C2: 256x256 complex64, batch 64/GPU, random symplectic ABCD, iid CN(0,1)"),
     3: (1024, 16, "c64", "C3: 1024x1024 complex64, batch 16/GPU, random symplectic ABCD, iid CN(0,1)"),
     4: (4096, 32, "c64", "C4: 4096x4096 complex64, batch 32/GPU, random symplectic ABCD, iid CN(0,1)"),
@@ -271,7 +272,8 @@ def run_ours(args):
         return run_slab(args, n, M, dtype, desc, world, rank, local, dev)
     gen = torch.Generator(device=dev)
     gen.manual_seed(synth.SEED_BASE + 1000 * args.config + rank)
-    x = torch.randn((batch, n, n), dtype=torch.complex64, device=dev, generator=gen)   # CN(0,1)
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    x = torch.randn((batch, n, n), dtype=tdt, device=dev, generator=gen)   # CN(0,1)
     out = torch.empty_like(x)
     plan = nslct.Plan(n, M, batch, dtype=dtype, profile=True, device=local, schedule=args.schedule,
                       variant=args.variant)
@@ -341,7 +343,7 @@ def run_ours(args):
     # end-to-end through the public C API with host buffers (H2D + exec + D2H per step)
     e2e = None
     if not args.no_e2e:
-        hin = torch.empty((batch, n, n), dtype=torch.complex64).pin_memory()
+        hin = torch.empty((batch, n, n), dtype=tdt).pin_memory()
         hin.copy_(x.cpu())
         hout = torch.empty_like(hin).pin_memory()
         plan.exec_host(hin, hout, stream)        # exec_host records no per-pass events
@@ -356,7 +358,7 @@ def run_ours(args):
         t_e2e = max_over_ranks(t_e2e, world, dev)
         # the PCIe ceiling of this e2e number: plain pinned copies of the same bytes, each
         # direction alone (exec_host overlaps H2D, passes and D2H chunk by chunk)
-        dbuf = torch.empty((batch, n, n), dtype=torch.complex64, device=dev)
+        dbuf = torch.empty((batch, n, n), dtype=tdt, device=dev)
         t_dir = []
         for direction in ("h2d", "d2h"):
             ts = []
@@ -385,10 +387,10 @@ def run_ours(args):
             ts.append(time.perf_counter() - t1)
         t_bidir = min(ts)
         del dbuf, dbuf2
-        e2e = {"value": total_units / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(hin.numel() * 8),
-               "d2h_bytes_per_step": int(hout.numel() * 8), "steps": nst,
-               "h2d_gbs": hin.numel() * 8 / t_dir[0] / 1e9, "d2h_gbs": hout.numel() * 8 / t_dir[1] / 1e9,
-               "bidir_gbs": (hin.numel() + hout.numel()) * 8 / t_bidir / 1e9,
+        e2e = {"value": total_units / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(hin.numel() * S),
+               "d2h_bytes_per_step": int(hout.numel() * S), "steps": nst,
+               "h2d_gbs": hin.numel() * S / t_dir[0] / 1e9, "d2h_gbs": hout.numel() * S / t_dir[1] / 1e9,
+               "bidir_gbs": (hin.numel() + hout.numel()) * S / t_bidir / 1e9,
                "pcie_bound_value": total_units / max(max(t_dir), t_bidir),
                "how": "nslct_exec_host: pinned host in -> device, %d launches, device -> pinned host out, "
                       "pipelined in ~64 MiB image chunks over two copy streams; wall clock per call "
