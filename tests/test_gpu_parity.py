@@ -875,3 +875,66 @@ def test_symm_mem_peer_exchange_single_rank(n):
     rel = float(torch.linalg.vector_norm((G - G1).to(torch.complex128)) /
                 torch.linalg.vector_norm(G1.to(torch.complex128)))
     assert rel <= 1e-6, rel
+
+
+def test_exec_pass_batched_equals_exec():
+    """nslct_exec_pass on a batched plan (the debugging entry point): running the plan's
+    passes one by one through the documented intermediate buffers gives exactly nslct_exec
+    (pipe, warp-specialised and on-chip-capable sizes)."""
+    for n in (1024, 4096):
+        mr, ir = synth.config_streams(960 + n)
+        M = synth.random_symplectic(mr)
+        x = torch.from_numpy(synth.iid_cn(ir, (2, n, n)).astype(np.complex64)).cuda()
+        with nslct.Plan(n, M, 2) as p:
+            ref = p.exec(x)
+            npass = p.info()["n_passes"]
+            bufs = [torch.empty_like(x), torch.empty_like(x)]
+            cur = x
+            for k in range(npass):
+                dst = bufs[k % 2]
+                nslct.lib().nslct_exec_pass(p._h, k, ctypes_ptr(cur), ctypes_ptr(dst),
+                                            ctypes_ptr_stream())
+                cur = dst
+            torch.cuda.synchronize()
+        assert torch.equal(cur, ref), n
+
+
+def ctypes_ptr(t):
+    import ctypes
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def ctypes_ptr_stream():
+    import ctypes
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+@pytest.mark.parametrize("n", [33, 165])
+def test_bluestein_c128_reversibility(n):
+    """Odd N through the Bluestein passes in complex128: exec(M^-1) exec(M) = I to fp64
+    rounding (P5) and Parseval (P4)."""
+    mr, ir = synth.config_streams(970 + n)
+    M = synth.random_symplectic(mr)
+    x = torch.from_numpy(synth.iid_cn(ir, (2, n, n))).cuda()
+    with nslct.Plan(n, M, 2, dtype="c128") as p, nslct.Plan(n, sy.inverse(M), 2, dtype="c128") as pi:
+        G = p.exec(x)
+        back = pi.exec(G)
+    assert float(torch.linalg.vector_norm(back - x) / torch.linalg.vector_norm(x)) < 1e-12
+    assert abs(float(torch.sum(torch.abs(G) ** 2) / torch.sum(torch.abs(x) ** 2)) - 1) < 1e-12
+
+
+def test_zero_padding_lc_and_form_i():
+    """Fused zero-padding with the LC variant and the form-I-only dispatch (165 -> 256 and
+    165 -> 200) against the oracle on the padded field."""
+    mr, ir = synth.config_streams(980)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (1, 165, 165)).astype(np.complex64)
+    for n in (256, 200):
+        for variant, policy in (("LC", "reversible"), ("HA", "formI")):
+            pl = opl.plan(M, variant=variant, policy=policy)
+            with nslct.Plan(n, M, 1, n_in=165, h_fixed=pl["h"],
+                            dispatch="formI" if policy == "formI" else "reversible") as p:
+                G = p.exec(torch.from_numpy(x).cuda()).cpu().numpy()[0]
+            ref, _ = op.nsdlct(op.zero_pad(x[0].astype(np.complex128), n), M,
+                               dx=math.sqrt(2 * math.pi / n), pl=pl, variant=variant)
+            assert me.rel_l2(G, ref) <= 1e-4, (n, variant, policy)
