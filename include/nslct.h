@@ -129,8 +129,8 @@ nslct_status nslct_exec(nslct_plan_t plan, const void* in, void* out, void* cuda
 
 /* Same transform from HOST memory: copies host_in -> device, runs the passes, copies the
  * result back to host_out, and returns only when host_out holds the result.  The batch
- * runs as a pipeline of chunks of whole images (about 64 MiB each; NSLCT_HOST_CHUNK_MB
- * overrides): the host->device copy of chunk i+1 (on a plan-owned copy stream), the
+ * runs as a pipeline of chunks of whole images (at most 64 MiB and about 1/8 of the batch
+ * each; NSLCT_HOST_CHUNK_MB overrides): the host->device copy of chunk i+1 (on a plan-owned copy stream), the
  * passes of chunk i (on cuda_stream) and the device->host copy of chunk i-1 (a second
  * plan-owned copy stream) overlap, so a large batch costs about one PCIe direction, not
  * both plus the compute.  The copies start after the work already queued on cuda_stream.

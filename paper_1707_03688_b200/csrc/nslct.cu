@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>   // PFN_cuTensorMapEncodeTiled (driver entry point, no -lcuda)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1155,12 +1156,14 @@ nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* ou
 // Images per exec_host chunk: about 64 MiB per copy (NSLCT_HOST_CHUNK_MB overrides), so
 // the H2D of chunk i+1, the passes of chunk i and the D2H of chunk i-1 overlap.
 static int64_t host_chunk_images(const nslct_plan_s* pl) {
-  double mb = 64.0;
+  const double img = (double)pl->n * (double)pl->n * (double)pl->elem;
+  // at most 64 MiB per chunk, and at least ~8 chunks when the batch allows it, so small
+  // batches still overlap their copies with the passes
+  double mb = std::min(64.0, img * (double)pl->batch / 8.0 / 1048576.0);
   if (const char* e = std::getenv("NSLCT_HOST_CHUNK_MB")) {
     const double v = std::atof(e);
     if (v > 0) mb = v;
   }
-  const double img = (double)pl->n * (double)pl->n * (double)pl->elem;
   int64_t c = (int64_t)(mb * 1048576.0 / img);
   if (c < 1) c = 1;
   if (c > pl->batch) c = pl->batch;
