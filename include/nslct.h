@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define NSLCT_ABI_VERSION 3
+#define NSLCT_ABI_VERSION 4
 
 typedef enum { NSLCT_C64 = 0, NSLCT_C128 = 1 } nslct_dtype;
 
@@ -49,7 +49,7 @@ typedef enum {
   NSLCT_E_UNSUPPORTED_N = 4,   /* N outside [2, 4096] and not a power of two <= 16384 (c128:
                                   8192); or no on-chip kernel for NSLCT_SCHEDULE_ON_CHIP     */
   NSLCT_E_CUDA = 5,            /* a CUDA launch/copy/allocation call failed (see last_error)  */
-  NSLCT_E_NCCL = 6,            /* reserved for the slab-sharded mode                          */
+  NSLCT_E_NCCL = 6,            /* NCCL unavailable, or an NCCL call of the slab mode failed     */
   NSLCT_E_OOM = 7              /* device allocation of the plan's scratch failed              */
 } nslct_status;
 
@@ -90,8 +90,33 @@ typedef struct {
                          n/2 - n_in/2 + n_in)), zeros elsewhere; same dx; the output is
                          [batch][n][n].  Padded plans cannot run in place and have no
                          row-slab form.                                                    */
+  int kernels;        /* NSLCT_KERNELS_*: which kernel family runs the line passes        */
+  int host_chunk_kb;  /* nslct_exec_host pipeline chunk (KiB); 0 = min(64 MiB, batch bytes / 8) */
+  void* comm;         /* NULL: single GPU.  An nslct_comm_t from nslct_comm_init: the plan is
+                         ONE n x n transform row-slab sharded over the communicator's ranks
+                         (SURVEY.md §8(e)); `batch` must be 1, and nslct_exec runs every pass
+                         and every all-to-all on its stream (see nslct_exec).               */
+  int exchange_chunks;/* slab mode: chunks per pass whose all-to-all overlaps the next
+                         chunk's compute (1, 2, 4 or 8; 0 = 2)                            */
+  int exchange;       /* slab mode: NSLCT_EXCHANGE_*                                        */
   int reserved[4];
 } nslct_opts;
+/* how a comm plan moves data between passes */
+enum { NSLCT_EXCHANGE_NCCL = 0,   /* NCCL grouped send/recv of each chunk's sub-blocks, on a
+                                     plan-owned stream, overlapping the next chunk's compute */
+       NSLCT_EXCHANGE_PEER = 1    /* the transposing pass stores row-block s of its output
+                                     straight into rank s's receive buffer over NVLink (CUDA
+                                     IPC peer mappings made at plan time; nranks <= 8), one
+                                     stream-ordered cross-rank barrier (a 4-byte NCCL
+                                     all-reduce) after each such pass: no separate exchange
+                                     phase and no send buffer                                */
+};
+/* kernel families (all compute the same operator) */
+enum { NSLCT_KERNELS_AUTO = 0,     /* the specialised kernels where they exist: persistent
+                                      TMA pipe (c64, N = 1024..4096), cluster pairs (c64,
+                                      N = 8192, 16384), on-chip (see schedule)              */
+       NSLCT_KERNELS_GENERIC = 1   /* one CTA per group of lines everywhere (A/B reference)  */
+};
 /* schedules of a batched plan (all compute the same operator) */
 enum { NSLCT_SCHEDULE_AUTO = 0,        /* the on-chip kernel for N <= 64 (measured faster at
                                           every batch size: tools/schedule_sweep.py,
@@ -124,20 +149,35 @@ nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16],
  * (in: [batch][n_in][n_in] for a zero-padding plan), 16-byte aligned, owned by the
  * caller; in == out is allowed (not for a padding plan).  Asynchronous and
  * stream-ordered: no host synchronisation, no allocation.  At most one exec per plan in
- * flight (the plan's scratch is shared).  Errors: E_ARG (null/misaligned), E_CUDA. */
+ * flight (the plan's scratch is shared).  Errors: E_ARG (null/misaligned), E_CUDA.
+ *
+ * Slab plans (opts.comm set): in/out are this rank's row slab [L][n], L = n/nranks (rows
+ * [rank*L, (rank+1)*L) of the input and of the output).  Every rank calls nslct_exec with
+ * its slab; the call enqueues the n_passes passes and, between consecutive passes, the
+ * all-to-all that re-shards row slabs into column slabs and back (the distributed form of
+ * the transposes the single-GPU passes fold into their stores): NCCL
+ * grouped send/recv of L x L/c sub-blocks, chunk by chunk (c = opts.exchange_chunks), on
+ * a plan-owned stream ordered after each chunk's pass, so chunk k's exchange overlaps
+ * chunk k+1's compute -- or, with opts.exchange = NSLCT_EXCHANGE_PEER, fused into the
+ * passes' stores to the peers' receive buffers.  Creating a comm plan is collective (every
+ * rank of the communicator, same arguments: the PEER mode exchanges IPC handles).
+ * Errors: additionally E_NCCL. */
 nslct_status nslct_exec(nslct_plan_t plan, const void* in, void* out, void* cuda_stream);
 
 /* Same transform from HOST memory: copies host_in -> device, runs the passes, copies the
  * result back to host_out, and returns only when host_out holds the result.  The batch
  * runs as a pipeline of chunks of whole images (at most 64 MiB and about 1/8 of the batch
- * each; NSLCT_HOST_CHUNK_MB overrides): the host->device copy of chunk i+1 (on a plan-owned copy stream), the
+ * each; opts.host_chunk_kb overrides): the host->device copy of chunk i+1 (on a plan-owned
+ * copy stream), the
  * passes of chunk i (on cuda_stream) and the device->host copy of chunk i-1 (a second
  * plan-owned copy stream) overlap, so a large batch costs about one PCIe direction, not
  * both plus the compute.  The copies start after the work already queued on cuda_stream.
  * host buffers [batch][n][n] complex (host_in [batch][n_in][n_in] for a padding plan;
  * pinned memory gives full copy speed and overlap).
  * Device staging buffers, copy streams and events are created on the first call and
- * owned by the plan.  Errors: E_ARG (null pointers, slab plan), E_CUDA, E_OOM. */
+ * owned by the plan.  Errors: E_ARG (null pointers, slab plan, or -- for a zero-padding
+ * plan, whose output chunks are larger than its input chunks -- overlapping host_in /
+ * host_out ranges), E_CUDA, E_OOM. */
 nslct_status nslct_exec_host(nslct_plan_t plan, const void* host_in, void* host_out,
                              void* cuda_stream);
 
@@ -178,6 +218,25 @@ nslct_status nslct_exec_pass(nslct_plan_t plan, int pass, const void* in, void* 
  * Asynchronous on cuda_stream; no allocation.  Errors: E_ARG, E_CUDA. */
 nslct_status nslct_exec_pass_peer(nslct_plan_t plan, int pass, const void* in, void* const* peer_out,
                                   int n_peers, void* cuda_stream);
+
+/* ---- multi-GPU communicator (slab mode) ----------------------------
+ * NCCL is loaded at run time (dlopen of libnccl.so.2: the copy already mapped into the
+ * process, e.g. PyTorch's, else the system one); the library does not link it.  One
+ * process per GPU: rank 0 calls nslct_comm_unique_id and distributes the 128 bytes (e.g.
+ * through torch.distributed), then every rank calls nslct_comm_init with the CUDA device
+ * it will run on current.  Errors: E_NCCL (library not found, NCCL error), E_ARG. */
+typedef struct nslct_comm_s* nslct_comm_t;
+nslct_status nslct_comm_unique_id(uint8_t unique_id[128]);
+nslct_status nslct_comm_init(nslct_comm_t* comm, const uint8_t unique_id[128], int rank, int nranks);
+/* rank / number of ranks of a communicator */
+nslct_status nslct_comm_info(nslct_comm_t comm, int* rank, int* nranks);
+/* Free the communicator (after every plan using it has been destroyed).  NULL is a no-op. */
+nslct_status nslct_comm_destroy(nslct_comm_t comm);
+
+/* The inverse transform's matrix M^-1 = (D^T, -B^T; -C^T, A^T) of Eq. CCCMCCCM20
+ * (it inverts any matrix satisfying Eq. Intro12), row-major 4x4 as in
+ * nslct_plan.  out may alias abcd.  Errors: E_ARG (null pointer). */
+nslct_status nslct_inverse_matrix(const double abcd[16], double out[16]);
 
 typedef struct {
   int kind;                    /* 0 = B=0 (Eq. Intro20), 1 = form I (Eq. HA28), 2 = form II,

@@ -20,6 +20,21 @@ FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-li
          "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v"]
 
 
+def nccl_include():
+    """Directory of nccl.h (types only: the library dlopens libnccl.so.2 at run time).
+    The NCCL wheel PyTorch ships with, else the system header."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for loc in (spec.submodule_search_locations or []) if spec else []:
+            d = os.path.join(loc, "include")
+            if os.path.exists(os.path.join(d, "nccl.h")):
+                return d
+    except Exception:
+        pass
+    return "/usr/include"
+
+
 def up_to_date():
     if not os.path.exists(LIB):
         return False
@@ -35,7 +50,7 @@ def build(force=False, verbose=False):
     objs, procs, logs = [], [], []
     for src in SOURCES:
         obj = os.path.join(HERE, "build_" + os.path.basename(src) + ".o")
-        cmd = [NVCC] + FLAGS + EXTRA + ["-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        cmd = [NVCC] + FLAGS + EXTRA + ["-I", os.path.join(ROOT, "include"), "-I", nccl_include(), "-c", src, "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
     ok = True
@@ -46,7 +61,7 @@ def build(force=False, verbose=False):
             ok = False
             sys.stderr.write(err[-4000:])
     if ok:
-        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp"] + objs
+        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp"] + objs + ["-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(" ".join(cmd) + "\n" + res.stdout + res.stderr)
         if res.returncode != 0:

@@ -28,11 +28,6 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-// The persistent c64 kernels cache their twiddle powers in tensor memory (TwTmem);
-// -DNSLCT_NO_TMEM_TWIDDLES regenerates them from per-thread bases instead (TwSet).
-#ifndef NSLCT_NO_TMEM_TWIDDLES
-#define NSLCT_TMEM_TWIDDLES 1
-#endif
 
 namespace nslct {
 
@@ -83,74 +78,6 @@ __device__ __forceinline__ cpx<T> cmul_1pj(cpx<T> a, T r) {
   return {r * (a.x - a.y), r * (a.x + a.y)};
 }
 
-// ---- complex64 on sm_100a: packed fp32x2 arithmetic (FADD2 / FMUL2 / FFMA2) --------
-// One packed instruction does both halves of a complex add; a complex multiply is
-// FMUL2 + FFMA2.  ptxas folds the lane swaps / broadcasts / single-lane negations of
-// the packing moves into operand selectors, so these helpers cost no extra moves.
-// (Packed ops halve issue slots, not FP-pipe cycles: tools/micro_fp.cu.)
-typedef unsigned long long u64;
-__device__ __forceinline__ u64 pk2(float x, float y) {
-  u64 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
-  return r;
-}
-__device__ __forceinline__ cpx<float> up2(u64 v) {
-  cpx<float> r;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
-  return r;
-}
-__device__ __forceinline__ u64 add2(u64 a, u64 b) {
-  u64 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
-  u64 d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
-  u64 d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
-  u64 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-#ifdef NSLCT_PACKED_FP32   // opt-in: measured ~4% slower than scalar in the 512-thread pass
-template <>
-__device__ __forceinline__ cpx<float> cadd<float>(cpx<float> a, cpx<float> b) {
-  return up2(add2(pk2(a.x, a.y), pk2(b.x, b.y)));
-}
-template <>
-__device__ __forceinline__ cpx<float> csub<float>(cpx<float> a, cpx<float> b) {
-  return up2(sub2(pk2(a.x, a.y), pk2(b.x, b.y)));
-}
-template <>
-__device__ __forceinline__ cpx<float> cmul<float>(cpx<float> a, cpx<float> b) {
-  // (ax bx, ay bx) + (-ay, ax) * by
-  return up2(fma2(pk2(-a.y, a.x), pk2(b.y, b.y), mul2(pk2(a.x, a.y), pk2(b.x, b.x))));
-}
-template <>
-__device__ __forceinline__ cpx<float> cscale<float>(cpx<float> a, float s) {
-  return up2(mul2(pk2(a.x, a.y), pk2(s, s)));
-}
-template <>
-__device__ __forceinline__ cpx<float> crot<float>(cpx<float> a, float c, float s) {
-  // (x, y) c + (y, -x) s
-  return up2(fma2(pk2(a.x, a.y), pk2(c, c), mul2(pk2(a.y, -a.x), pk2(s, s))));
-}
-template <>
-__device__ __forceinline__ cpx<float> cmul_1mj<float>(cpx<float> a, float r) {
-  return up2(mul2(add2(pk2(a.x, a.y), pk2(a.y, -a.x)), pk2(r, r)));
-}
-template <>
-__device__ __forceinline__ cpx<float> cmul_1pj<float>(cpx<float> a, float r) {
-  return up2(mul2(add2(pk2(a.x, a.y), pk2(-a.y, a.x)), pk2(r, r)));
-}
-#endif  // NSLCT_PACKED_FP32
 
 // ---------------------------------------------------------------------------------
 // Small DFTs in registers (forward, e^{-2 pi i n k / R}), natural order in and out.
@@ -318,7 +245,6 @@ struct FftShape {
 
 template <typename T, int LOG2N>
 struct TwSet {
-  static constexpr bool kFft64 = false;
   static constexpr bool kBluestein = false;
   using Sh = FftShape<LOG2N>;
   static constexpr int NBMAX = 16 / Sh::template R<Sh::NS - 1>() > 1 ? 16 / Sh::template R<Sh::NS - 1>() : 1;
@@ -399,7 +325,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t ta, const float (&f)[16]) {
 
 template <int LOG2N>
 struct TwTmem {
-  static constexpr bool kFft64 = false;
   static constexpr bool kBluestein = false;
   using Sh = FftShape<LOG2N>;
   uint32_t ta;   // this thread's TMEM address: lane quadrant + its warp's column base
@@ -460,153 +385,6 @@ struct TwTmem {
     }
   }
 };
-
-// ---------------------------------------------------------------------------------
-// 4096-point line FFT as 64 x 64 with tensor-memory quad exchanges (c64 pipe kernel).
-//
-// Same contract as line_fft: thread j (256 per line) holds x[j + 256 e], e = 0..15, in
-// and X[j + 256 e] out.  With p = j % 64, m = j / 64, n = n1 + 64 n2, k = k2 + 64 k1:
-//   step 1  Y[n1][k2]  = DFT64 over n2 of x[n1 + 64 n2]      (n1 = p, n2 = m + 4e)
-//   step 2  Y'[n1][k2] = W4096^(n1 k2) Y[n1][k2]
-//   step 3  X[k2 + 64 k1] = DFT64 over n1 of Y'[n1][k2]      (k2 = p, n1 = m + 4e)
-// Each DFT64 over an index r = m + 4e is a DFT16 over e in registers, the twiddle
-// W64^(m a), and a DFT4 over m ACROSS the four threads p + 64m.  Those four threads sit
-// in warps (p/16) + 4m at the same lane, i.e. on the same TMEM lane, so the DFT4 inputs
-// are exchanged through tensor memory (tcgen05.st / tcgen05.ld; thread m keeps outputs
-// a = m + 4i, which makes the output distribution equal the input one).  Only the
-// step 2 -> 3 transpose goes through shared memory: ONE exchange per FFT instead of the
-// Stockham kernel's two (shared-memory traffic was the floor of the 2-FFT passes,
-// DESIGN.md §6.6).  TMEM columns (512 per CTA): warp w keeps its constants in
-// [64 (w/4), +62) -- W64^(m a), a = 1..15, then W4096^(p k2) for its 16 k2 -- and the
-// quad exchanges alternate between two 128-column buffers at 256 and 384.
-// ---------------------------------------------------------------------------------
-__device__ __forceinline__ void tmem_st8(uint32_t ta, float a0, float a1, float a2, float a3, float a4,
-                                         float a5, float a6, float a7) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
-               "r"(__float_as_uint(a0)), "r"(__float_as_uint(a1)), "r"(__float_as_uint(a2)),
-               "r"(__float_as_uint(a3)), "r"(__float_as_uint(a4)), "r"(__float_as_uint(a5)),
-               "r"(__float_as_uint(a6)), "r"(__float_as_uint(a7))
-               : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t ta, float (&f)[32]) {
-  uint32_t v[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(ta)
-      : "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-}
-
-struct TwFft64 {
-  static constexpr bool kFft64 = true;
-  static constexpr bool kBluestein = false;
-  uint32_t tcol;   // lane quadrant << 16 | this warp's 64 constant columns
-  uint32_t xcol;   // lane quadrant << 16 | column 256 (two 128-column exchange buffers)
-  int m;           // j / 64 (warp-uniform)
-  int p;           // j % 64
-  int q;           // warp % 4: the quad's named barrier is 1 + q (128 threads)
-  // once per kernel: this thread's constants from the fp64-accurate table tw[k] = W4096^k
-  __device__ __forceinline__ void fill(const cpx<float>* __restrict__ tw) const {
-    float f[32];
-#pragma unroll
-    for (int a = 1; a < 16; ++a) {
-      const cpx<float> w = tw[(64 * m * a) & 4095];
-      f[2 * (a - 1)] = w.x;
-      f[2 * (a - 1) + 1] = w.y;
-    }
-    f[30] = f[31] = 0.f;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      tmem_st8(tcol + 8 * c, f[8 * c], f[8 * c + 1], f[8 * c + 2], f[8 * c + 3], f[8 * c + 4], f[8 * c + 5],
-               f[8 * c + 6], f[8 * c + 7]);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {   // r = i + 4b  <->  k2 = m + 4i + 16b
-      const int k2 = m + 4 * (r & 3) + 16 * (r >> 2);
-      const cpx<float> w = tw[(p * k2) & 4095];
-      f[2 * r] = w.x;
-      f[2 * r + 1] = w.y;
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      tmem_st8(tcol + 32 + 8 * c, f[8 * c], f[8 * c + 1], f[8 * c + 2], f[8 * c + 3], f[8 * c + 4],
-               f[8 * c + 5], f[8 * c + 6], f[8 * c + 7]);
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-  }
-  template <int S>
-  __device__ __forceinline__ void prefetch() const {}
-  // v[a] *= W64^(m a)
-  __device__ __forceinline__ void twiddle64(cpx<float> (&v)[16]) const {
-    float h[32];
-    tmem_ld32(tcol, h);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int a = 1; a < 16; ++a) v[a] = cmul(v[a], cpx<float>{h[2 * (a - 1)], h[2 * (a - 1) + 1]});
-  }
-  // v[r] *= W4096^(p k2(r))
-  __device__ __forceinline__ void twiddle4096(cpx<float> (&v)[16]) const {
-    float h[32];
-    tmem_ld32(tcol + 32, h);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = cmul(v[r], cpx<float>{h[2 * r], h[2 * r + 1]});
-  }
-  // DFT4 over m across the quad: in v[a] = V_m[a]; out v[i + 4b] = sum_m' W4^(m' b) V_m'[m + 4i]
-  template <int B>
-  __device__ __forceinline__ void quad_dft4(cpx<float> (&v)[16]) const {
-    const uint32_t base = xcol + 128 * B;
-    // V[a] -> column (a % 4) * 32 + m * 8 + (a / 4) * 2: reader m' takes columns m' * 32 .. +31
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      tmem_st8(base + 32 * c + 8 * m, v[c].x, v[c].y, v[c + 4].x, v[c + 4].y, v[c + 8].x, v[c + 8].y,
-               v[c + 12].x, v[c + 12].y);
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    asm volatile("bar.sync %0, 128;" ::"r"(1 + q) : "memory");
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    float h[32];
-    tmem_ld32(base + 32 * m, h);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      cpx<float> a0{h[2 * i], h[2 * i + 1]}, a1{h[8 + 2 * i], h[9 + 2 * i]};
-      cpx<float> a2{h[16 + 2 * i], h[17 + 2 * i]}, a3{h[24 + 2 * i], h[25 + 2 * i]};
-      dft4(a0, a1, a2, a3);
-      v[i] = a0;
-      v[i + 4] = a1;
-      v[i + 8] = a2;
-      v[i + 12] = a3;
-    }
-  }
-};
-
-// X = exchange index of this FFT's shared-memory transpose (ExPad2 buffer alternation)
-template <int X, class E>
-__device__ __forceinline__ void fft64x64(cpx<float> (&v)[16], const TwFft64& t, const E& ex) {
-  // step 1: DFT64 over n2 = m + 4e for n1 = p
-  dft<16>(v);
-  if (t.m != 0) t.twiddle64(v);
-  t.quad_dft4<0>(v);   // v[i + 4b] = Y[p][m + 4i + 16b]
-  // step 2: twiddle, transpose through shared memory: Y'[n1][k2] at k2 * 65 + n1
-  t.twiddle4096(v);
-  cpx<float>* buf = ex.template b<X>();
-#pragma unroll
-  for (int r = 0; r < 16; ++r) buf[(t.m + 4 * (r & 3) + 16 * (r >> 2)) * 65 + t.p] = v[r];
-  ex.template sync<X>();
-  ex.template after_barrier<X>();
-  const cpx<float>* rb = buf + t.p * 65 + t.m;
-#pragma unroll
-  for (int e = 0; e < 16; ++e) v[e] = rb[4 * e];   // Y'[m + 4e][p]
-  // step 3: DFT64 over n1 = m + 4e for k2 = p  ->  v[e] = X[p + 64 (m + 4e)] = X[j + 256 e]
-  dft<16>(v);
-  if (t.m != 0) t.twiddle64(v);
-  t.quad_dft4<1>(v);
-}
 
 // Exchange policies (how a stage hands its outputs to the next stage through shared
 // memory).  X is the compile-time index of the exchange within the pass.
@@ -744,7 +522,6 @@ struct FftInfo {
 // ---------------------------------------------------------------------------------
 template <typename T, int LOG2M>
 struct TwBluestein {
-  static constexpr bool kFft64 = false;
   static constexpr bool kBluestein = true;
   TwSet<T, LOG2M> inner;   // twiddles of the length-M FFT
   const cpx<T>* __restrict__ bq;
@@ -779,9 +556,6 @@ template <typename T, int LOG2N, int X0, class E, class TW>
 __device__ __forceinline__ void line_fft(cpx<T> (&v)[16], int j, const TW& tw, const E& ex) {
   if constexpr (TW::kBluestein) {
     bluestein_dft<T, LOG2N, X0>(v, j, tw, ex);
-  } else if constexpr (TW::kFft64) {
-    static_assert(LOG2N == 12, "the 64x64 FFT is for N = 4096");
-    fft64x64<X0>(v, tw, ex);
   } else {
     FftStages<T, LOG2N, 0, FftInfo<LOG2N>::NS, X0, E, TW>::run(v, j, tw, ex);
   }
@@ -789,7 +563,7 @@ __device__ __forceinline__ void line_fft(cpx<T> (&v)[16], int j, const TW& tw, c
 // shared-memory exchanges per line FFT
 template <int LOG2N, class TW>
 struct FftNX {
-  static constexpr int value = TW::kFft64 ? 1 : FftInfo<LOG2N>::NX;
+  static constexpr int value = FftInfo<LOG2N>::NX;
 };
 
 // ---------------------------------------------------------------------------------
@@ -936,6 +710,17 @@ struct PassArgs {
   void* peer_out[8];
   int peer_on, peer_rank;
   int persist_ctas;   // persistent cluster-pair kernels: grid size (even; 0 = one per line)
+  // Row-slab launches of a chunk of the rank's lines (nslct_exec over a communicator: the
+  // all-to-all of chunk c overlaps the compute of chunk c+1): this launch processes local
+  // lines [line_base, line_base + n_lines), and a transposing pass stores its [N][L]
+  // output as L x L blocks (block s for rank s) each made of L/out_chunk sub-blocks of
+  // L x out_chunk, sub-block c holding producer lines [c out_chunk, (c+1) out_chunk):
+  //   element (consumer line lam of block s, producer line ll) at
+  //   s L^2 + (ll / Lc) L Lc + lam Lc + ll % Lc        (Lc = out_chunk; Lc = L: [N][L])
+  // (pair kernels: the pair-interleaved order inside each sub-block).  The consumer then
+  // reads its lines with in_chunk = Lc, in_chunk_stride = L Lc.
+  int line_base;
+  int out_chunk;
 };
 
 // The per-line work of one pass (registers v hold elements j + TL*e of line l).
@@ -1032,7 +817,7 @@ line_pass_kernel(PassArgs a) {
   const int j = tid % TL;
   const int gl = tid / TL;
   const int L = a.lines_per_img;
-  const long long line0 = (long long)blockIdx.x * G;   // first line (over the batch) of this CTA
+  const long long line0 = (long long)blockIdx.x * G + a.line_base;   // first line (over the batch) of this CTA
   const long long line = line0 + gl;
   const long long img = line / L;
   const int ll = (int)(line % L);                       // local line within the image
@@ -1083,15 +868,20 @@ line_pass_kernel(PassArgs a) {
     for (int e = 0; e < 16; ++e) buf[pad16(j + TL * e)] = v[e];
     __syncthreads();
     const int l0 = (int)(line0 % L);
+    // block s = e / L, sub-block c = ll / Lc (see PassArgs::out_chunk); Lc = L = N for
+    // batched plans reduces this to out[e L + ll]
+    const int lgL = __ffs(L) - 1, lgLc = __ffs(a.out_chunk) - 1;
+    const int Lc = 1 << lgLc;
     if (a.peer_on) {   // fused exchange: block e / L goes to rank e / L
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         const int f = tid + k * THREADS;
         const int gg = f % G;
         const int e = f / G;
-        const int sblk = e / L;
+        const int sblk = e >> lgL, ll2 = l0 + gg;
         cpx<T>* dst = reinterpret_cast<cpx<T>*>(a.peer_out[sblk]) + (long long)a.peer_rank * L * L;
-        dst[(long long)(e - sblk * L) * L + l0 + gg] = smem[gg * LS + pad16(e)];
+        dst[((long long)(ll2 >> lgLc) << (lgL + lgLc)) + ((long long)(e & (L - 1)) << lgLc) + (ll2 & (Lc - 1))] =
+            smem[gg * LS + pad16(e)];
       }
     } else {
 #pragma unroll
@@ -1099,7 +889,9 @@ line_pass_kernel(PassArgs a) {
         const int f = tid + k * THREADS;
         const int gg = f % G;
         const int e = f / G;
-        out[(long long)e * L + l0 + gg] = smem[gg * LS + pad16(e)];
+        const int ll2 = l0 + gg;
+        out[((long long)(e >> lgL) << (2 * lgL)) + ((long long)(ll2 >> lgLc) << (lgL + lgLc)) +
+            ((long long)(e & (L - 1)) << lgLc) + (ll2 & (Lc - 1))] = smem[gg * LS + pad16(e)];
       }
     }
   }
@@ -1223,29 +1015,16 @@ __device__ __forceinline__ void load_group(cpx<T>* dst, const cpx<T>* src, uint6
   }
 }
 
-// The persistent kernels' TMEM-resident twiddles: the 64x64 FFT's constants at N = 4096
-// (NSLCT_FFT64), else the Stockham stage powers.  lanebase = TMEM base | lane quadrant.
-template <int LOG2N, bool F64>
-struct TwMaker {
-  using type = TwTmem<LOG2N>;
-  __device__ static type make(uint32_t lanebase, int warp, int j, const cpx<float>* __restrict__ tw) {
-    const type t{lanebase + (uint32_t)((warp >> 2) * 128)};
-    t.fill(tw, j);
-    return t;
-  }
-};
+// The persistent kernels' TMEM-resident twiddles (TwTmem): lanebase = TMEM base | lane
+// quadrant; warp w takes columns (w/4)*128.
 template <int LOG2N>
-struct TwMaker<LOG2N, true> {
-  using type = TwFft64;
-  __device__ static type make(uint32_t lanebase, int warp, int j, const cpx<float>* __restrict__ tw) {
-    const type t{lanebase + (uint32_t)(64 * (warp >> 2)), lanebase + 256u, j / 64, j % 64, warp & 3};
-    t.fill(tw);
-    return t;
-  }
-};
-// F64: the 64x64 TMEM-exchange FFT at N = 4096 (parity-verified, measured 3% slower than
-// the Stockham kernel; selected at plan time by NSLCT_FFT64=1).
-template <typename T, int LOG2N, int MODE, bool F64 = false>
+__device__ __forceinline__ TwTmem<LOG2N> make_tw_tmem(uint32_t lanebase, int warp, int j,
+                                                     const cpx<float>* __restrict__ tw) {
+  const TwTmem<LOG2N> t{lanebase + (uint32_t)((warp >> 2) * 128)};
+  t.fill(tw, j);
+  return t;
+}
+template <typename T, int LOG2N, int MODE>
 __global__ void __launch_bounds__(512, 1)
 line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counter,
                       const __grid_constant__ CUtensorMap omap) {
@@ -1269,8 +1048,8 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
   const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in);
   cpx<T>* __restrict__ out = reinterpret_cast<cpx<T>*>(a.out);
 
-#ifdef NSLCT_TMEM_TWIDDLES
   // this thread's twiddle powers, the same for every group, cached in TMEM (TwTmem)
+  static_assert(sizeof(T) == 4, "the persistent pipe kernels are complex64");
   const int warp = tid >> 5;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_taddr)));
@@ -1280,14 +1059,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *s_taddr;
-  static_assert(!F64 || LOG2N == 12, "the 64x64 FFT is for N = 4096");
-  using Maker = TwMaker<LOG2N, F64>;
-  const typename Maker::type tws = Maker::make(tmem_base + ((uint32_t)(32 * (warp & 3)) << 16), warp, j, tw);
-#else
-  (void)s_taddr;
-  TwSet<T, LOG2N> tws;   // this thread's twiddle bases, the same for every group
-  tws.load(tw, j);
-#endif
+  const TwTmem<LOG2N> tws = make_tw_tmem<LOG2N>(tmem_base + ((uint32_t)(32 * (warp & 3)) << 16), warp, j, tw);
 
   // Groups are claimed in order from a global counter (not round-robin) so the groups
   // in flight across the GPU stay a contiguous window: the segments of the transposed
@@ -1415,11 +1187,9 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     bx = free_i;
   }
   if (tid == 0) bulk_wait0();
-#ifdef NSLCT_TMEM_TWIDDLES
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
-#endif
 }
 
 // ---------------------------------------------------------------------------------
@@ -1555,9 +1325,8 @@ line_pass_ws_kernel(PassArgs a, long long n_groups, unsigned long long* counter,
   const int gl = tid % G;
   const int j = tid / G;
   const uint32_t tmem_base = *s_taddr;
-  using Maker = TwMaker<LOG2N, false>;
-  const typename Maker::type tws = Maker::make(tmem_base + ((uint32_t)(32 * (warp & 3)) << 16), warp, j,
-                                               reinterpret_cast<const cpx<T>*>(a.tw));
+  const TwTmem<LOG2N> tws = make_tw_tmem<LOG2N>(tmem_base + ((uint32_t)(32 * (warp & 3)) << 16), warp, j,
+                                                reinterpret_cast<const cpx<T>*>(a.tw));
   int bs = 0, bx = 2, bn = 1;
   uint32_t phases = 0;
   for (;;) {
@@ -1657,7 +1426,9 @@ line_pass_pair_kernel(PassArgs a) {
   const int lgC = SLAB ? __ffs(a.in_chunk) - 1 : LOG2N;
   const int L = 1 << lgL, C = 1 << lgC;
   const long long slab_elems = (long long)L * N;
-  const long long npairs = a.n_lines / 2;
+  const long long npairs = a.n_lines / 2;   // this launch: local lines line_base + [0, n_lines)
+  const int lgLc = SLAB ? __ffs(a.out_chunk) - 1 : LOG2N;   // output sub-block width (PassArgs)
+  const int Lc = 1 << lgLc;
   const long long ncl = gridDim.x / 2;              // persistent: clusters stride the pairs
   const long long cl = blockIdx.x / 2;
   const cpx<T>* __restrict__ tw = reinterpret_cast<const cpx<T>*>(a.tw);
@@ -1676,12 +1447,12 @@ line_pass_pair_kernel(PassArgs a) {
   const bool contiguous = !SLAB || ModeIO<MODE>::kUserIn || C == N;
   auto prefetch = [&](long long p) {
     if (!SLAB || contiguous) {
-      const long long line = 2 * p + c;
-      const cpx<T>* src = ModeIO<MODE>::kUserIn ? in + line * N : in + (2 * p) * N + (long long)c * N;
+      const long long line = a.line_base + 2 * p + c;
+      const cpx<T>* src = ModeIO<MODE>::kUserIn ? in + line * N : in + (a.line_base + 2 * p) * N + (long long)c * N;
       bulk_prefetch_l2(src, (uint32_t)(N * sizeof(cpx<T>)));
     } else if constexpr (SLAB) {   // chunked (slab) input: the pair's 2C-element run in every
                                    // block, CTA c taking every other block
-      const long long line = 2 * p;
+      const long long line = a.line_base + 2 * p;
       const long long img = line / L;
       const int lp = (int)(line % L);
       for (int sb = (int)c; sb < N / C; sb += 2)
@@ -1693,7 +1464,7 @@ line_pass_pair_kernel(PassArgs a) {
 
   for (long long p = cl; p < npairs; p += ncl) {
     if (tid == 0 && p + ncl < npairs) prefetch(p + ncl);
-    const long long line = 2 * p + c;                  // over the batch
+    const long long line = a.line_base + 2 * p + c;   // over the batch
     const long long img = line >> lgL;
     const int ll = (int)(line & (L - 1));              // local line
     const int l = a.line_offset + ll;                  // global line (chirps)
@@ -1748,7 +1519,7 @@ line_pass_pair_kernel(PassArgs a) {
           const int sblk = e0 >> lgL, lam = e0 & (L - 1);
           cpx<T>* base = a.peer_on ? reinterpret_cast<cpx<T>*>(a.peer_out[sblk]) + (long long)a.peer_rank * L * L
                                    : out + (long long)sblk * L * L;
-          d = base + (long long)(lam / 2) * 2 * L + 2 * lp;
+          d = base + ((long long)(lp >> lgLc) << (lgL + lgLc)) + (long long)(lam / 2) * 2 * Lc + 2 * (lp & (Lc - 1));
         } else {
           d = out + (long long)q * 2 * N + 2 * lp;
         }

@@ -3,6 +3,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>   // PFN_cuTensorMapEncodeTiled (driver entry point, no -lcuda)
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>           // types only: NCCL is dlopen'ed at run time (nccl_api below)
 
 #include <algorithm>
 #include <cmath>
@@ -97,27 +99,26 @@ struct PairRow {
 
 // persistent TMA-pipelined variant: grid = #SMs (one CTA per SM)
 constexpr size_t kPipeExtra = 64;   // 3 mbarriers + 3 claimed-group slots + TMEM base
-template <typename T, int LOG2N, int MODE, bool F64 = false>
+template <typename T, int LOG2N, int MODE>
 cudaError_t launch_pipe(const PassArgs& a, cudaStream_t s, int grid, unsigned long long* counter,
                         const CUtensorMap& omap) {
   using Cfg = nslct::PipeCfg<LOG2N>;
   const size_t smem = (size_t)Cfg::NBUF * Cfg::BUF_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
   const long long n_groups = a.n_lines / Cfg::G;
   const long long g = n_groups < grid ? n_groups : grid;
-  nslct::line_pass_pipe_kernel<T, LOG2N, MODE, F64><<<(unsigned)g, Cfg::THREADS, smem, s>>>(a, n_groups, counter,
-                                                                                           omap);
+  nslct::line_pass_pipe_kernel<T, LOG2N, MODE><<<(unsigned)g, Cfg::THREADS, smem, s>>>(a, n_groups, counter, omap);
   return cudaGetLastError();
 }
-template <typename T, int LOG2N, int MODE, bool F64 = false>
+template <typename T, int LOG2N, int MODE>
 cudaError_t set_attr_pipe() {
   using Cfg = nslct::PipeCfg<LOG2N>;
   const size_t smem = (size_t)Cfg::NBUF * Cfg::BUF_ELEMS * sizeof(nslct::cpx<T>) + kPipeExtra;
-  return cudaFuncSetAttribute(nslct::line_pass_pipe_kernel<T, LOG2N, MODE, F64>,
+  return cudaFuncSetAttribute(nslct::line_pass_pipe_kernel<T, LOG2N, MODE>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 typedef cudaError_t (*pipe_fn)(const PassArgs&, cudaStream_t, int, unsigned long long*, const CUtensorMap&);
 
-// warp-specialised variant (kernels.cuh line_pass_ws_kernel, opt-in NSLCT_WS=1)
+// warp-specialised variant (kernels.cuh line_pass_ws_kernel): passes of modes 1-3
 template <int LOG2N, int MODE>
 cudaError_t launch_ws(const PassArgs& a, cudaStream_t s, int grid, unsigned long long* counter,
                       const CUtensorMap& omap) {
@@ -185,19 +186,16 @@ nslct_status make_store_map(CUtensorMap* m, void* out, int log2n, long long imag
 
 constexpr int kModes = 6;   // pass modes 0..5 (kernels.cuh pass_body)
 
+// the non-warp-specialised pipe kernel runs the passes that read the user's input (modes
+// 0, 4: measured faster there than the warp-specialised kernel) and the
+// three-FFT LC pass of form II (mode 5); modes 1-3 run line_pass_ws_kernel
 template <typename T, int LOG2N>
 struct PipeRow {
   static void fill(pipe_fn* l, attr_fn* at) {
     l[0] = launch_pipe<T, LOG2N, 0>;
-    l[1] = launch_pipe<T, LOG2N, 1>;
-    l[2] = launch_pipe<T, LOG2N, 2>;
-    l[3] = launch_pipe<T, LOG2N, 3>;
     l[4] = launch_pipe<T, LOG2N, 4>;
     l[5] = launch_pipe<T, LOG2N, 5>;
     at[0] = set_attr_pipe<T, LOG2N, 0>;
-    at[1] = set_attr_pipe<T, LOG2N, 1>;
-    at[2] = set_attr_pipe<T, LOG2N, 2>;
-    at[3] = set_attr_pipe<T, LOG2N, 3>;
     at[4] = set_attr_pipe<T, LOG2N, 4>;
     at[5] = set_attr_pipe<T, LOG2N, 5>;
   }
@@ -261,12 +259,6 @@ struct Table {
   attr_fn atpair[2][kMaxLog + 1][kModes] = {};
   pipe_fn lp[kMaxLog + 1][kModes] = {};   // c64 only
   attr_fn atp[kMaxLog + 1][kModes] = {};
-  pipe_fn lp64[kModes] = {launch_pipe<float, 12, 0, true>, launch_pipe<float, 12, 1, true>,
-                          launch_pipe<float, 12, 2, true>, launch_pipe<float, 12, 3, true>,
-                          launch_pipe<float, 12, 4, true>, launch_pipe<float, 12, 5, true>};
-  attr_fn atp64[kModes] = {set_attr_pipe<float, 12, 0, true>, set_attr_pipe<float, 12, 1, true>,
-                           set_attr_pipe<float, 12, 2, true>, set_attr_pipe<float, 12, 3, true>,
-                           set_attr_pipe<float, 12, 4, true>, set_attr_pipe<float, 12, 5, true>};
   Table() {
     li[0][5] = launch_img<float, 5, 1>, ati[0][5] = set_attr_img<float, 5, 1>;
     li[0][6] = launch_img<float, 6, 1>, ati[0][6] = set_attr_img<float, 6, 1>;
@@ -368,6 +360,74 @@ Phase to_phase(const Poly& P, bool line_is_x) {
 
 }  // namespace
 
+// ---- NCCL, loaded at run time ----------------------------------------------------------
+// The library links no NCCL: dlopen("libnccl.so.2") returns the copy already mapped into
+// the process (glibc matches the soname -- PyTorch's NCCL when torch is loaded), else the
+// one the loader finds.  Only the entry points the slab exchange needs are resolved.
+namespace {
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      const char* e = dlerror();
+      a.err = std::string("dlopen(libnccl.so.2): ") + (e ? e : "not found");
+      return a;
+    }
+    bool ok = true;
+    auto sym = [&](const char* name) {
+      void* f = dlsym(h, name);
+      if (!f) {
+        ok = false;
+        a.err += std::string(a.err.empty() ? "" : "; ") + "missing " + name;
+      }
+      return f;
+    };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(sym("ncclAllGather"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    a.ok = ok;
+    return a;
+  }();
+  return api;
+}
+}  // namespace
+
+#define NCCL_TRY(expr)                                                                      \
+  do {                                                                                      \
+    ncclResult_t r_ = (expr);                                                               \
+    if (r_ != ncclSuccess)                                                                  \
+      return fail(NSLCT_E_NCCL, std::string(#expr) + ": " + nccl_api().GetErrorString(r_)); \
+  } while (0)
+
+struct nslct_comm_s {
+  ncclComm_t c = nullptr;
+  int rank = 0, nranks = 1, device = 0;
+};
+
 struct nslct_plan_s {
   int64_t n = 0, batch = 0;
   int log2n = 0;       // power-of-two plans: log2 N; Bluestein plans: log2 M (FFT length)
@@ -392,15 +452,27 @@ struct nslct_plan_s {
   PassArgs args[5];
   int n_passes = 5;
   int mode[5] = {0, 1, 2, 1, 3};   // HA schedule; LC (y-axis H) uses 3 passes
-  bool slab = false;   // row-slab plan (nslct_plan_slab)
+  bool slab = false;   // row-slab plan (nslct_plan_slab, or nslct_plan_ex with opts.comm)
   int nranks = 1, rank = 0;
+  int64_t L = 0;       // rows of this rank's slab
+  int nc = 1;          // slab: exchange chunks per transposing pass; sub-block width lc = L / nc
+  int64_t lc = 0;
+  nslct_comm_s* comm = nullptr;          // slab plans run by nslct_exec (opts.comm)
+  void* xsend = nullptr;                 // comm plans: pass output / all-to-all send buffer
+  void* xrecv[2] = {nullptr, nullptr};   // all-to-all receive buffers (alternating passes)
+  cudaStream_t cs_comm = nullptr;        // NCCL stream
+  std::vector<cudaEvent_t> xev;          // nc chunk events + 1 exchange-done event
+  int exchange = NSLCT_EXCHANGE_NCCL;    // comm plans: NCCL send/recv, or stores to peers
+  void* peer_recv[2][8] = {};            // PEER: every rank's receive buffer b (own = xrecv[b])
+  bool peer_opened[2][8] = {};           //       ... opened through cudaIpcOpenMemHandle
+  int* xbar = nullptr;                   // PEER: 4-byte all-reduce "barrier" buffer
   bool pipe = false;   // persistent TMA-pipelined kernels
   bool image = false;  // fully on-chip kernel (one launch per exec)
-  bool fft64 = false;  // pipe kernels with the 64x64 TMEM-exchange FFT (N = 4096, opt-in)
-  bool ws = false;     // warp-specialised pipe kernels for modes 1-3 (NSLCT_WS=0 disables)
+  bool ws = false;     // warp-specialised pipe kernels for modes 1-3
   bool pair = false;   // large-N cluster-pair line passes (N = 8192, 16384, complex64)
   unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
   int num_sms = 148;
+  int host_chunk_kb = 0;    // opts.host_chunk_kb (exec_host pipeline chunk; 0 = auto)
   nslct::B0Args b0{};
   nslct::DingArgs ding{};
   struct EvSet {
@@ -413,15 +485,21 @@ struct nslct_plan_s {
 namespace {
 struct DeviceGuard {
   int prev = -1;
+  cudaError_t status = cudaSuccess;   // of the cudaSetDevice (plan_internal validates the ordinal)
   explicit DeviceGuard(int dev) {
     if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    if (prev != dev) cudaSetDevice(dev);
+    if (prev != dev) status = cudaSetDevice(dev);
   }
   ~DeviceGuard() {
     int cur = -1;
     if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
   }
 };
+
+#define GUARD_DEVICE(pl)                                                                  \
+  DeviceGuard guard((pl)->device);                                                        \
+  if (guard.status != cudaSuccess)                                                        \
+  return fail(NSLCT_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(guard.status))
 
 void free_plan(nslct_plan_s* pl) {
   if (!pl) return;
@@ -430,6 +508,16 @@ void free_plan(nslct_plan_s* pl) {
   if (pl->bq) cudaFree(pl->bq);
   if (pl->bhat) cudaFree(pl->bhat);
   if (pl->scratch) cudaFree(pl->scratch);
+  if (pl->xsend) cudaFree(pl->xsend);
+  for (void* r : pl->xrecv)
+    if (r) cudaFree(r);
+  if (pl->cs_comm) cudaStreamDestroy(pl->cs_comm);
+  for (int b = 0; b < 2; ++b)
+    for (int s = 0; s < 8; ++s)
+      if (pl->peer_opened[b][s]) cudaIpcCloseMemHandle(pl->peer_recv[b][s]);
+  if (pl->xbar) cudaFree(pl->xbar);
+  for (auto e : pl->xev)
+    if (e) cudaEventDestroy(e);
   if (pl->counters) cudaFree(pl->counters);
   if (pl->h_in) cudaFree(pl->h_in);
   if (pl->h_out) cudaFree(pl->h_out);
@@ -558,11 +646,54 @@ static bool lc_y(const nslct::Plan& p) {
   return p.kind != 0 && p.H.q11 == 0.0 && p.H.q12 == 0.0 && p.H.q22 != 0.0;
 }
 
+// PEER exchange (NSLCT_EXCHANGE_PEER): map every rank's two receive buffers into this
+// process.  Collective over the plan's communicator: each rank publishes the CUDA IPC
+// handles of its xrecv[0..1] by an NCCL all-gather, then opens the other ranks' (its own
+// buffers are used directly).
+static nslct_status peer_setup(nslct_plan_s* pl) {
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return fail(NSLCT_E_NCCL, api.err);
+  const int P = pl->nranks;
+  constexpr size_t H = sizeof(cudaIpcMemHandle_t);   // 64 bytes
+  std::vector<unsigned char> mine(2 * H), all((size_t)P * 2 * H);
+  for (int b = 0; b < 2; ++b)
+    CUDA_TRY(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(mine.data() + b * H), pl->xrecv[b]));
+  unsigned char* dev = nullptr;
+  CUDA_TRY(cudaMalloc(&dev, (size_t)(P + 1) * 2 * H));
+  cudaError_t e = cudaMemcpy(dev + (size_t)P * 2 * H, mine.data(), 2 * H, cudaMemcpyHostToDevice);
+  ncclResult_t r = ncclSuccess;
+  if (e == cudaSuccess) r = api.AllGather(dev + (size_t)P * 2 * H, dev, 2 * H, ncclInt8, pl->comm->c, pl->cs_comm);
+  if (e == cudaSuccess && r == ncclSuccess) e = cudaStreamSynchronize(pl->cs_comm);
+  if (e == cudaSuccess && r == ncclSuccess) e = cudaMemcpy(all.data(), dev, all.size(), cudaMemcpyDeviceToHost);
+  cudaFree(dev);
+  if (r != ncclSuccess) return fail(NSLCT_E_NCCL, std::string("ncclAllGather(IPC handles): ") + api.GetErrorString(r));
+  if (e != cudaSuccess) return fail(NSLCT_E_CUDA, std::string("IPC handle exchange: ") + cudaGetErrorString(e));
+  for (int s = 0; s < P; ++s)
+    for (int b = 0; b < 2; ++b) {
+      if (s == pl->rank) {
+        pl->peer_recv[b][s] = pl->xrecv[b];
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, all.data() + ((size_t)s * 2 + b) * H, H);
+      CUDA_TRY(cudaIpcOpenMemHandle(&pl->peer_recv[b][s], h, cudaIpcMemLazyEnablePeerAccess));
+      pl->peer_opened[b][s] = true;
+    }
+  CUDA_TRY(cudaMalloc(&pl->xbar, sizeof(int)));
+  CUDA_TRY(cudaMemset(pl->xbar, 0, sizeof(int)));
+  return NSLCT_OK;
+}
+
 static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double abcd[16], int64_t batch,
                                   nslct_dtype dtype, const nslct_opts* opts, int nranks, int rank);
 
 nslct_status nslct_plan_ex(nslct_plan_t* plan, int64_t n, const double abcd[16], int64_t batch,
                            nslct_dtype dtype, const nslct_opts* opts) {
+  if (opts && opts->comm) {   // one transform, row slabs over the communicator's ranks
+    const nslct_comm_s* c = static_cast<const nslct_comm_s*>(opts->comm);
+    if (batch != 1) return fail(NSLCT_E_ARG, "a comm (row-slab) plan transforms one image: batch must be 1");
+    return plan_internal(plan, n, abcd, 1, dtype, opts, c->nranks, c->rank);
+  }
   return plan_internal(plan, n, abcd, batch, dtype, opts, 0, 0);
 }
 
@@ -603,7 +734,8 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
     return fail(NSLCT_E_ARG, "bad dx");
 
   const bool slab = nranks > 0;
-  int64_t L = n;
+  int64_t L = n, Lc = n;
+  int nc = 1;
   if (slab) {
     if (n % nranks) return fail(NSLCT_E_ARG, "nranks must divide n");
     L = n / nranks;
@@ -611,7 +743,19 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
     const int64_t TB = (n <= 2048) ? 256 : (n <= 8192 ? 512 : 1024);
     const int64_t G = (TB / TL < n) ? TB / TL : n;
     if (L % G) return fail(NSLCT_E_ARG, "slab height n/nranks must be a multiple of the lines per CTA");
+    // exchange chunks: sub-blocks of lc = L/nc producer lines (PassArgs::out_chunk); each
+    // chunk a whole number of CTA line groups (and of line pairs)
+    const int want = (o.exchange_chunks > 0) ? o.exchange_chunks : 2;
+    if (want != 1 && want != 2 && want != 4 && want != 8)
+      return fail(NSLCT_E_ARG, "exchange_chunks must be 0, 1, 2, 4 or 8");
+    nc = want;
+    while (nc > 1 && ((L / nc) % G || (L / nc) % 2)) nc /= 2;
+    Lc = L / nc;
   }
+  if (o.comm && !slab) return fail(NSLCT_E_ARG, "opts.comm: use nslct_plan_ex (not nslct_plan_slab)");
+  if (o.exchange != NSLCT_EXCHANGE_NCCL && o.exchange != NSLCT_EXCHANGE_PEER) return fail(NSLCT_E_ARG, "bad exchange");
+  if (o.comm && o.exchange == NSLCT_EXCHANGE_PEER && nranks > 8)
+    return fail(NSLCT_E_ARG, "the peer-store exchange supports at most 8 ranks");
   std::string err;
   nslct::Plan p;
   int st = nslct::make_plan(abcd, o.variant, o.dispatch, o.h_fixed, &p, &err);
@@ -652,7 +796,19 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
   pl->slab = slab;
   pl->nranks = slab ? nranks : 1;
   pl->rank = slab ? rank : 0;
+  pl->L = L;
+  pl->nc = nc;
+  pl->lc = Lc;
+  pl->comm = static_cast<nslct_comm_s*>(o.comm);
+  pl->exchange = o.exchange;
   if (o.device >= 0) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || o.device >= count) {
+      delete pl;
+      return fail(NSLCT_E_ARG, "opts.device " + std::to_string(o.device) + " is not a CUDA device ordinal (" +
+                                   std::to_string(count) + " devices)");
+    }
     pl->device = o.device;
   } else {
     cudaError_t e = cudaGetDevice(&pl->device);
@@ -661,9 +817,14 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       return fail(NSLCT_E_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
     }
   }
+  pl->host_chunk_kb = o.host_chunk_kb;
   nslct_status result = NSLCT_OK;
   do {
     DeviceGuard guard(pl->device);
+    if (guard.status != cudaSuccess) {
+      result = fail(NSLCT_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(guard.status));
+      break;
+    }
     const int ti = (dtype == NSLCT_C64) ? 0 : 1;
     const double dx = pl->dx;
     const double dw = 2.0 * M_PI / ((double)n * dx);  // frequency grid
@@ -725,6 +886,34 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
         result = fail(e == cudaErrorMemoryAllocation ? NSLCT_E_OOM : NSLCT_E_CUDA,
                       std::string("twiddles: ") + cudaGetErrorString(e));
         break;
+      }
+    }
+    if (pl->comm) {   // row slabs over a communicator: send + 2 receive buffers, NCCL stream
+      if (pl->comm->device != pl->device) {
+        result = fail(NSLCT_E_ARG, "opts.comm was initialised on another device than the plan's");
+        break;
+      }
+      const size_t sb = (size_t)L * (size_t)n * pl->elem;
+      cudaError_t e = (o.exchange == NSLCT_EXCHANGE_NCCL) ? cudaMalloc(&pl->xsend, sb) : cudaSuccess;
+      if (e == cudaSuccess) e = cudaMalloc(&pl->xrecv[0], sb);
+      if (e == cudaSuccess) e = cudaMalloc(&pl->xrecv[1], sb);
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pl->cs_comm, cudaStreamNonBlocking);
+      for (int i = 0; i <= nc && e == cudaSuccess; ++i) {
+        cudaEvent_t ev;
+        e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) pl->xev.push_back(ev);
+      }
+      if (e != cudaSuccess) {
+        result = fail(e == cudaErrorMemoryAllocation ? NSLCT_E_OOM : NSLCT_E_CUDA,
+                      std::string("slab exchange buffers: ") + cudaGetErrorString(e));
+        break;
+      }
+      if (o.exchange == NSLCT_EXCHANGE_PEER) {
+        nslct_status st = peer_setup(pl);
+        if (st != NSLCT_OK) {
+          result = st;
+          break;
+        }
       }
     }
     if (!slab) {
@@ -799,8 +988,10 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
     for (int k = 0; k < 5; ++k) {
       pl->args[k].lines_per_img = (int)L;
       pl->args[k].line_offset = slab ? (int)(rank * L) : 0;
-      pl->args[k].in_chunk = (slab && k > 0) ? (int)L : (int)n;
-      pl->args[k].in_chunk_stride = (slab && k > 0) ? L * L : n * n;
+      pl->args[k].in_chunk = (slab && k > 0) ? (int)Lc : (int)n;
+      pl->args[k].in_chunk_stride = (slab && k > 0) ? L * Lc : n * n;
+      pl->args[k].out_chunk = (int)Lc;
+      pl->args[k].line_base = 0;
       pl->args[k].n_lines = slab ? L : batch * n;
       pl->args[k].n_in = (k == 0 && n_in != n) ? (int)n_in : 0;
       pl->args[k].in_off = (k == 0 && n_in != n) ? (int)(n / 2 - n_in / 2) : 0;
@@ -820,6 +1011,7 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
         a.lines_per_img = (int)nl;
         a.in_chunk = (int)nl;
         a.in_chunk_stride = nl * nl;
+        a.out_chunk = (int)nl;
         a.n_lines = batch * nl;
         a.n_in = (k == 0) ? (int)n : 0;
         a.in_off = (k == 0) ? (int)(nl / 2 - n / 2) : 0;
@@ -844,38 +1036,27 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       int sms = 0;
       if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device) == cudaSuccess && sms > 0)
         pl->num_sms = sms;
-      const char* np = std::getenv("NSLCT_NO_PIPE");
       const bool plain = pow2 && n_in == n && p.kind != 3;   // neither Bluestein, padded nor Ding
-      pl->pipe = (plain && !slab && ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog && !(np && np[0] == '1'));
+      // opts.kernels = NSLCT_KERNELS_GENERIC: the one-CTA-per-line-group kernels everywhere
+      // (same operator; the reference for A/B checks of the specialised kernels)
+      const bool special = o.kernels == NSLCT_KERNELS_AUTO;
+      pl->pipe = (plain && special && !slab && ti == 0 && lg >= kPipeMinLog && lg <= kPipeMaxLog);
       // L2 prefetch one claim ahead in the persistent kernels: one grid of groups ahead
       // (the group this CTA most likely claims next).  Measured on the C4 bench (DESIGN.md
-      // §6.6): K1 1.51 -> 1.32 ms, K2-K5 +0.5-1% -- so by default on the first pass only.
-      // NSLCT_L2_AHEAD (groups ahead, 0 = off) and NSLCT_L2_PASSES (bit mask of passes)
-      // override for experiments.
-      if (pl->pipe) {
-        const char* la = std::getenv("NSLCT_L2_AHEAD");
-        const char* lp = std::getenv("NSLCT_L2_PASSES");
-        const int ahead = la ? std::atoi(la) : pl->num_sms;
-        const int mask = lp ? std::atoi(lp) : 1;
-        for (int k = 0; k < 5; ++k) pl->args[k].l2_ahead = ((mask >> k) & 1) ? ahead : 0;
-      }
+      // §6.6): K1 1.51 -> 1.32 ms, K2-K5 +0.5-1% -- so on the first pass only.
+      if (pl->pipe) pl->args[0].l2_ahead = pl->num_sms;
       // complex64 chirps by anchored rotation recurrences (kernels.cuh struct Phase) on
       // every pass: measured K5 1.71 -> 1.66 ms, K2-K4 -1.4..-2% on the C4 bench (DESIGN.md
-      // §6.3); the bit mask of passes NSLCT_CHIRP_REC overrides.
+      // §6.3)
       if (ti == 0) {
-        const char* cr = std::getenv("NSLCT_CHIRP_REC");
-        int mask = 31;
-        if (cr) mask = std::atoi(cr);
         const int tl = (1 << lg) / 16;
-        for (int k = 0; k < 5; ++k)
-          if ((mask >> k) & 1) {
-            set_rec(&pl->args[k].ph, tl);
-            set_rec(&pl->args[k].ph_b, tl);
-            set_rec(&pl->args[k].ph_c, tl);
-          }
+        for (int k = 0; k < 5; ++k) {
+          set_rec(&pl->args[k].ph, tl);
+          set_rec(&pl->args[k].ph_b, tl);
+          set_rec(&pl->args[k].ph_c, tl);
+        }
       }
-      const char* npair = std::getenv("NSLCT_NO_PAIR");
-      pl->pair = plain && ti == 0 && (lg == 13 || lg == 14) && (L % 2 == 0) && !(npair && npair[0] == '1');
+      pl->pair = plain && special && ti == 0 && (lg == 13 || lg == 14) && (L % 2 == 0);
       for (int k = 0; k < 5 && pl->pair; ++k) pl->args[k].persist_ctas = (pl->num_sms / 2) * 2;
       for (int m = 0; m < kModes && pl->pair; ++m) {
         cudaError_t e = table().atpair[slab ? 1 : 0][lg][m]();
@@ -885,12 +1066,9 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
         }
       }
       if (result != NSLCT_OK) break;
-      const char* f64 = std::getenv("NSLCT_FFT64");
-      pl->fft64 = pl->pipe && lg == 12 && f64 && f64[0] == '1';
       // warp-specialised kernels for the passes after the first (measured K2-K5 -0.6..-1.6%,
       // K1 +2.4% -- so not for mode 0)
-      const char* wse = std::getenv("NSLCT_WS");
-      pl->ws = pl->pipe && !pl->fft64 && !(wse && wse[0] == '0');
+      pl->ws = pl->pipe;
       if (pl->ws) {
         const WsRow* row = ws_row_of(lg);
         cudaError_t e = row ? cudaSuccess : cudaErrorInvalidValue;
@@ -923,7 +1101,8 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       }
     }
     for (int m = 0; m < kModes && pl->pipe; ++m) {
-      cudaError_t e = pl->fft64 ? table().atp64[m]() : table().atp[lg][m]();
+      if (!table().atp[lg][m]) continue;   // modes 1-3 run the warp-specialised kernel
+      cudaError_t e = table().atp[lg][m]();
       if (e != cudaSuccess) {
         result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(pipe): ") + cudaGetErrorString(e));
         break;
@@ -963,10 +1142,8 @@ static nslct_status launch_pipe_pass(nslct_plan_t pl, int k, const PassArgs& a, 
     nslct_status st = make_store_map(&map, a.out, pl->log2n, a.n_lines >> pl->log2n);
     if (st != NSLCT_OK) return st;
   }
-  if (pl->ws && m >= 1 && m <= 3) {
+  if (m >= 1 && m <= 3)
     CUDA_TRY(ws_row_of(pl->log2n)->launch[m - 1](a, s, pl->num_sms, pl->counters + k, map));
-  } else if (pl->fft64)
-    CUDA_TRY(table().lp64[m](a, s, pl->num_sms, pl->counters + k, map));
   else
     CUDA_TRY(table().lp[pl->log2n][m](a, s, pl->num_sms, pl->counters + k, map));
   return NSLCT_OK;
@@ -1111,14 +1288,109 @@ static nslct_status run_images(nslct_plan_t pl, const void* in, void* out, int64
   return NSLCT_OK;
 }
 
+// One launch of pass k of a slab plan (the cluster-pair kernels at N = 8192 / 16384 c64,
+// else the generic line pass), over local lines a.line_base + [0, a.n_lines).
+static nslct_status launch_slab_pass(nslct_plan_t pl, int k, const PassArgs& a, cudaStream_t s) {
+  const int ti = (pl->dtype == NSLCT_C64) ? 0 : 1;
+  if (pl->pair)
+    CUDA_TRY(table().lpair[1][pl->log2n][pl->mode[k]](a, s));
+  else
+    CUDA_TRY(table().l[ti][pl->log2n][pl->mode[k]](a, s));
+  return NSLCT_OK;
+}
+
+// The whole row-slab transform of a comm plan on stream s (include/nslct.h nslct_exec):
+// pass k in nc chunks of lc lines into the send buffer; after chunk c, the NCCL stream
+// moves sub-block (q, c) to every rank q (grouped send/recv, NCCL 2.28 over NVLink /
+// NVSwitch) while chunk c+1 computes; pass k+1 waits for the whole exchange and reads the
+// receive buffer, which alternates between passes (the exchange of pass k+1 writes the
+// other one while pass k+1 still reads this one).
+static nslct_status run_slab_comm(nslct_plan_t pl, const void* in, void* out, cudaStream_t s, bool profile) {
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return fail(NSLCT_E_NCCL, api.err);
+  cudaEvent_t* ev = nullptr;
+  if (profile) {
+    if (pl->ev_used == pl->ev.size()) {
+      nslct_plan_s::EvSet set{};
+      for (auto& e : set.e) CUDA_TRY(cudaEventCreate(&e));
+      pl->ev.push_back(set);
+    }
+    ev = pl->ev[pl->ev_used].e;
+  }
+  const size_t blk = (size_t)pl->L * (size_t)pl->L * pl->elem;   // bytes of one L x L block
+  const size_t sub = (size_t)pl->L * (size_t)pl->lc * pl->elem;  // bytes of one sub-block
+  unsigned char* send = static_cast<unsigned char*>(pl->xsend);
+  const int np = pl->n_passes;
+  const void* src = in;
+  for (int k = 0; k < np; ++k) {
+    if (ev) CUDA_TRY(cudaEventRecord(ev[k], s));
+    PassArgs a = pl->args[k];
+    a.in = src;
+    if (k == np - 1) {   // straight output, rows of this rank's slab
+      a.out = out;
+      nslct_status st = launch_slab_pass(pl, k, a, s);
+      if (st != NSLCT_OK) return st;
+      break;
+    }
+    unsigned char* recv = static_cast<unsigned char*>(pl->xrecv[k & 1]);
+    if (pl->exchange == NSLCT_EXCHANGE_PEER) {
+      // the store IS the exchange: row-block q of this pass's output lands in rank q's
+      // receive buffer k&1 at block offset rank L^2 (kernels.cuh peer_on); then a
+      // stream-ordered barrier over all ranks (a 4-byte NCCL all-reduce): every rank's pass
+      // k stores are complete before any rank's pass k+1 reads them, and every rank has
+      // finished reading buffer (k+1)&1 (its pass k input) before pass k+1 overwrites it.
+      a.out = pl->peer_recv[k & 1][pl->rank];
+      a.peer_on = 1;
+      a.peer_rank = pl->rank;
+      for (int q = 0; q < pl->nranks; ++q) a.peer_out[q] = pl->peer_recv[k & 1][q];
+      nslct_status st = launch_slab_pass(pl, k, a, s);
+      if (st != NSLCT_OK) return st;
+      const ncclResult_t r = api.AllReduce(pl->xbar, pl->xbar, 1, ncclInt32, ncclSum, pl->comm->c, s);
+      if (r != ncclSuccess) return fail(NSLCT_E_NCCL, std::string("barrier (ncclAllReduce): ") + api.GetErrorString(r));
+      src = recv;
+      continue;
+    }
+    a.out = send;
+    for (int c = 0; c < pl->nc; ++c) {
+      PassArgs ac = a;
+      ac.line_base = (int)(c * pl->lc);
+      ac.n_lines = pl->lc;
+      nslct_status st = launch_slab_pass(pl, k, ac, s);
+      if (st != NSLCT_OK) return st;
+      CUDA_TRY(cudaEventRecord(pl->xev[c], s));
+      CUDA_TRY(cudaStreamWaitEvent(pl->cs_comm, pl->xev[c], 0));
+      ncclResult_t r = api.GroupStart();
+      for (int q = 0; q < pl->nranks && r == ncclSuccess; ++q) {
+        const size_t off = (size_t)q * blk + (size_t)c * sub;
+        r = api.Send(send + off, sub, ncclInt8, q, pl->comm->c, pl->cs_comm);
+        if (r == ncclSuccess) r = api.Recv(recv + off, sub, ncclInt8, q, pl->comm->c, pl->cs_comm);
+      }
+      const ncclResult_t r2 = api.GroupEnd();   // always close the group
+      if (r != ncclSuccess || r2 != ncclSuccess)
+        return fail(NSLCT_E_NCCL, std::string("slab all-to-all (grouped ncclSend/ncclRecv): ") +
+                                      api.GetErrorString(r != ncclSuccess ? r : r2));
+    }
+    CUDA_TRY(cudaEventRecord(pl->xev[pl->nc], pl->cs_comm));
+    CUDA_TRY(cudaStreamWaitEvent(s, pl->xev[pl->nc], 0));
+    src = recv;
+  }
+  if (ev) {
+    CUDA_TRY(cudaEventRecord(ev[np], s));
+    ++pl->ev_used;
+  }
+  return NSLCT_OK;
+}
+
 nslct_status nslct_exec(nslct_plan_t pl, const void* in, void* out, void* stream) {
   if (!pl) return fail(NSLCT_E_ARG, "null plan");
   if (!in || !out) return fail(NSLCT_E_ARG, "null in/out pointer");
   if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(NSLCT_E_ARG, "in/out must be 16-byte aligned");
-  if (pl->slab) return fail(NSLCT_E_ARG, "slab plans run pass by pass: nslct_exec_pass");
+  if (pl->slab && !pl->comm)
+    return fail(NSLCT_E_ARG, "nslct_plan_slab plans run pass by pass (nslct_exec_pass); comm plans run here");
   if (pl->n_in != pl->n && in == out) return fail(NSLCT_E_ARG, "a padded plan cannot run in place");
-  DeviceGuard guard(pl->device);
+  GUARD_DEVICE(pl);
+  if (pl->comm) return run_slab_comm(pl, in, out, reinterpret_cast<cudaStream_t>(stream), pl->profile != 0);
   return run_images(pl, in, out, 0, pl->batch, reinterpret_cast<cudaStream_t>(stream),
                     pl->profile != 0);
 }
@@ -1132,7 +1404,7 @@ nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* ou
   if (pl->p.kind == 3) return fail(NSLCT_E_ARG, "Ding plans run through nslct_exec");
   if (pass < 0 || pass >= pl->n_passes) return fail(NSLCT_E_ARG, "pass out of range");
   if (pass < pl->n_passes - 1 && in == out) return fail(NSLCT_E_ARG, "transposing passes cannot run in place");
-  DeviceGuard guard(pl->device);
+  GUARD_DEVICE(pl);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int ti = (pl->dtype == NSLCT_C64) ? 0 : 1;
   PassArgs a = pl->args[pass];
@@ -1153,17 +1425,69 @@ nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* ou
   return NSLCT_OK;
 }
 
-// Images per exec_host chunk: about 64 MiB per copy (NSLCT_HOST_CHUNK_MB overrides), so
+// ---- communicator -------------------------------------------------------------------
+nslct_status nslct_comm_unique_id(uint8_t unique_id[128]) {
+  if (!unique_id) return fail(NSLCT_E_ARG, "null pointer");
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return fail(NSLCT_E_NCCL, api.err);
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+  ncclUniqueId id;
+  NCCL_TRY(api.GetUniqueId(&id));
+  std::memcpy(unique_id, &id, 128);
+  return NSLCT_OK;
+}
+
+nslct_status nslct_comm_init(nslct_comm_t* comm, const uint8_t unique_id[128], int rank, int nranks) {
+  if (!comm || !unique_id) return fail(NSLCT_E_ARG, "null pointer");
+  *comm = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(NSLCT_E_ARG, "bad rank / nranks");
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return fail(NSLCT_E_NCCL, api.err);
+  nslct_comm_s* c = new (std::nothrow) nslct_comm_s();
+  if (!c) return fail(NSLCT_E_OOM, "host allocation failed");
+  cudaError_t e = cudaGetDevice(&c->device);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(NSLCT_E_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, 128);
+  const ncclResult_t r = api.CommInitRank(&c->c, nranks, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(NSLCT_E_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+  }
+  c->rank = rank;
+  c->nranks = nranks;
+  *comm = c;
+  return NSLCT_OK;
+}
+
+nslct_status nslct_comm_info(nslct_comm_t comm, int* rank, int* nranks) {
+  if (!comm) return fail(NSLCT_E_ARG, "null communicator");
+  if (rank) *rank = comm->rank;
+  if (nranks) *nranks = comm->nranks;
+  return NSLCT_OK;
+}
+
+nslct_status nslct_comm_destroy(nslct_comm_t comm) {
+  if (!comm) return NSLCT_OK;
+  const NcclApi& api = nccl_api();
+  ncclResult_t r = ncclSuccess;
+  if (api.ok && comm->c) r = api.CommDestroy(comm->c);
+  delete comm;
+  if (r != ncclSuccess) return fail(NSLCT_E_NCCL, std::string("ncclCommDestroy: ") + api.GetErrorString(r));
+  return NSLCT_OK;
+}
+
+// Images per exec_host chunk: about 64 MiB per copy (opts.host_chunk_kb overrides), so
 // the H2D of chunk i+1, the passes of chunk i and the D2H of chunk i-1 overlap.
 static int64_t host_chunk_images(const nslct_plan_s* pl) {
   const double img = (double)pl->n * (double)pl->n * (double)pl->elem;
   // at most 64 MiB per chunk, and at least ~8 chunks when the batch allows it, so small
   // batches still overlap their copies with the passes
   double mb = std::min(64.0, img * (double)pl->batch / 8.0 / 1048576.0);
-  if (const char* e = std::getenv("NSLCT_HOST_CHUNK_MB")) {
-    const double v = std::atof(e);
-    if (v > 0) mb = v;
-  }
+  if (pl->host_chunk_kb > 0) mb = (double)pl->host_chunk_kb / 1024.0;
   int64_t c = (int64_t)(mb * 1048576.0 / img);
   if (c < 1) c = 1;
   if (c > pl->batch) c = pl->batch;
@@ -1182,7 +1506,7 @@ nslct_status nslct_exec_pass_peer(nslct_plan_t pl, int pass, const void* in, voi
     if (!peer_out[s] || (reinterpret_cast<uintptr_t>(peer_out[s]) & 15))
       return fail(NSLCT_E_ARG, "peer buffers must be non-null and 16-byte aligned");
   if (reinterpret_cast<uintptr_t>(in) & 15) return fail(NSLCT_E_ARG, "in must be 16-byte aligned");
-  DeviceGuard guard(pl->device);
+  GUARD_DEVICE(pl);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int ti = (pl->dtype == NSLCT_C64) ? 0 : 1;
   PassArgs a = pl->args[pass];
@@ -1202,7 +1526,14 @@ nslct_status nslct_exec_host(nslct_plan_t pl, const void* host_in, void* host_ou
   if (!pl) return fail(NSLCT_E_ARG, "null plan");
   if (pl->slab) return fail(NSLCT_E_ARG, "slab plans run pass by pass: nslct_exec_pass");
   if (!host_in || !host_out) return fail(NSLCT_E_ARG, "null host pointer");
-  DeviceGuard guard(pl->device);
+  if (pl->n_in != pl->n) {
+    // output chunks are larger than input chunks: chunk i's device->host copy could
+    // overwrite input bytes of a later chunk not yet uploaded
+    const uintptr_t i0 = reinterpret_cast<uintptr_t>(host_in), o0 = reinterpret_cast<uintptr_t>(host_out);
+    const uintptr_t i1 = i0 + pl->in_img_bytes * (size_t)pl->batch, o1 = o0 + pl->bytes;
+    if (i0 < o1 && o0 < i1) return fail(NSLCT_E_ARG, "a zero-padding plan needs disjoint host_in / host_out");
+  }
+  GUARD_DEVICE(pl);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (!pl->h_in) CUDA_TRY(cudaMalloc(&pl->h_in, pl->in_img_bytes * (size_t)pl->batch));
   if (!pl->h_out) CUDA_TRY(cudaMalloc(&pl->h_out, pl->bytes));
@@ -1300,7 +1631,7 @@ nslct_status nslct_plan_describe(int64_t n, const double abcd[16], const nslct_o
 nslct_status nslct_pass_ms(nslct_plan_t pl, float* ms, int capacity, int* n_written) {
   if (!pl || !ms) return fail(NSLCT_E_ARG, "null pointer");
   if (!pl->profile || pl->ev_used == 0) return fail(NSLCT_E_ARG, "plan not profiled / no exec yet");
-  DeviceGuard guard(pl->device);
+  GUARD_DEVICE(pl);
   const int np = (pl->p.kind == 0 || pl->image) ? 1 : pl->n_passes;
   if (capacity < np) return fail(NSLCT_E_ARG, "capacity too small");
   for (int k = 0; k < np; ++k) ms[k] = 0.0f;
@@ -1316,6 +1647,23 @@ nslct_status nslct_pass_ms(nslct_plan_t pl, float* ms, int capacity, int* n_writ
   for (int k = 0; k < np; ++k) ms[k] /= (float)pl->ev_used;
   pl->ev_used = 0;
   if (n_written) *n_written = np;
+  return NSLCT_OK;
+}
+
+nslct_status nslct_inverse_matrix(const double abcd[16], double out[16]) {
+  if (!abcd || !out) return fail(NSLCT_E_ARG, "null pointer");
+  // Eq. CCCMCCCM20: (A, B; C, D)^-1 = (D^T, -B^T; -C^T, A^T); row-major
+  // 4x4, block (r, c) of M at rows 2r.., columns 2c..
+  double m[16];
+  std::memcpy(m, abcd, sizeof(m));
+  auto at = [&](int br, int bc, int i, int k) { return m[(2 * br + i) * 4 + 2 * bc + k]; };
+  for (int i = 0; i < 2; ++i)
+    for (int k = 0; k < 2; ++k) {
+      out[i * 4 + k] = at(1, 1, k, i);                  // D^T
+      out[i * 4 + 2 + k] = -at(0, 1, k, i);             // -B^T
+      out[(2 + i) * 4 + k] = -at(1, 0, k, i);           // -C^T
+      out[(2 + i) * 4 + 2 + k] = at(0, 0, k, i);        // A^T
+    }
   return NSLCT_OK;
 }
 

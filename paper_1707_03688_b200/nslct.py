@@ -25,7 +25,11 @@ KINDS = {0: "B0", 1: "I", 2: "II", 3: "DING"}
 EXPORTS = ("nslct_opts_default", "nslct_plan", "nslct_plan_ex", "nslct_exec", "nslct_exec_host",
            "nslct_plan_info", "nslct_plan_describe", "nslct_pass_ms", "nslct_destroy",
            "nslct_last_error", "nslct_abi_version", "nslct_plan_slab", "nslct_exec_pass",
-           "nslct_exec_pass_peer")
+           "nslct_exec_pass_peer", "nslct_inverse_matrix", "nslct_comm_unique_id", "nslct_comm_init",
+           "nslct_comm_info", "nslct_comm_destroy")
+ABI_VERSION = 4
+KERNELS = {"auto": 0, "generic": 1}
+EXCHANGES = {"nccl": 0, "peer": 1}
 
 
 class NslctError(RuntimeError):
@@ -38,7 +42,9 @@ class NslctError(RuntimeError):
 class nslct_opts(ctypes.Structure):
     _fields_ = [("dx", ctypes.c_double), ("variant", ctypes.c_int), ("dispatch", ctypes.c_int),
                 ("h_fixed", ctypes.c_double * 3), ("device", ctypes.c_int), ("profile", ctypes.c_int),
-                ("schedule", ctypes.c_int), ("n_in", ctypes.c_int), ("reserved", ctypes.c_int * 4)]
+                ("schedule", ctypes.c_int), ("n_in", ctypes.c_int), ("kernels", ctypes.c_int),
+                ("host_chunk_kb", ctypes.c_int), ("comm", ctypes.c_void_p), ("exchange_chunks", ctypes.c_int),
+                ("exchange", ctypes.c_int), ("reserved", ctypes.c_int * 4)]
 
 
 class nslct_plan_desc(ctypes.Structure):
@@ -77,12 +83,21 @@ def lib():
         L.nslct_plan_describe.argtypes = [i64, dp, ctypes.POINTER(nslct_opts), ctypes.POINTER(nslct_plan_desc)]
         L.nslct_pass_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         L.nslct_destroy.argtypes = [vp]
+        L.nslct_inverse_matrix.argtypes = [dp, dp]
+        L.nslct_comm_unique_id.argtypes = [ctypes.c_char_p]
+        L.nslct_comm_init.argtypes = [ctypes.POINTER(vp), ctypes.c_char_p, ctypes.c_int, ctypes.c_int]
+        L.nslct_comm_info.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+        L.nslct_comm_destroy.argtypes = [vp]
         L.nslct_last_error.restype = ctypes.c_char_p
         L.nslct_abi_version.restype = ctypes.c_int
         for f in ("nslct_plan", "nslct_plan_ex", "nslct_exec", "nslct_exec_host", "nslct_plan_info",
                   "nslct_plan_describe", "nslct_pass_ms", "nslct_destroy", "nslct_plan_slab",
-                  "nslct_exec_pass", "nslct_exec_pass_peer"):
+                  "nslct_exec_pass", "nslct_exec_pass_peer", "nslct_inverse_matrix", "nslct_comm_unique_id",
+                  "nslct_comm_init", "nslct_comm_info", "nslct_comm_destroy"):
             getattr(L, f).restype = ctypes.c_int
+        if L.nslct_abi_version() != ABI_VERSION:
+            raise ImportError("libnslct.so ABI %d, binding expects %d: rebuild (python -m paper_1707_03688_b200.build)"
+                              % (L.nslct_abi_version(), ABI_VERSION))
         _LIB = L
     return _LIB
 
@@ -101,7 +116,8 @@ SCHEDULES = {"auto": 0, "line_passes": 1, "on_chip": 2}
 
 
 def make_opts(dx=None, variant="HA", dispatch="reversible", h_fixed=None, device=None, profile=False,
-              schedule="auto", n_in=None):
+              schedule="auto", n_in=None, kernels="auto", host_chunk_kb=0, comm=None, exchange_chunks=0,
+              exchange="nccl"):
     o = nslct_opts()
     lib().nslct_opts_default(ctypes.byref(o))
     o.dx = float(dx) if dx else 0.0
@@ -115,6 +131,11 @@ def make_opts(dx=None, variant="HA", dispatch="reversible", h_fixed=None, device
     o.profile = 1 if profile else 0
     o.schedule = SCHEDULES[schedule]
     o.n_in = 0 if n_in is None else int(n_in)
+    o.kernels = KERNELS[kernels]
+    o.host_chunk_kb = int(host_chunk_kb)
+    o.comm = None if comm is None else comm.handle
+    o.exchange_chunks = int(exchange_chunks)
+    o.exchange = EXCHANGES[exchange]
     return o
 
 
@@ -138,22 +159,48 @@ def nslct_plan_describe(n, M, **kw):
     return _desc_dict(d)
 
 
+def _want_dtype(dtype):
+    import torch
+    return torch.complex64 if dtype == "c64" else torch.complex128
+
+
 class Plan:
     """RAII wrapper of nslct_plan_t.  exec() takes torch CUDA tensors (complex64/128).
-    n_in (< n): fused zero-padding -- inputs are [batch, n_in, n_in], outputs [batch, n, n]."""
+    n_in (< n): fused zero-padding -- inputs are [batch, n_in, n_in], outputs [batch, n, n].
+    comm (a Communicator): ONE n x n transform row-slab sharded over the communicator's
+    ranks -- batch must be 1 and exec() takes this rank's slab [n/nranks, n]; the library
+    runs every pass and every exchange itself (exchange="nccl": chunked NCCL all-to-all
+    overlapping the passes; "peer": stores straight into the peers' buffers over NVLink).
+    Creating a comm plan is collective over the communicator."""
 
     def __init__(self, n, M, batch, dtype="c64", dx=None, variant="HA", dispatch="reversible",
-                 h_fixed=None, device=None, profile=False, schedule="auto", n_in=None):
+                 h_fixed=None, device=None, profile=False, schedule="auto", n_in=None, kernels="auto",
+                 host_chunk_kb=0, comm=None, exchange_chunks=0, exchange="nccl"):
         self.n, self.batch = int(n), int(batch)
         self.n_in = self.n if n_in is None else int(n_in)
         self.dtype = dtype
+        self.comm = comm
+        if device is None:
+            try:
+                import torch
+                device = torch.cuda.current_device() if torch.cuda.is_available() else None
+            except ImportError:
+                device = None
+        self.device = device
         a, ap = _abcd(M)
-        o = make_opts(dx, variant, dispatch, h_fixed, device, profile, schedule, n_in)
+        o = make_opts(dx, variant, dispatch, h_fixed, device, profile, schedule, n_in, kernels, host_chunk_kb,
+                      comm, exchange_chunks, exchange)
         h = ctypes.c_void_p()
         _check(lib().nslct_plan_ex(ctypes.byref(h), self.n, ap, self.batch,
                                    C64 if dtype == "c64" else C128, ctypes.byref(o)))
         self._h = h
         self.profile = profile
+        if comm is not None:
+            self.rows = self.n // comm.nranks
+            self.in_shape = self.out_shape = (self.rows, self.n)
+        else:
+            self.in_shape = (self.batch, self.n_in, self.n_in)
+            self.out_shape = (self.batch, self.n, self.n)
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -181,30 +228,56 @@ class Plan:
         _check(lib().nslct_exec(self._h, ctypes.c_void_p(in_ptr), ctypes.c_void_p(out_ptr),
                                 ctypes.c_void_p(stream_ptr)))
 
+    def _check_dev(self, t, name, shape):
+        want = _want_dtype(self.dtype)
+        if not (t.is_cuda and t.dtype == want and t.is_contiguous() and tuple(t.shape) == tuple(shape)):
+            raise ValueError("%s must be a contiguous CUDA %s tensor of shape %s (got %s %s %s)"
+                             % (name, want, tuple(shape), t.device, t.dtype, tuple(t.shape)))
+        if self.device is not None and t.device.index != self.device:
+            raise ValueError("%s is on %s, the plan on cuda:%d" % (name, t.device, self.device))
+
     def exec(self, x, out=None, stream=None):
-        """x: torch CUDA tensor [batch, n_in, n_in] of complex64 (c64) / complex128 (c128)."""
+        """x: torch CUDA tensor of the plan's input shape ([batch, n_in, n_in], or the
+        slab [n/nranks, n] of a comm plan), complex64 (c64) / complex128 (c128).  out:
+        optional tensor of the output shape (may be x unless the plan zero-pads)."""
         import torch
-        want = torch.complex64 if self.dtype == "c64" else torch.complex128
-        ni = self.n_in
-        if not (x.is_cuda and x.dtype == want and x.is_contiguous()
-                and tuple(x.shape[-2:]) == (ni, ni) and x.numel() == self.batch * ni * ni):
-            raise ValueError("exec expects a contiguous CUDA %s tensor of %d x %d x %d"
-                             % (want, self.batch, ni, ni))
+        if x.dim() == 2 and self.comm is None and self.batch == 1:
+            x = x.unsqueeze(0)
+        self._check_dev(x, "x", self.in_shape)
         if out is None:
-            out = torch.empty((self.batch, self.n, self.n), dtype=want, device=x.device)
+            out = torch.empty(self.out_shape, dtype=x.dtype, device=x.device)
+        else:
+            self._check_dev(out, "out", self.out_shape)
         s = stream if stream is not None else torch.cuda.current_stream(x.device)
         self.exec_ptr(x.data_ptr(), out.data_ptr(), s.cuda_stream)
         return out
 
     def exec_host(self, host_in, host_out, stream=None):
-        """host_in/host_out: CPU torch tensors or numpy arrays (pinned for full speed)."""
-        def ptr(t):
-            return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+        """host_in/host_out: CPU torch tensors or numpy arrays (pinned for full speed) of the
+        plan's input/output shapes and dtype, C-contiguous."""
+        want = np.complex64 if self.dtype == "c64" else np.complex128
+
+        def ptr(t, name, shape):
+            if hasattr(t, "data_ptr"):
+                import torch
+                ok = (not t.is_cuda and t.dtype == _want_dtype(self.dtype) and t.is_contiguous()
+                      and tuple(t.shape) == tuple(shape))
+                p = t.data_ptr()
+            else:
+                ok = (isinstance(t, np.ndarray) and t.dtype == want and t.flags.c_contiguous
+                      and tuple(t.shape) == tuple(shape))
+                p = t.ctypes.data if ok else 0
+            if not ok:
+                raise ValueError("%s must be a C-contiguous host %s array of shape %s" % (name, want.__name__, tuple(shape)))
+            return p
+        if self.comm is not None:
+            raise ValueError("exec_host: not for comm (slab) plans")
+        pi = ptr(host_in, "host_in", self.in_shape)
+        po = ptr(host_out, "host_out", self.out_shape)
         sp = 0
         if stream is not None:
             sp = stream.cuda_stream
-        _check(lib().nslct_exec_host(self._h, ctypes.c_void_p(ptr(host_in)),
-                                     ctypes.c_void_p(ptr(host_out)), ctypes.c_void_p(sp)))
+        _check(lib().nslct_exec_host(self._h, ctypes.c_void_p(pi), ctypes.c_void_p(po), ctypes.c_void_p(sp)))
         return host_out
 
     def pass_ms(self):
@@ -214,29 +287,81 @@ class Plan:
         return [buf[i] for i in range(nw.value)]
 
 
-class SlabPlan(Plan):
-    """One n x n transform sharded as row slabs over nranks (nslct_plan_slab).
+class Communicator:
+    """nslct_comm_t: the library's own NCCL communicator (one process per GPU).
+    Communicator(group): over a torch.distributed process group -- rank 0's NCCL unique id
+    is broadcast through the group, then every rank initialises on its current CUDA device.
+    Communicator.local(): a one-rank communicator (no process group needed)."""
 
-    run(x_slab, exchange) executes the passes of this rank's slab of L = n/nranks rows;
-    exchange(send, recv) must perform the all-to-all of nranks blocks of L*L elements
-    between passes (torch_all_to_all() for NCCL/gloo process groups)."""
+    def __init__(self, group=None, _uid=None, _rank=None, _nranks=None):
+        if _uid is None:
+            import torch.distributed as dist
+            uid = ctypes.create_string_buffer(128)
+            if dist.get_rank(group) == 0:
+                _check(lib().nslct_comm_unique_id(uid))
+            obj = [bytes(uid.raw)]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(obj, src=src, group=group)
+            _uid, _rank, _nranks = obj[0], dist.get_rank(group), dist.get_world_size(group)
+        h = ctypes.c_void_p()
+        _check(lib().nslct_comm_init(ctypes.byref(h), _uid, int(_rank), int(_nranks)))
+        self.handle = h
+        r, nr = ctypes.c_int(), ctypes.c_int()
+        _check(lib().nslct_comm_info(h, ctypes.byref(r), ctypes.byref(nr)))
+        self.rank, self.nranks = r.value, nr.value
+
+    @classmethod
+    def local(cls):
+        uid = ctypes.create_string_buffer(128)
+        _check(lib().nslct_comm_unique_id(uid))
+        return cls(_uid=bytes(uid.raw), _rank=0, _nranks=1)
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            lib().nslct_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class SlabPlan(Plan):
+    """One pass at a time of a row-slab transform (nslct_plan_slab / nslct_exec_pass /
+    nslct_exec_pass_peer): the entry points a caller uses to run the slab passes with its
+    own exchange -- e.g. the single-GPU multi-rank emulation in the tests.  The product
+    path for multi-GPU is Plan(..., comm=Communicator(...)), which runs every pass and
+    exchange inside the library."""
 
     def __init__(self, n, M, nranks, rank, dtype="c64", dx=None, variant="HA", dispatch="reversible",
-                 h_fixed=None, device=None):
+                 h_fixed=None, device=None, kernels="auto", exchange_chunks=0):
         self.n, self.batch, self.dtype = int(n), 1, dtype
         self.nranks, self.rank = int(nranks), int(rank)
         self.L = self.n // self.nranks
+        self.comm = None
+        self.device = device
         a, ap = _abcd(M)
-        o = make_opts(dx, variant, dispatch, h_fixed, device, False)
+        o = make_opts(dx, variant, dispatch, h_fixed, device, False, kernels=kernels, exchange_chunks=exchange_chunks)
         h = ctypes.c_void_p()
         _check(lib().nslct_plan_slab(ctypes.byref(h), self.n, ap, self.nranks, self.rank,
                                      C64 if dtype == "c64" else C128, ctypes.byref(o)))
         self._h = h
         self.profile = False
+        self.in_shape = self.out_shape = (self.L, self.n)
         self.n_passes = self.info()["n_passes"]
 
     def exec_pass(self, k, x, out, stream=None):
         import torch
+        self._check_dev(x, "x", self.in_shape)
+        self._check_dev(out, "out", self.out_shape)
         s = stream if stream is not None else torch.cuda.current_stream(x.device)
         _check(lib().nslct_exec_pass(self._h, int(k), ctypes.c_void_p(x.data_ptr()),
                                      ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(s.cuda_stream)))
@@ -246,127 +371,11 @@ class SlabPlan(Plan):
         """Transposing pass k with the exchange fused into its store: row-block s goes to
         peer_ptrs[s] (device pointers, one per rank) at block offset rank*L*L."""
         import torch
+        self._check_dev(x, "x", self.in_shape)
         s = stream if stream is not None else torch.cuda.current_stream(x.device)
         arr = (ctypes.c_void_p * len(peer_ptrs))(*[int(p) for p in peer_ptrs])
         _check(lib().nslct_exec_pass_peer(self._h, int(k), ctypes.c_void_p(x.data_ptr()), arr,
                                           len(peer_ptrs), ctypes.c_void_p(s.cuda_stream)))
-
-    def run_peer(self, x_slab, recv, peer_ptrs, barrier, out=None, stream=None):
-        """The slab transform with every all-to-all fused into the producing pass's store
-        (nslct_exec_pass_peer).  recv: this rank's two receive buffers [L, n] (double
-        buffering across passes); peer_ptrs[b][s]: rank s's receive buffer b; barrier():
-        a stream-ordered cross-rank barrier run after each transposing pass."""
-        import torch
-        out = torch.empty_like(x_slab) if out is None else out
-        cur = x_slab
-        for k in range(self.n_passes - 1):
-            self.exec_pass_peer(k, cur, peer_ptrs[k % 2], stream)
-            barrier()
-            cur = recv[k % 2]
-        self.exec_pass(self.n_passes - 1, cur, out, stream)
-        return out
-
-    def run(self, x_slab, exchange, out=None, stream=None):
-        """x_slab: contiguous CUDA tensor [L, n] (this rank's rows).  Returns [L, n]."""
-        import torch
-        want = torch.complex64 if self.dtype == "c64" else torch.complex128
-        if not (x_slab.is_cuda and x_slab.dtype == want and x_slab.is_contiguous()
-                and tuple(x_slab.shape) == (self.L, self.n)):
-            raise ValueError("run expects a contiguous CUDA %s tensor of %d x %d" % (want, self.L, self.n))
-        send = torch.empty_like(x_slab)    # pass outputs: nranks row-blocks of [L][L]
-        recv = torch.empty_like(x_slab)    # all-to-all results: the next pass's input
-        out = torch.empty_like(x_slab) if out is None else out
-        cur = x_slab
-        for k in range(self.n_passes):
-            if k == self.n_passes - 1:
-                self.exec_pass(k, cur, out, stream)
-            else:
-                self.exec_pass(k, cur, send, stream)
-                exchange(send, recv)   # stream-ordered after pass k; recv was last read by pass k
-                cur = recv
-        return out
-
-
-def torch_all_to_all(group=None):
-    """exchange(send, recv) for SlabPlan.run over a torch.distributed process group
-    (NCCL on GPUs): nranks equal blocks of L*L elements."""
-    import torch.distributed as dist
-
-    def exchange(send, recv):
-        dist.all_to_all_single(recv.view(-1), send.view(-1), group=group)
-    return exchange
-
-
-def symm_mem_exchange(L, n, dtype="c64", group=None):
-    """Receive buffers for SlabPlan.run_peer in torch symmetric memory (CUDA peer memory
-    over NVLink on a multi-GPU node): returns (recv, peer_ptrs, barrier).  Multi-GPU only;
-    not exercised by this round's single-GPU tests (the kernel path is, through
-    emulate_slabs_peer)."""
-    import torch
-    import torch.distributed as dist
-    import torch.distributed._symmetric_memory as symm
-    want = torch.complex64 if dtype == "c64" else torch.complex128
-    grp = group if group is not None else dist.group.WORLD
-    recv, handles = [], []
-    for _ in range(2):
-        b = symm.empty(L, n, dtype=want, device=torch.device("cuda", torch.cuda.current_device()))
-        handles.append(symm.rendezvous(b, grp))
-        recv.append(b)
-    peer_ptrs = [list(h.buffer_ptrs) for h in handles]
-    return recv, peer_ptrs, (lambda: handles[0].barrier())
-
-
-def emulate_slabs_peer(n, M, x_full, nranks, dtype="c64", **kw):
-    """Single-GPU emulation of the fused peer-store exchange: nranks slab plans run one
-    after another, each transposing pass storing its row-blocks straight into the other
-    "ranks'" receive buffers (all on this GPU; no kernel waits on another).  Returns the
-    assembled [n, n] output."""
-    import torch
-    L = n // nranks
-    plans = [SlabPlan(n, M, nranks, r, dtype=dtype, **kw) for r in range(nranks)]
-    cur = [x_full[r * L:(r + 1) * L].contiguous() for r in range(nranks)]
-    recv = [[torch.empty_like(cur[0]) for _ in range(nranks)] for _ in range(2)]
-    np_ = plans[0].n_passes
-    for k in range(np_ - 1):
-        ptrs = [t.data_ptr() for t in recv[k % 2]]
-        for r in range(nranks):
-            plans[r].exec_pass_peer(k, cur[r], ptrs)
-        cur = recv[k % 2]
-    outs = [torch.empty_like(c) for c in cur]
-    for r in range(nranks):
-        plans[r].exec_pass(np_ - 1, cur[r], outs[r])
-    for p in plans:
-        p.close()
-    return torch.cat(outs, dim=0)
-
-
-def emulate_slabs(n, M, x_full, nranks, dtype="c64", **kw):
-    """Single-GPU emulation of the row-slab mode: nranks slab plans run one after another,
-    the all-to-all done by block copies on the device (no kernel waits on another).
-    x_full: CUDA tensor [n, n].  Returns the assembled [n, n] output."""
-    import torch
-    L = n // nranks
-    plans = [SlabPlan(n, M, nranks, r, dtype=dtype, **kw) for r in range(nranks)]
-    cur = [x_full[r * L:(r + 1) * L].contiguous() for r in range(nranks)]
-    outs = [torch.empty_like(c) for c in cur]
-    np_ = plans[0].n_passes
-    for k in range(np_):
-        last = (k == np_ - 1)
-        for r in range(nranks):
-            plans[r].exec_pass(k, cur[r], outs[r])
-        if last:
-            break
-        # all-to-all: block s of rank r's output -> block r of rank s's input
-        nxt = [torch.empty_like(c) for c in cur]
-        for r in range(nranks):
-            src = outs[r].view(nranks, L * L)
-            for s_ in range(nranks):
-                nxt[s_].view(nranks, L * L)[r].copy_(src[s_])
-        cur = nxt
-        outs = [torch.empty_like(c) for c in cur]
-    for p in plans:
-        p.close()
-    return torch.cat(outs, dim=0)
 
 
 def default_dx(n):
@@ -374,10 +383,12 @@ def default_dx(n):
 
 
 def inverse_matrix(M):
-    """M^-1 = (D^T, -B^T; -C^T, A^T) (Eq. CCCMCCCM20): the inverse transform's matrix."""
-    M = np.asarray(M, dtype=np.float64).reshape(4, 4)
-    A, B, C, D = M[:2, :2], M[:2, 2:], M[2:, :2], M[2:, 2:]
-    return np.block([[D.T, -B.T], [-C.T, A.T]])
+    """M^-1 = (D^T, -B^T; -C^T, A^T) (Eq. CCCMCCCM20), computed by the
+    library (nslct_inverse_matrix): the inverse transform's matrix."""
+    a, ap = _abcd(M)
+    out = np.empty(16, np.float64)
+    _check(lib().nslct_inverse_matrix(ap, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    return out.reshape(4, 4)
 
 
 def nsdlct(x, M, variant="HA", dispatch="reversible", dx=None, n=None, h_fixed=None, stream=None):

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(L, name), name
     assert sorted(nslct.EXPORTS) == declared
-    assert L.nslct_abi_version() == 3
+    assert L.nslct_abi_version() == nslct.ABI_VERSION == 4
 
 
 def test_describe_errors():

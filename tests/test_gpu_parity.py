@@ -23,6 +23,8 @@ pytestmark = pytest.mark.gpu
 
 from paper_1707_03688_b200 import nslct  # noqa: E402
 
+import slab_emulation  # noqa: E402  (tests/slab_emulation.py)
+
 TOL = {"c64": 1e-4, "c128": 1e-10}
 TDT = {"c64": torch.complex64, "c128": torch.complex128}
 NDT = {"c64": np.complex64, "c128": np.complex128}
@@ -129,6 +131,51 @@ def test_config4_n4096_batch32():
         assert abs(e_out / e_in - 1) < 1e-5, i
 
 
+def test_config4_bench_call_own_planner():
+    """C4 through the exact call bench.py times: nslct.Plan(4096, M, 32, profile=True) with
+    the library's OWN plan (no FIXED_H).  The plan equals the oracle planner's (kind, H to
+    1e-9); images 0 and 31 equal the oracle run with its own plan (relL2 <= 1e-4)."""
+    mr, ir = synth.config_streams(4)
+    M = synth.random_symplectic(mr)
+    x = np.empty((32, 4096, 4096), np.complex64)
+    for i in range(32):
+        x[i] = synth.iid_cn(ir, (4096, 4096))
+    with nslct.Plan(4096, M, 32, profile=True) as p:
+        info = p.info()
+        G = p.exec(torch.from_numpy(x).cuda()).cpu().numpy()
+        p.pass_ms()
+    for i in (0, 31):
+        ref, pl = oracle(x[i], M)
+        assert info["kind"] == pl["kind"] and np.abs(info["h"] - pl["h"]).max() < 1e-9
+        err = me.rel_l2(G[i], ref)
+        assert err <= TOL["c64"], (i, err)
+
+
+def test_config5_n16384_oracle_parity():
+    """C5 (16384^2 complex64, BASELINE configs[4]) element-wise against the fp64 oracle
+    O_plan (all 2.7e8 outputs; dense-DFT chain of Eq. HA28): the
+    single-GPU transform with the library's own plan (the bench's call), the 8-rank
+    row-slab form (emulated on this GPU, two exchange chunks -- the
+    default sub-block layout) and the same slab form with the exchange fused into the
+    stores (peer emulation).  relL2 <= 1e-4 each.  The oracle takes minutes on the host."""
+    n = 16384
+    mr, ir = synth.config_streams(5)
+    M = synth.random_symplectic(mr)
+    x = synth.iid_cn(ir, (n, n)).astype(np.complex64)
+    xt = torch.from_numpy(x).to("cuda")
+    with nslct.Plan(n, M, 1, profile=True) as p:
+        info = p.info()
+        G1 = p.exec(xt.view(1, n, n))[0].cpu().numpy()
+    G8 = slab_emulation.emulate_slabs(n, M, xt, 8).cpu().numpy()
+    G8p = slab_emulation.emulate_slabs_peer(n, M, xt, 8).cpu().numpy()
+    del xt
+    torch.cuda.empty_cache()
+    ref, pl = oracle(x, M)
+    assert info["kind"] == pl["kind"] and np.abs(info["h"] - pl["h"]).max() < 1e-9
+    errs = [me.rel_l2(G, ref) for G in (G1, G8, G8p)]
+    assert max(errs) <= TOL["c64"], errs
+
+
 def test_config5_n16384_properties():
     """C5 on one GPU: 16384x16384 complex64 single transform (2 GiB).  The full oracle is
     out of reach, so: (i) Parseval; (ii) reversibility exec(M^-1) exec(M) = I; (iii) the
@@ -168,7 +215,7 @@ def test_config5_n16384_properties():
 
 
 @pytest.mark.parametrize("n,batch,variant", [(8192, 2, "HA"), (16384, 1, "HA"), (8192, 1, "LC")])
-def test_large_n_cluster_pair_kernels(monkeypatch, n, batch, variant):
+def test_large_n_cluster_pair_kernels(n, batch, variant):
     """N = 8192, 16384 (complex64, batched): the persistent 2-CTA cluster-pair line passes
     (pair-interleaved intermediates, 32-byte segment stores through DSMEM) compute what the
     one-line-per-CTA passes compute -- same butterflies and chirps, only the intermediate
@@ -187,8 +234,7 @@ def test_large_n_cluster_pair_kernels(monkeypatch, n, batch, variant):
     rel = float(torch.linalg.vector_norm((back - xt).to(torch.complex128)) /
                 torch.linalg.vector_norm(xt.to(torch.complex128)))
     assert rel < 1e-5, rel
-    monkeypatch.setenv("NSLCT_NO_PAIR", "1")
-    with nslct.Plan(n, M, batch, **kw) as p:
+    with nslct.Plan(n, M, batch, kernels="generic", **kw) as p:
         G_line = p.exec(xt)
     torch.cuda.synchronize()
     d = float(torch.linalg.vector_norm((G - G_line).to(torch.complex128)) /
@@ -285,15 +331,17 @@ def test_both_forms(policy):
 
 
 def test_gpu_own_planner_matches_oracle():
-    """Without FIXED_H: the library's own HA plan gives the oracle's operator (planner parity)."""
+    """Without FIXED_H: the library's own HA plan (planner.cpp) IS the oracle's plan (same
+    kind and H to 1e-9, reading R5) and gives the oracle's operator (planner parity)."""
     mr, ir = synth.config_streams(8)
     for _ in range(3):
         M = synth.random_symplectic(mr)
         x = synth.iid_cn(ir, (1, 64, 64))
         G, info = run_gpu(x, M, "c128")
         ref, pl = oracle(x[0], M)
-        if np.abs(info["h"] - pl["h"]).max() < 1e-9:
-            assert me.rel_l2(G[0], ref) <= 1e-9
+        assert info["kind"] == pl["kind"]
+        assert np.abs(info["h"] - pl["h"]).max() < 1e-9, (info["h"], pl["h"])
+        assert me.rel_l2(G[0], ref) <= 1e-9
 
 
 def test_lc_variant():
@@ -366,30 +414,10 @@ def test_lc_y_reversible_and_slab():
     rel = float(torch.linalg.vector_norm((back - xt).to(torch.complex128)) /
                 torch.linalg.vector_norm(xt.to(torch.complex128)))
     assert rel < 1e-5, rel
-    Gs = nslct.emulate_slabs(n, M, xt[0], 4, "c64", variant="LC")
+    Gs = slab_emulation.emulate_slabs(n, M, xt[0], 4, "c64", variant="LC")
     d = float(torch.linalg.vector_norm((Gs - G[0]).to(torch.complex128)) /
               torch.linalg.vector_norm(G[0].to(torch.complex128)))
     assert d < 1e-6, d
-
-
-@pytest.mark.parametrize("kind", ["I", "II"])
-def test_fft64_variant(kind, monkeypatch):
-    """The opt-in 64x64 TMEM-exchange FFT (NSLCT_FFT64=1, N = 4096 pipe kernels): HA both
-    forms and the LC 3-pass schedule (odd exchange count per pass) vs the oracle."""
-    monkeypatch.setenv("NSLCT_FFT64", "1")
-    n = 4096
-    mr, ir = synth.config_streams(500)
-    while True:
-        M = synth.random_symplectic(mr)
-        if opl.plan(M)["kind"] == kind:
-            break
-    x = synth.iid_cn(ir, (2, n, n)).astype(np.complex64)
-    err, info, _ = parity(x, M, "c64", check_imgs=[1])
-    assert err <= TOL["c64"], (kind, err)
-    Ml, pl = lc_matrix(22, kind, "y")
-    G, info = run_gpu(x[:1], Ml, "c64", variant="LC")
-    ref, _ = op.nsdlct(x[0].astype(np.complex128), Ml, variant="LC", pl=pl)
-    assert info["n_passes"] == 3 and me.rel_l2(G[0], ref) <= TOL["c64"]
 
 
 def test_schedule_errors():
@@ -450,21 +478,20 @@ def test_in_place_and_host_exec():
         assert np.array_equal(hout.numpy(), ref)
 
 
-@pytest.mark.parametrize("n,batch,chunk_mb,kind", [
-    (1024, 7, "16", "ha"),     # pipe kernels, 2 images per chunk, ragged last chunk
-    (64, 5, "0.07", "ha"),     # on-chip kernel, 2 images per chunk
-    (256, 3, "0.6", "b0"),     # B = 0 gather, 1 image per chunk
-    (128, 4, "64", "ha"),      # whole batch in one chunk
+@pytest.mark.parametrize("n,batch,chunk_kb,kind", [
+    (1024, 7, 16384, "ha"),    # pipe kernels, 2 images per chunk, ragged last chunk
+    (64, 5, 72, "ha"),         # on-chip kernel, 2 images per chunk
+    (256, 3, 614, "b0"),       # B = 0 gather, 1 image per chunk
+    (128, 4, 65536, "ha"),     # whole batch in one chunk
 ])
-def test_exec_host_chunked(monkeypatch, n, batch, chunk_mb, kind):
+def test_exec_host_chunked(n, batch, chunk_kb, kind):
     """nslct_exec_host pipelines the batch in image chunks over two copy streams: the
     result equals the device exec bit for bit, whatever the chunking (include/nslct.h)."""
-    monkeypatch.setenv("NSLCT_HOST_CHUNK_MB", chunk_mb)
     mr, ir = synth.config_streams(13)
     M = (synth.random_symplectic(mr) if kind == "ha"
          else synth.b0_matrix4([[1.2, 0.3], [-0.4, 0.9]], [[0.5, -0.2], [-0.2, 1.1]]))
     x = synth.iid_cn(ir, (batch, n, n)).astype(np.complex64)
-    with nslct.Plan(n, M, batch) as p:
+    with nslct.Plan(n, M, batch, host_chunk_kb=chunk_kb) as p:
         ref = p.exec(torch.from_numpy(x).cuda()).cpu().numpy()
         hin = torch.from_numpy(x).pin_memory()
         for _ in range(2):   # second call reuses the streams and events
@@ -519,19 +546,22 @@ def test_profile_pass_times():
 
 
 # ------------------------------------------------------------------ row-slab mode (a12)
-@pytest.mark.parametrize("n,nranks,dtype", [(256, 2, "c64"), (256, 4, "c128"), (1024, 8, "c64"), (4096, 4, "c64"),
-                                            (8192, 4, "c64"), (8192, 2, "c128")])
-def test_slab_mode_emulated(n, nranks, dtype):
+@pytest.mark.parametrize("n,nranks,dtype,chunks", [(256, 2, "c64", 1), (256, 4, "c128", 2), (1024, 8, "c64", 4),
+                                                   (4096, 4, "c64", 8), (8192, 4, "c64", 4), (8192, 2, "c128", 2),
+                                                   (16384, 8, "c64", 1)])
+def test_slab_mode_emulated(n, nranks, dtype, chunks):
     """§8(e): one transform as nranks row slabs with the all-to-all between passes
     (emulated on one GPU by block copies; every pass runs the real slab kernels with global
-    chirp indices and chunked lines).  Matches the single-plan transform bit-for-bit up to
-    rounding order (relL2 <= 1e-6 c64 / 1e-13 c128) and the oracle (small n)."""
+    chirp indices and chunked lines; the output blocks split into `chunks` sub-blocks, the
+    layout of the chunked NCCL exchange).  Matches the single-plan transform bit-for-bit up
+    to rounding order (relL2 <= 1e-6 c64 / 1e-13 c128) and the oracle (small n)."""
     mr, ir = synth.config_streams(60 + n)
     M = synth.random_symplectic(mr)
     x = synth.iid_cn(ir, (n, n)).astype(NDT[dtype])
     pl = opl.plan(M)
     xt = torch.from_numpy(x).cuda()
-    G_slab = nslct.emulate_slabs(n, M, xt, nranks, dtype=dtype, h_fixed=pl["h"]).cpu().numpy()
+    G_slab = slab_emulation.emulate_slabs(n, M, xt, nranks, dtype=dtype, h_fixed=pl["h"],
+                                          exchange_chunks=chunks).cpu().numpy()
     with nslct.Plan(n, M, 1, dtype=dtype, h_fixed=pl["h"]) as p:
         G_one = p.exec(xt.view(1, n, n)).cpu().numpy()[0]
     assert me.rel_l2(G_slab, G_one) <= (1e-6 if dtype == "c64" else 1e-13)
@@ -549,7 +579,7 @@ def test_slab_mode_c5_16384_emulated_8_ranks():
     g = torch.Generator(device="cuda")
     g.manual_seed(5)
     xt = torch.randn((n, n), dtype=torch.complex64, device="cuda", generator=g)
-    G_slab = nslct.emulate_slabs(n, M, xt, nranks)
+    G_slab = slab_emulation.emulate_slabs(n, M, xt, nranks)
     with nslct.Plan(n, M, 1) as p:
         G_one = p.exec(xt.view(1, n, n))[0]
     rel = float(torch.linalg.vector_norm((G_slab - G_one).to(torch.complex128)) /
@@ -576,8 +606,8 @@ def test_slab_fused_peer_exchange_emulated(n, nranks, dtype, variant):
         xt = torch.randn((n, n), dtype=torch.complex64, device="cuda", generator=g)
     else:
         xt = torch.from_numpy(synth.iid_cn(ir, (n, n)).astype(NDT[dtype])).cuda()
-    G_peer = nslct.emulate_slabs_peer(n, M, xt, nranks, dtype=dtype, **kw)
-    G_a2a = nslct.emulate_slabs(n, M, xt, nranks, dtype=dtype, **kw)
+    G_peer = slab_emulation.emulate_slabs_peer(n, M, xt, nranks, dtype=dtype, **kw)
+    G_a2a = slab_emulation.emulate_slabs(n, M, xt, nranks, dtype=dtype, **kw)
     assert torch.equal(G_peer, G_a2a)
     with nslct.Plan(n, M, 1, dtype=dtype, **kw) as p:
         G_one = p.exec(xt.view(1, n, n))[0]
@@ -844,37 +874,57 @@ def test_one_shot_api():
     assert Gp.shape == (100, 100) and me.rel_l2(Gp, refp) <= 1e-4
 
 
-@pytest.mark.parametrize("n", [1024, 8192])
-def test_symm_mem_peer_exchange_single_rank(n):
-    """The multi-GPU fused-exchange plumbing (torch symmetric memory receive buffers, their
-    peer pointers and stream-ordered barrier -- nslct.symm_mem_exchange -- driving
-    SlabPlan.run_peer) on a one-rank NCCL process group: the transform equals the
-    single-plan result.  (Real peers need more than one GPU.)"""
-    import tempfile
-
-    import torch.distributed as dist
-    if dist.is_initialized():
-        pytest.skip("a process group already exists")
-    mr, ir = synth.config_streams(950 + n)
+@pytest.mark.parametrize("n,dtype,exchange,chunks", [(1024, "c64", "nccl", 2), (1024, "c64", "peer", 1),
+                                                     (512, "c128", "nccl", 4), (8192, "c64", "nccl", 2),
+                                                     (8192, "c64", "peer", 2)])
+def test_comm_plan_single_rank(n, dtype, exchange, chunks):
+    """The multi-GPU product path on one rank: a comm plan (nslct_plan_ex with
+    opts.comm = the library's own NCCL communicator) run by ONE nslct_exec call -- passes,
+    chunked grouped ncclSend/ncclRecv (or the peer-store exchange with its NCCL barrier),
+    no host-side pass loop.  Equals the emulated slab passes of the same layout bit for
+    bit, the batched plan (bit for bit with the generic kernels, which run the same
+    arithmetic; to 1e-6 otherwise) and the oracle."""
+    mr, ir = synth.config_streams(940 + n)
     M = synth.random_symplectic(mr)
-    g = torch.Generator(device="cuda")
-    g.manual_seed(n)
-    x = torch.randn((n, n), dtype=torch.complex64, device="cuda", generator=g)
-    with tempfile.NamedTemporaryFile() as f:
-        dist.init_process_group("nccl", init_method="file://" + f.name, rank=0, world_size=1,
-                                device_id=torch.device("cuda", torch.cuda.current_device()))
-        try:
-            recv, ptrs, barrier = nslct.symm_mem_exchange(n, n)
-            with nslct.SlabPlan(n, M, 1, 0) as sp:
-                G = sp.run_peer(x, recv, ptrs, barrier)
+    x = synth.iid_cn(ir, (n, n)).astype(NDT[dtype])
+    xt = torch.from_numpy(x).cuda()
+    with nslct.Communicator.local() as comm:
+        assert (comm.rank, comm.nranks) == (0, 1)
+        with nslct.Plan(n, M, 1, dtype=dtype, comm=comm, exchange=exchange, exchange_chunks=chunks) as p:
+            G = p.exec(xt)
+            G2 = p.exec(xt)          # the exchange buffers are reused
             torch.cuda.synchronize()
-        finally:
-            dist.destroy_process_group()
-    with nslct.Plan(n, M, 1) as p:
-        G1 = p.exec(x.view(1, n, n))[0]
-    rel = float(torch.linalg.vector_norm((G - G1).to(torch.complex128)) /
-                torch.linalg.vector_norm(G1.to(torch.complex128)))
-    assert rel <= 1e-6, rel
+    assert torch.equal(G, G2)
+    Ge = slab_emulation.emulate_slabs(n, M, xt, 1, dtype=dtype, exchange_chunks=chunks)
+    assert torch.equal(G, Ge)
+    kern = "generic" if n < 8192 else "auto"
+    with nslct.Plan(n, M, 1, dtype=dtype, kernels=kern) as p:
+        Gb = p.exec(xt.view(1, n, n))[0]
+    if kern == "generic":
+        assert torch.equal(G, Gb)
+    else:
+        rel = float(torch.linalg.vector_norm((G - Gb).to(torch.complex128)) /
+                    torch.linalg.vector_norm(Gb.to(torch.complex128)))
+        assert rel <= 1e-6, rel
+    if n <= 1024:
+        ref, _ = oracle(x, M)
+        assert me.rel_l2(G.cpu().numpy(), ref) <= TOL[dtype]
+
+
+def test_comm_plan_errors():
+    """Comm plans: batch must be 1; nslct_plan_slab refuses opts.comm; bad exchange options."""
+    M = synth.random_symplectic(np.random.default_rng(5))
+    with nslct.Communicator.local() as comm:
+        for kw in (dict(batch=2), dict(batch=1, exchange_chunks=3)):
+            b = kw.pop("batch")
+            with pytest.raises(nslct.NslctError) as e:
+                nslct.Plan(1024, M, b, comm=comm, **kw)
+            assert e.value.name == "E_ARG"
+        with nslct.Plan(1024, M, 1, comm=comm) as p:
+            with pytest.raises(ValueError):
+                p.exec(torch.zeros((1, 1024, 1024), dtype=torch.complex64, device="cuda"))
+            with pytest.raises(ValueError):
+                p.exec_host(np.zeros((1024, 1024), np.complex64), np.zeros((1024, 1024), np.complex64))
 
 
 def test_exec_pass_batched_equals_exec():

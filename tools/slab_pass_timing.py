@@ -1,6 +1,6 @@
 """Per-rank pass times of the row-slab mode, measured on ONE GPU by running every rank's
 passes one after another (the all-to-all replaced by device block copies, as in
-nslct.emulate_slabs).  Prints one JSON line: per-pass ms summed over ranks (= one GPU doing
+tests/slab_emulation.py).  Prints one JSON line: per-pass ms summed over ranks (= one GPU doing
 all ranks' HBM work) and divided by P (the per-GPU HBM time of a P-GPU run, without the
 exchange).  Usage: python tools/slab_pass_timing.py [n] [P] [reps]"""
 import json
@@ -42,7 +42,7 @@ def main():
             cur = out   # layout-only stand-in for the exchange: the timing is what matters
             out = [torch.empty_like(t) for t in x]
     hbm = 2.0 * n * n * 8
-    res = {"n": n, "P": P, "pair_kernels": os.environ.get("NSLCT_NO_PAIR") != "1",
+    res = {"n": n, "P": P, "pair_kernels": True,
            "pass_ms_all_ranks": [round(t, 3) for t in tot],
            "per_gpu_ms": round(sum(tot) / P, 3),
            "hbm_TBps_per_pass": [round(hbm / (t * 1e-3) / 1e12, 2) for t in tot]}
