@@ -32,17 +32,19 @@ def _Finv(G, workers):
     return sfft.fftshift(sfft.ifft2(sfft.ifftshift(G), workers=workers))
 
 
-def transform(g, chain, dx, workers=-1):
-    """g: (N, N) complex; chain: [("CM", Q) | ("CC", B), ...] in application order."""
-    out = np.asarray(g, np.complex128)
+def transform(g, chain, dx, workers=-1, dtype=np.complex128):
+    """g: (N, N) complex; chain: [("CM", Q) | ("CC", B), ...] in application order.
+    dtype: complex128 (fp64 FFTs) or complex64 (fp32 FFTs; chirps computed in fp64 and
+    rounded)."""
+    out = np.asarray(g, dtype)
     n = out.shape[-1]
     dw = 2.0 * math.pi / (n * dx)
     for kind, Q in chain:
         Q = np.asarray(Q, np.float64)
         if kind == "CM":
-            out = _chirp(n, Q, dx) * out
+            out = _chirp(n, Q, dx).astype(dtype) * out
         elif kind == "CC":
-            out = _Finv(_chirp(n, -Q, dw) * _F(out, workers), workers)
+            out = _Finv(_chirp(n, -Q, dw).astype(dtype) * _F(out, workers), workers)
         else:
             raise ValueError("the FFT baseline covers the HA chain only (%s)" % kind)
     return out

@@ -281,6 +281,12 @@ nslct_status nslct_plan_describe(int64_t n, const double abcd[16], const nslct_o
  * n_launches floats; *n_written receives n_launches (one value for an on-chip plan). */
 nslct_status nslct_pass_ms(nslct_plan_t plan, float* ms, int capacity, int* n_written);
 
+/* Measured FP32 FMA throughput of `device` (TFLOP/s, 2 flops per FFMA): a calibration
+ * kernel of independent FFMA chains on every SM, best of 3 timed launches (~ms each).  The
+ * ALU ceiling reported next to the HBM roofline.  Synchronous.
+ * Errors: E_ARG, E_CUDA. */
+nslct_status nslct_fp32_peak(int device, double* tflops);
+
 /* Free the plan and everything it owns (device-synchronises its buffers). NULL is a no-op. */
 nslct_status nslct_destroy(nslct_plan_t plan);
 

@@ -1667,6 +1667,58 @@ nslct_status nslct_inverse_matrix(const double abcd[16], double out[16]) {
   return NSLCT_OK;
 }
 
+// ---- FP32 roofline calibration --------------------------------------------------------
+// 16 independent FFMA chains per thread, 2048 threads per SM: the FMA pipe's issue-bound
+// rate (SURVEY.md §8(d) asks for the measured FP32 ceiling next to the HBM one).
+}  // extern "C"
+namespace {
+__global__ void __launch_bounds__(1024) fp32_peak_kernel(float* out, int iters, float a, float b) {
+  float x[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) x[k] = (float)(threadIdx.x + k);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = fmaf(x[k], a, b);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) s += x[k];
+  if (s == 1.2345f) out[blockIdx.x] = s;   // never true for the launch below; keeps the work
+}
+}  // namespace
+extern "C" {
+
+nslct_status nslct_fp32_peak(int device, double* tflops) {
+  if (!tflops) return fail(NSLCT_E_ARG, "null pointer");
+  DeviceGuard guard(device);
+  if (guard.status != cudaSuccess) return fail(NSLCT_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(guard.status));
+  int sms = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  float* out = nullptr;
+  CUDA_TRY(cudaMalloc(&out, (size_t)sms * 2 * sizeof(float)));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  const int iters = 1 << 16;
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0, 0);
+    fp32_peak_kernel<<<sms * 2, 1024>>>(out, iters, 0.999f, 1e-3f);
+    cudaEventRecord(e1, 0);
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    const double flops = 2.0 * 16.0 * iters * (double)sms * 2.0 * 1024.0;
+    if (rep > 0 && ms > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  CUDA_TRY(cudaGetLastError());
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  *tflops = best;
+  return NSLCT_OK;
+}
+
 nslct_status nslct_destroy(nslct_plan_t pl) {
   free_plan(pl);
   return NSLCT_OK;

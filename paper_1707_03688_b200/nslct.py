@@ -26,7 +26,7 @@ EXPORTS = ("nslct_opts_default", "nslct_plan", "nslct_plan_ex", "nslct_exec", "n
            "nslct_plan_info", "nslct_plan_describe", "nslct_pass_ms", "nslct_destroy",
            "nslct_last_error", "nslct_abi_version", "nslct_plan_slab", "nslct_exec_pass",
            "nslct_exec_pass_peer", "nslct_inverse_matrix", "nslct_comm_unique_id", "nslct_comm_init",
-           "nslct_comm_info", "nslct_comm_destroy")
+           "nslct_comm_info", "nslct_comm_destroy", "nslct_fp32_peak")
 ABI_VERSION = 4
 KERNELS = {"auto": 0, "generic": 1}
 EXCHANGES = {"nccl": 0, "peer": 1}
@@ -88,12 +88,13 @@ def lib():
         L.nslct_comm_init.argtypes = [ctypes.POINTER(vp), ctypes.c_char_p, ctypes.c_int, ctypes.c_int]
         L.nslct_comm_info.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
         L.nslct_comm_destroy.argtypes = [vp]
+        L.nslct_fp32_peak.argtypes = [ctypes.c_int, dp]
         L.nslct_last_error.restype = ctypes.c_char_p
         L.nslct_abi_version.restype = ctypes.c_int
         for f in ("nslct_plan", "nslct_plan_ex", "nslct_exec", "nslct_exec_host", "nslct_plan_info",
                   "nslct_plan_describe", "nslct_pass_ms", "nslct_destroy", "nslct_plan_slab",
                   "nslct_exec_pass", "nslct_exec_pass_peer", "nslct_inverse_matrix", "nslct_comm_unique_id",
-                  "nslct_comm_init", "nslct_comm_info", "nslct_comm_destroy"):
+                  "nslct_comm_init", "nslct_comm_info", "nslct_comm_destroy", "nslct_fp32_peak"):
             getattr(L, f).restype = ctypes.c_int
         if L.nslct_abi_version() != ABI_VERSION:
             raise ImportError("libnslct.so ABI %d, binding expects %d: rebuild (python -m paper_1707_03688_b200.build)"
@@ -376,6 +377,13 @@ class SlabPlan(Plan):
         arr = (ctypes.c_void_p * len(peer_ptrs))(*[int(p) for p in peer_ptrs])
         _check(lib().nslct_exec_pass_peer(self._h, int(k), ctypes.c_void_p(x.data_ptr()), arr,
                                           len(peer_ptrs), ctypes.c_void_p(s.cuda_stream)))
+
+
+def fp32_peak_tflops(device=0):
+    """Measured FP32 FMA throughput of the device (nslct_fp32_peak), TFLOP/s."""
+    t = ctypes.c_double(0.0)
+    _check(lib().nslct_fp32_peak(int(device), ctypes.byref(t)))
+    return t.value
 
 
 def default_dx(n):

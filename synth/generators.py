@@ -17,7 +17,7 @@ __all__ = [
     "SEED_BASE", "config_streams", "rot2", "block", "random_symplectic",
     "dft_matrix4", "idft_matrix4", "gyrator_matrix4", "separable_matrix4",
     "b0_matrix4", "identity4", "iid_cn", "chirp_gauss_field",
-    "random_phase_field", "default_dx", "CONFIGS",
+    "random_phase_field", "default_dx", "CONFIGS", "c3_sweep_matrices",
 ]
 
 SEED_BASE = 170703688
@@ -147,6 +147,34 @@ def chirp_gauss_field(rng: np.random.Generator, n: int, batch: int, dx: float = 
 def random_phase_field(rng: np.random.Generator, shape) -> np.ndarray:
     """Config-3 input: unit amplitude, phase 2*pi*U[0,1)."""
     return np.exp(2j * math.pi * rng.uniform(0.0, 1.0, shape))
+
+
+def c3_sweep_matrices(rng: np.random.Generator) -> dict:
+    """Config-3 special-case sweep (BASELINE.json configs[2]), drawn in
+    this order from the config's matrix stream: the 2D DFT (0,I;-I,0); a gyrator with
+    alpha ~ U[0,pi), redrawn while sin^2 alpha <= 0.1; a separable pair with a_i, b_i, c_i
+    ~ U[-2,2], |b_i| > 0.32, |a_i| > 0.1; and a B = 0 matrix (D^-T, 0; S D^-T, D) with
+    D ~ U[-2,2], 0.5 <= |det D| <= 2, S ~ U[-2,2] symmetrised."""
+    subs = {"dft": dft_matrix4()}
+    while True:
+        a = rng.uniform(0, math.pi)
+        if math.sin(a) ** 2 > 0.1:
+            break
+    subs["gyrator"] = gyrator_matrix4(a)
+    while True:
+        a = rng.uniform(-2, 2, 2)
+        b = rng.uniform(-2, 2, 2)
+        c = rng.uniform(-2, 2, 2)
+        if np.all(np.abs(b) > 0.32) and np.all(np.abs(a) > 0.1):
+            break
+    subs["separable"] = separable_matrix4(a, b, c)
+    while True:
+        D = rng.uniform(-2, 2, (2, 2))
+        if 0.5 <= abs(np.linalg.det(D)) <= 2:
+            break
+    S = rng.uniform(-2, 2, (2, 2))
+    subs["b0"] = b0_matrix4(D, S)
+    return subs
 
 
 CONFIGS = {

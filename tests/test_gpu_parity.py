@@ -91,24 +91,7 @@ def test_config3_n1024_sweep(sub):
     """C3: 1024x1024 complex64, batch 16, special-case sweep; 4 of 16 images vs the oracle,
     the remaining images through the same launch."""
     mr, ir = synth.config_streams(3)
-    subs = {}
-    subs["dft"] = synth.dft_matrix4()
-    while True:
-        a = mr.uniform(0, math.pi)
-        if math.sin(a) ** 2 > 0.1:
-            break
-    subs["gyrator"] = synth.gyrator_matrix4(a)
-    while True:
-        a = mr.uniform(-2, 2, 2); b = mr.uniform(-2, 2, 2); c = mr.uniform(-2, 2, 2)
-        if np.all(np.abs(b) > 0.32) and np.all(np.abs(a) > 0.1):
-            break
-    subs["separable"] = synth.separable_matrix4(a, b, c)
-    while True:
-        D = mr.uniform(-2, 2, (2, 2))
-        if 0.5 <= abs(np.linalg.det(D)) <= 2:
-            break
-    S = mr.uniform(-2, 2, (2, 2))
-    subs["b0"] = synth.b0_matrix4(D, S)
+    subs = synth.c3_sweep_matrices(mr)
     M = subs[sub]
     x = synth.random_phase_field(ir, (16, 1024, 1024)).astype(np.complex64)
     err, info, _ = parity(x, M, "c64", check_imgs=[0, 5, 10, 15])

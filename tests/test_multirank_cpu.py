@@ -101,3 +101,24 @@ def test_slab_all_to_all_layout_gloo():
             for m in range(n):
                 # the value at that position is the pass output (element = s*L+ql, line = m)
                 assert flat[(m // L) * L * L + ql * L + m % L] == 1000 * (s * L + ql) + m
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`python bench.py --gpus 2` (no torchrun environment) starts 2 ranks itself
+    (torch.distributed.run, 127.0.0.1) and reports n_gpus = 2 with the global batch of 32
+    sharded 16 per rank (BASELINE configs[3]); --dry-run swaps the GPU step for a CPU
+    stand-in and NCCL for gloo, keeping the spawn / max-over-ranks / sum-over-ranks path."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "2",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["ranks_reporting"] == 2
+    assert d["config"]["global_batch"] == 32 and d["config"]["per_gpu_batch"] == 16
+    assert d["scaling"] == "strong" and d["value"] > 0
