@@ -115,7 +115,11 @@ enum { NSLCT_EXCHANGE_NCCL = 0,   /* NCCL grouped send/recv of each chunk's sub-
 enum { NSLCT_KERNELS_AUTO = 0,     /* the specialised kernels where they exist: persistent
                                       TMA pipe (c64, N = 1024..4096), cluster pairs (c64,
                                       N = 8192, 16384), on-chip (see schedule)              */
-       NSLCT_KERNELS_GENERIC = 1   /* one CTA per group of lines everywhere (A/B reference)  */
+       NSLCT_KERNELS_GENERIC = 1,  /* one CTA per group of lines everywhere (A/B reference)  */
+       NSLCT_KERNELS_PAIR_V1 = 2   /* as AUTO, but N = 8192 / 16384 c64 with the round-1
+                                      cluster-pair kernels (per-thread loads, pair-interleaved
+                                      intermediates): A/B reference of the TMA-pipelined
+                                      large-N kernels                                       */
 };
 /* schedules of a batched plan (all compute the same operator) */
 enum { NSLCT_SCHEDULE_AUTO = 0,        /* the on-chip kernel for N <= 64 (measured faster at

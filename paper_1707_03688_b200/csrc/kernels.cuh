@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 
 namespace nslct {
 
@@ -272,6 +274,35 @@ struct TwSet {
   }
 };
 
+// Stage twiddle bases loaded when the previous stage's exchange begins (prefetch<S>, from
+// the fp64-accurate table, L2-resident), so only one stage's bases occupy registers: the
+// 1024-thread large-N kernel has 64 registers per thread.
+template <int LOG2N>
+struct TwLazy {
+  static constexpr bool kBluestein = false;
+  using Sh = FftShape<LOG2N>;
+  static constexpr int NBMAX = 16 / Sh::template R<Sh::NS - 1>() > 1 ? 16 / Sh::template R<Sh::NS - 1>() : 1;
+  const cpx<float>* __restrict__ tw;
+  int j;
+  mutable cpx<float> w[NBMAX];
+  template <int S>
+  __device__ __forceinline__ void prefetch() const {
+    if constexpr (S >= 1 && S < Sh::NS) {
+      constexpr int R = Sh::template R<S>(), Ns = Sh::template Ns<S>(), NB = 16 / R;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int jp = j + b * Sh::TL;
+        const float2 t = __ldg(reinterpret_cast<const float2*>(tw) + (jp % Ns) * (Sh::N / (Ns * R)));
+        w[b] = cpx<float>{t.x, t.y};
+      }
+    }
+  }
+  template <int S, int R>
+  __device__ __forceinline__ void apply(cpx<float>* u, int b, int /*jp*/) const {
+    apply_twiddles<R>(u, w[b]);
+  }
+};
+
 // ---------------------------------------------------------------------------------
 // Line FFT of length N = 2^LOG2N, E = 16 elements per thread, TL = N/16 threads per line.
 // Register slot e of thread j holds element j + TL*e, before and after (Stockham
@@ -395,6 +426,7 @@ struct TwTmem {
 //         barrier is not needed.
 template <typename T>
 struct ExPad {
+  static constexpr bool kSplit = false;
   static constexpr bool kDouble = false;
   static constexpr bool kPadded = true;
   static constexpr int kPadW = 1;
@@ -409,6 +441,7 @@ struct ExPad {
 };
 template <typename T, class Hook, int PW = 1>
 struct ExPad2 {   // two padded buffers used alternately: write, barrier, read
+  static constexpr bool kSplit = false;
   static constexpr bool kDouble = true;
   static constexpr bool kPadded = true;
   static constexpr int kPadW = PW;
@@ -427,7 +460,79 @@ struct ExPad2 {   // two padded buffers used alternately: write, barrier, read
 };
 
 template <typename T, int LOG2N, int STAGE, int NS, int X, class E, class TW>
+__device__ __forceinline__ void fft_stage_split(cpx<T> (&v)[16], int j, const TW& tw, const E& ex) {
+  constexpr int N = 1 << LOG2N;
+  constexpr int TL = N / 16;
+  constexpr int NFULL = LOG2N / 4;
+  constexpr int R = (STAGE < NFULL) ? 16 : (1 << (LOG2N % 4));
+  constexpr int NB = 16 / R;
+  constexpr bool LAST = (STAGE == NS - 1);
+  constexpr int Ns = (STAGE < NFULL) ? (1 << (4 * STAGE)) : (1 << (4 * NFULL));
+  static_assert(TL % 16 == 0, "split exchange: padded fast addressing");
+  constexpr int WSTEP = (Ns >= 16) ? Ns + Ns / 16 : Ns;
+  constexpr int RSTEP = TL + TL / 16;
+  // butterflies: outputs stay in registers (slot b + r NB)
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int jp = j + b * TL;
+    cpx<T> u[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) u[r] = v[b + r * NB];
+    if constexpr (Ns > 1) tw.template apply<STAGE, R>(u, b, jp);
+    dft<R>(u);
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[b + r * NB] = u[r];
+  }
+  if constexpr (!LAST) {
+    tw.template prefetch<STAGE + 1>();
+    float* buf = ex.buf;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      if (half == 1 || STAGE > 0 || X > 0) __syncthreads();   // the previous round's reads are done
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int jp = j + b * TL;
+        const int idxD = (jp / Ns) * Ns * R + (jp % Ns);
+        float* wb = buf + padw<1>(idxD);
+#pragma unroll
+        for (int r = 0; r < R; ++r) wb[r * WSTEP] = half ? v[b + r * NB].y : v[b + r * NB].x;
+      }
+      __syncthreads();
+      const float* rb = buf + padw<1>(j);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        if (half)
+          v[e].y = rb[e * RSTEP];
+        else
+          v[e].x = rb[e * RSTEP];
+      }
+    }
+  }
+}
+
+//  ExSplit: ONE padded buffer of floats (half the bytes of a complex line): each exchange
+//         runs in two rounds, real parts then imaginary parts -- write, barrier, read,
+//         barrier, per round.  For the 128 KB lines of N = 16384, where a complex
+//         exchange buffer and the TMA landing buffer of the next line do not both fit in
+//         shared memory (line_pass_big_kernel).
+struct ExSplit {
+  static constexpr bool kSplit = true;
+  static constexpr bool kDouble = false;
+  static constexpr bool kPadded = true;
+  static constexpr int kPadW = 1;
+  float* buf;
+  template <int X>
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+  template <int X>
+  __device__ __forceinline__ void after_barrier() const {}
+};
+
+template <typename T, int LOG2N, int STAGE, int NS, int X, class E, class TW>
 __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TW& tw, const E& ex) {
+  if constexpr (E::kSplit) {
+    fft_stage_split<T, LOG2N, STAGE, NS, X>(v, j, tw, ex);
+    return;
+  } else {
   constexpr int N = 1 << LOG2N;
   constexpr int TL = N / 16;
   constexpr int NFULL = LOG2N / 4;
@@ -487,6 +592,7 @@ __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TW& tw, 
       for (int e = 0; e < 16; ++e) v[e] = buf[ex.idx(j + TL * e)];
     }
     if constexpr (!E::kDouble) __syncthreads();
+  }
   }
 }
 
@@ -1204,6 +1310,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
 // ---------------------------------------------------------------------------------
 template <typename T>
 struct ExPadWS {   // as ExPad2, but the 16 compute warps only (named barrier 1), no hook
+  static constexpr bool kSplit = false;
   static constexpr bool kDouble = true;
   static constexpr bool kPadded = true;
   static constexpr int kPadW = 1;
@@ -1535,6 +1642,177 @@ line_pass_pair_kernel(PassArgs a) {
 }
 
 // ---------------------------------------------------------------------------------
+// Large-N line pass, TMA-pipelined (N = 8192, 16384; complex64; batched and row-slab
+// plans).  Persistent 2-CTA clusters stride the line pairs; CTA c takes line 2p + c of
+// pair p.  The NEXT pair's line is brought into a landing buffer by TMA while this one
+// computes (the one-line-per-CTA kernel above could not overlap its loads: ncu showed its
+// warps waiting on 16 per-thread loads each, lg_throttle and long-scoreboard stalls).
+//   * intermediate layout "Q16" (nslct.h): element mu of consumer line lam at
+//         (mu / C) L C + (lam >> 1) 2C + ((mu % C) >> 1) 4 + (lam & 1) 2 + (mu & 1)
+//     -- inside a pair block, 32-byte segments [lam: mu, mu+1 | lam+1: mu, mu+1] -- so a
+//     CTA reads ITS line as 16-byte pieces with TMA tensor loads (5D map: 16 B, line
+//     parity, mu pair, line pair, chunk; nslct.cu make_q16_map) while the partner reads
+//     the other half of the same sectors;
+//   * a 32-byte output segment is [(i, l0) (i, l1) (i+1, l0) (i+1, l1)] for the pair's
+//     lines l0, l1: each CTA stages (half of) its line in shared memory and, after a
+//     cluster barrier, writes the segments of its share reading the partner's elements
+//     through DSMEM (row slabs: into the all-to-all sub-blocks, or the peers' buffers);
+//   * shared memory = landing buffer (the whole next line) + exchange buffer; at N = 16384
+//     both fit only with the two-round (real / imaginary) exchange (ExSplit);
+//   * twiddle bases per stage loaded lazily (TwLazy): 64 registers at 1024 threads.
+// ---------------------------------------------------------------------------------
+template <int LOG2N>
+struct BigCfg {
+  static constexpr int N = 1 << LOG2N;
+  static constexpr int TL = N / 16;
+  static constexpr int THREADS = TL;                      // one line per CTA
+  static constexpr bool SPLIT = (LOG2N >= 14);
+  static constexpr int XELEMS = N + N / 16 + 16;         // padded exchange index i + i/16
+  static constexpr size_t XBYTES = (size_t)XELEMS * (SPLIT ? 4 : 8);
+  static constexpr size_t LBYTES = (size_t)N * 8;         // landing buffer: one line
+  static constexpr int ROUNDS = SPLIT ? 2 : 1;            // output staging rounds
+  static constexpr size_t SMEM = LBYTES + XBYTES + 64;
+  static_assert((size_t)(N / ROUNDS) * 8 <= XBYTES, "staging fits the exchange buffer");
+};
+
+__device__ __forceinline__ void tensor_g2s_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                              int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
+      "[%7];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
+template <int LOG2N, int MODE, bool SLAB>
+__global__ void __launch_bounds__(BigCfg<LOG2N>::THREADS, 1)
+line_pass_big_kernel(PassArgs a, const __grid_constant__ CUtensorMap imap) {
+  using Cfg = BigCfg<LOG2N>;
+  constexpr int N = Cfg::N, TL = Cfg::TL, THREADS = Cfg::THREADS, ROUNDS = Cfg::ROUNDS;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cpx<float>* land = reinterpret_cast<cpx<float>*>(smem_raw);
+  unsigned char* xraw = smem_raw + Cfg::LBYTES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + Cfg::LBYTES + Cfg::XBYTES);
+  uint32_t c;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c));
+  const int tid = threadIdx.x;
+  const int j = tid;
+  // layout parameters (batched: L = C = Lc = N, one block per image)
+  const int lgL = SLAB ? __ffs(a.lines_per_img) - 1 : LOG2N;
+  const int lgC = SLAB ? __ffs(a.in_chunk) - 1 : LOG2N;
+  const int lgLc = SLAB ? __ffs(a.out_chunk) - 1 : LOG2N;
+  const int L = 1 << lgL, C = 1 << lgC, Lc = 1 << lgLc;
+  const long long npairs = a.n_lines / 2;                 // this launch: local lines line_base + [0, n_lines)
+  const long long ncl = gridDim.x / 2;
+  const long long cl = blockIdx.x / 2;
+  const cpx<float>* __restrict__ in = reinterpret_cast<const cpx<float>*>(a.in);
+  uint64_t rx;   // the partner's staging buffer (DSMEM)
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(rx) : "l"(reinterpret_cast<uint64_t>(xraw)), "r"(c ^ 1u));
+  const cpx<float>* pbuf = reinterpret_cast<const cpx<float>*>(rx);
+
+  // thread 0: line a.line_base + 2p + c into the landing buffer
+  auto issue_load = [&](long long p) {
+    const long long line = a.line_base + 2 * p + c;
+    mbar_expect_tx(bar, (uint32_t)(N * sizeof(cpx<float>)));
+    if constexpr (ModeIO<MODE>::kUserIn) {   // the user's row (batched and slab: row-major lines)
+      bulk_g2s(land, in + line * N, (uint32_t)(N * sizeof(cpx<float>)), bar);
+    } else {                                 // Q16: 16-byte pieces of this line, chunk by chunk
+      const long long img = line >> lgL;
+      const int ll = (int)(line & (L - 1));
+      const int nck = N >> lgC, half = C >> 1, rows = half < 256 ? half : 256;
+      for (int k = 0; k < nck; ++k)
+        for (int r0 = 0; r0 < half; r0 += rows)
+          tensor_g2s_5d(land + k * C + 2 * r0, &imap, bar, 0, ll & 1, r0, ll >> 1, (int)(img * nck + k));
+    }
+  };
+
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  cluster_sync_all();   // barrier initialised; the partner's shared memory is live (DSMEM)
+  if (tid == 0 && cl < npairs) issue_load(cl);
+  TwLazy<LOG2N> tws{reinterpret_cast<const cpx<float>*>(a.tw), j};
+  using Ex = typename std::conditional<Cfg::SPLIT, ExSplit, ExPad<float>>::type;
+  Ex ex;
+  if constexpr (Cfg::SPLIT)
+    ex = ExSplit{reinterpret_cast<float*>(xraw)};
+  else
+    ex = ExPad<float>{reinterpret_cast<cpx<float>*>(xraw)};
+  uint32_t phase = 0;
+  for (long long p = cl; p < npairs; p += ncl) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    if constexpr (ModeIO<MODE>::kStraightOut)   // in place (batched K5): both loads of this pair are
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");   // complete before any store
+    cpx<float> v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = land[j + TL * e];
+    __syncthreads();   // the landing buffer is free
+    if (tid == 0 && p + ncl < npairs) {
+      fence_proxy_async_smem();
+      issue_load(p + ncl);
+    }
+    const long long line = a.line_base + 2 * p + c;
+    const long long img = line >> lgL;
+    const int ll = (int)(line & (L - 1));
+    const int l = a.line_offset + ll;
+    pass_body<float, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ex);
+
+    cpx<float>* out = reinterpret_cast<cpx<float>*>(a.out);
+    if constexpr (ModeIO<MODE>::kStraightOut) {
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+      cpx<float>* dst = out + line * N;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
+    } else {
+      cpx<float>* sb = reinterpret_cast<cpx<float>*>(xraw);
+      const int l0 = ll & ~1;                       // the pair's even line (local)
+      constexpr int EPR = 16 / ROUNDS;              // staged slots per round
+      constexpr int QR = N / (2 * ROUNDS);          // element pairs (i, i+1) per round
+#pragma unroll
+      for (int h = 0; h < ROUNDS; ++h) {
+        __syncthreads();   // the exchange buffer's last reads (FFT / previous round) are done
+#pragma unroll
+        for (int e = 0; e < EPR; ++e) sb[j + TL * e] = v[h * EPR + e];
+        cluster_sync_all();   // both CTAs' halves staged
+        for (int t = tid; t < QR / 2; t += THREADS) {
+          const int q = h * QR + (int)c * (QR / 2) + t;   // element pair of the whole line
+          const int i = 2 * q;
+          const int si = i - h * (N / ROUNDS);
+          const float4 mine = *reinterpret_cast<const float4*>(sb + si);
+          float4 part;
+          asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(part.x), "=f"(part.y), "=f"(part.z), "=f"(part.w)
+                       : "l"(reinterpret_cast<uint64_t>(pbuf + si)));
+          const float4 e0 = c ? part : mine;   // line l0: elements i, i+1
+          const float4 e1 = c ? mine : part;   // line l0 + 1
+          cpx<float>* d;
+          if constexpr (SLAB) {
+            const int s = i >> lgL, lam = i & (L - 1);
+            cpx<float>* base = a.peer_on ? reinterpret_cast<cpx<float>*>(a.peer_out[s]) + (long long)a.peer_rank * L * L
+                                         : out + (long long)s * L * L;
+            d = base + ((long long)(l0 >> lgLc) << (lgL + lgLc)) + (long long)(lam >> 1) * 2 * Lc +
+                ((l0 & (Lc - 1)) >> 1) * 4;
+          } else {
+            d = out + img * (long long)N * N + (long long)(i >> 1) * 2 * N + (l0 >> 1) * 4;
+          }
+          reinterpret_cast<float4*>(d)[0] = make_float4(e0.x, e0.y, e1.x, e1.y);
+          reinterpret_cast<float4*>(d)[1] = make_float4(e0.z, e0.w, e1.z, e1.w);
+        }
+        cluster_sync_relaxed();   // the partner has read this CTA's staging
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // Fully on-chip small-N transform.  One CTA -- or a thread-block
 // cluster of C CTAs sharing their shared memory (DSMEM) -- holds one image and runs every
 // pass of the schedule on it, so the image crosses HBM once each way instead of once per
@@ -1677,39 +1955,48 @@ struct B0Args {
   int in_off;         // input sample (r, c) sits at (r + in_off, c + in_off) of the grid
 };
 
+// One CTA per output row (image img, row i): the row's fp64 terms, chirp row polynomial and
+// image base are computed once per CTA, and the threads stride the row's n outputs -- no
+// 64-bit index divisions per output (the one-thread-per-output version spent most of its
+// instructions on them: 28% of the HBM roofline at C3).  Same arithmetic per output as
+// the plain formula (p1 = d11 p + d21 q with separately rounded products, no FMA).
 template <typename T>
 __global__ void __launch_bounds__(256) b0_kernel(B0Args a) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= a.total) return;
   const int n = a.n, h = n / 2;
-  const long long nn = (long long)n * n;
-  const long long img = idx / nn;
-  const int i = (int)((idx % nn) / n);
-  const int jj = (int)(idx % n);
-  const double p = (double)(i - h), q = (double)(jj - h);
-  const double p1 = __dadd_rn(__dmul_rn(a.d11, p), __dmul_rn(a.d21, q));
-  const double q1 = __dadd_rn(__dmul_rn(a.d12, p), __dmul_rn(a.d22, q));
-  const double p2 = floor(p1), q2 = floor(q1);
-  const double kk = p1 - p2, lw = q1 - q2;
+  const long long row = blockIdx.x;                 // img * n + i
+  const long long img = row / n;
+  const int i = (int)(row - img * n);
+  const double p = (double)(i - h);
+  const double dp1 = __dmul_rn(a.d11, p), dq1 = __dmul_rn(a.d12, p);
   const long long nin = a.n_in;
   const cpx<T>* __restrict__ g = reinterpret_cast<const cpx<T>*>(a.in) + img * nin * nin;
-  const long long ia = (long long)p2 + h - a.in_off, ja = (long long)q2 + h - a.in_off;
+  cpx<T>* __restrict__ orow = reinterpret_cast<cpx<T>*>(a.out) + row * n;
+  const uint64_t ui = (uint64_t)i;
+  const uint64_t trow = a.ph.cA * ui * ui + a.ph.cL * ui + a.ph.cK;   // t = trow + tlin j + cC j^2
+  const uint64_t tlin = a.ph.cB * ui + a.ph.cE;
+  const cpx<T> amp = {(T)a.amp_re, (T)a.amp_im};
   auto tap = [&](long long r, long long c) -> cpx<T> {
     if (r < 0 || r >= nin || c < 0 || c >= nin) return {T(0), T(0)};
     return g[r * nin + c];
   };
-  const cpx<T> g00 = tap(ia, ja), g01 = tap(ia, ja + 1), g10 = tap(ia + 1, ja), g11 = tap(ia + 1, ja + 1);
-  const T w00 = (T)((1.0 - kk) * (1.0 - lw)), w01 = (T)((1.0 - kk) * lw);
-  const T w10 = (T)(kk * (1.0 - lw)), w11 = (T)(kk * lw);
-  cpx<T> s;
-  s.x = w00 * g00.x + w01 * g01.x + w10 * g10.x + w11 * g11.x;
-  s.y = w00 * g00.y + w01 * g01.y + w10 * g10.y + w11 * g11.y;
-  const uint64_t ui = (uint64_t)i, uj = (uint64_t)jj;
-  const uint64_t t = a.ph.cA * ui * ui + a.ph.cB * ui * uj + a.ph.cC * uj * uj + a.ph.cL * ui +
-                     a.ph.cE * uj + a.ph.cK;
-  const cpx<T> c = chirp_of<T>(t, T(1));
-  const cpx<T> amp = {(T)a.amp_re, (T)a.amp_im};
-  reinterpret_cast<cpx<T>*>(a.out)[idx] = cmul(amp, cmul(c, s));
+  for (int jj = threadIdx.x; jj < n; jj += blockDim.x) {
+    const double q = (double)(jj - h);
+    const double p1 = __dadd_rn(dp1, __dmul_rn(a.d21, q));
+    const double q1 = __dadd_rn(dq1, __dmul_rn(a.d22, q));
+    const double p2 = floor(p1), q2 = floor(q1);
+    const double kk = p1 - p2, lw = q1 - q2;
+    const long long ia = (long long)p2 + h - a.in_off, ja = (long long)q2 + h - a.in_off;
+    const cpx<T> g00 = tap(ia, ja), g01 = tap(ia, ja + 1), g10 = tap(ia + 1, ja), g11 = tap(ia + 1, ja + 1);
+    const T w00 = (T)((1.0 - kk) * (1.0 - lw)), w01 = (T)((1.0 - kk) * lw);
+    const T w10 = (T)(kk * (1.0 - lw)), w11 = (T)(kk * lw);
+    cpx<T> s;
+    s.x = w00 * g00.x + w01 * g01.x + w10 * g10.x + w11 * g11.x;
+    s.y = w00 * g00.y + w01 * g01.y + w10 * g10.y + w11 * g11.y;
+    const uint64_t uj = (uint64_t)jj;
+    const uint64_t t = trow + tlin * uj + a.ph.cC * uj * uj;
+    const cpx<T> c = chirp_of<T>(t, T(1));
+    orow[jj] = cmul(amp, cmul(c, s));
+  }
 }
 
 // ---------------------------------------------------------------------------------

@@ -97,6 +97,44 @@ struct PairRow {
   }
 };
 
+// large-N TMA-pipelined kernels (N = 8192, 16384, complex64): 2-CTA clusters, persistent
+template <int LOG2N, int MODE, bool SLAB>
+cudaError_t launch_big(const PassArgs& a, cudaStream_t s, const CUtensorMap& map) {
+  using Cfg = nslct::BigCfg<LOG2N>;
+  cudaLaunchConfig_t cfg = {};
+  long long grid = a.persist_ctas > 0 ? a.persist_ctas : a.n_lines;
+  if (grid > a.n_lines) grid = a.n_lines;
+  grid &= ~1ll;
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, nslct::line_pass_big_kernel<LOG2N, MODE, SLAB>, a, map);
+}
+template <int LOG2N, int MODE, bool SLAB>
+cudaError_t set_attr_big() {
+  return cudaFuncSetAttribute(nslct::line_pass_big_kernel<LOG2N, MODE, SLAB>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nslct::BigCfg<LOG2N>::SMEM);
+}
+typedef cudaError_t (*big_fn)(const PassArgs&, cudaStream_t, const CUtensorMap&);
+template <int LOG2N, bool SLAB>
+struct BigRow {
+  static void fill(big_fn* l, attr_fn* at) {
+    l[0] = launch_big<LOG2N, 0, SLAB>; l[1] = launch_big<LOG2N, 1, SLAB>; l[2] = launch_big<LOG2N, 2, SLAB>;
+    l[3] = launch_big<LOG2N, 3, SLAB>; l[4] = launch_big<LOG2N, 4, SLAB>; l[5] = launch_big<LOG2N, 5, SLAB>;
+    at[0] = set_attr_big<LOG2N, 0, SLAB>; at[1] = set_attr_big<LOG2N, 1, SLAB>;
+    at[2] = set_attr_big<LOG2N, 2, SLAB>; at[3] = set_attr_big<LOG2N, 3, SLAB>;
+    at[4] = set_attr_big<LOG2N, 4, SLAB>; at[5] = set_attr_big<LOG2N, 5, SLAB>;
+  }
+};
+
 // persistent TMA-pipelined variant: grid = #SMs (one CTA per SM)
 constexpr size_t kPipeExtra = 64;   // 3 mbarriers + 3 claimed-group slots + TMEM base
 template <typename T, int LOG2N, int MODE>
@@ -184,6 +222,25 @@ nslct_status make_store_map(CUtensorMap* m, void* out, int log2n, long long imag
   return NSLCT_OK;
 }
 
+// Tensor map of a large-N pass's Q16 input (kernels.cuh line_pass_big_kernel): 5D view
+// {16 B piece (4 floats), line parity (16 B), mu pair (32 B), line pair (2C elements),
+// chunk / image (L C elements)} of `images` blocks of L lines x N elements in chunks of C;
+// box = one 16-byte piece x up to 256 mu pairs.
+nslct_status make_q16_map(CUtensorMap* m, const void* in, int log2n, long long L, long long C, long long images) {
+  auto fn = encode_tiled();
+  if (!fn) return fail(NSLCT_E_CUDA, "cuTensorMapEncodeTiled entry point not available");
+  const cuuint64_t n = 1ull << log2n;
+  const cuuint64_t dims[5] = {4, 2, (cuuint64_t)C / 2, (cuuint64_t)L / 2, (n / (cuuint64_t)C) * (cuuint64_t)images};
+  const cuuint64_t strides[4] = {16, 32, (cuuint64_t)C * 16, (cuuint64_t)(L * C) * 8};
+  const cuuint32_t box[5] = {4, 1, (cuuint32_t)(C / 2 < 256 ? C / 2 : 256), 1, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void*>(in), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NSLCT_E_CUDA, "cuTensorMapEncodeTiled (Q16) failed (" + std::to_string((int)r) + ")");
+  return NSLCT_OK;
+}
+
 constexpr int kModes = 6;   // pass modes 0..5 (kernels.cuh pass_body)
 
 // the non-warp-specialised pipe kernel runs the passes that read the user's input (modes
@@ -257,6 +314,8 @@ struct Table {
   attr_fn at[2][kMaxLog + 1][kModes] = {};
   launch_fn lpair[2][kMaxLog + 1][kModes] = {};   // c64 N = 8192, 16384 (cluster pairs): [slab]
   attr_fn atpair[2][kMaxLog + 1][kModes] = {};
+  big_fn lbig[2][kMaxLog + 1][kModes] = {};     // c64 N = 8192, 16384 (TMA-pipelined): [slab]
+  attr_fn atbig[2][kMaxLog + 1][kModes] = {};
   pipe_fn lp[kMaxLog + 1][kModes] = {};   // c64 only
   attr_fn atp[kMaxLog + 1][kModes] = {};
   Table() {
@@ -271,6 +330,10 @@ struct Table {
     PairRow<14, false>::fill(lpair[0][14], atpair[0][14]);
     PairRow<13, true>::fill(lpair[1][13], atpair[1][13]);
     PairRow<14, true>::fill(lpair[1][14], atpair[1][14]);
+    BigRow<13, false>::fill(lbig[0][13], atbig[0][13]);
+    BigRow<14, false>::fill(lbig[0][14], atbig[0][14]);
+    BigRow<13, true>::fill(lbig[1][13], atbig[1][13]);
+    BigRow<14, true>::fill(lbig[1][14], atbig[1][14]);
     PipeRow<float, 10>::fill(lp[10], atp[10]);
     PipeRow<float, 11>::fill(lp[11], atp[11]);
     PipeRow<float, 12>::fill(lp[12], atp[12]);
@@ -469,7 +532,8 @@ struct nslct_plan_s {
   bool pipe = false;   // persistent TMA-pipelined kernels
   bool image = false;  // fully on-chip kernel (one launch per exec)
   bool ws = false;     // warp-specialised pipe kernels for modes 1-3
-  bool pair = false;   // large-N cluster-pair line passes (N = 8192, 16384, complex64)
+  bool pair = false;   // large-N cluster-pair line passes, one-line loads (opts.kernels = 2, A/B only)
+  bool big = false;    // large-N TMA-pipelined cluster-pair passes (N = 8192, 16384, complex64)
   unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
   int num_sms = 148;
   int host_chunk_kb = 0;    // opts.host_chunk_kb (exec_host pipeline chunk; 0 = auto)
@@ -717,6 +781,7 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
   if (batch < 1) return fail(NSLCT_E_ARG, "batch must be >= 1");
   if (o.variant < 0 || o.variant > 3 || o.dispatch < 0 || o.dispatch > 1 || o.schedule < 0 || o.schedule > 2)
     return fail(NSLCT_E_ARG, "bad variant/dispatch option");
+  if (o.kernels < 0 || o.kernels > NSLCT_KERNELS_PAIR_V1) return fail(NSLCT_E_ARG, "bad kernels option");
   int lg = 0;
   while ((int64_t(1) << lg) < n && lg < 62) ++lg;
   const bool pow2 = n >= 1 && (int64_t(1) << lg) == n && lg >= kMinLog && lg <= kMaxLog &&
@@ -1056,12 +1121,14 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
           set_rec(&pl->args[k].ph_c, tl);
         }
       }
-      pl->pair = plain && special && ti == 0 && (lg == 13 || lg == 14) && (L % 2 == 0);
-      for (int k = 0; k < 5 && pl->pair; ++k) pl->args[k].persist_ctas = (pl->num_sms / 2) * 2;
-      for (int m = 0; m < kModes && pl->pair; ++m) {
-        cudaError_t e = table().atpair[slab ? 1 : 0][lg][m]();
+      const bool large = plain && ti == 0 && (lg == 13 || lg == 14) && (L % 2 == 0) && (Lc % 16 == 0);
+      pl->big = large && special;
+      pl->pair = large && o.kernels == NSLCT_KERNELS_PAIR_V1;
+      for (int k = 0; k < 5 && (pl->pair || pl->big); ++k) pl->args[k].persist_ctas = (pl->num_sms / 2) * 2;
+      for (int m = 0; m < kModes && (pl->pair || pl->big); ++m) {
+        cudaError_t e = pl->big ? table().atbig[slab ? 1 : 0][lg][m]() : table().atpair[slab ? 1 : 0][lg][m]();
         if (e != cudaSuccess) {
-          result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(pair): ") + cudaGetErrorString(e));
+          result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(large N): ") + cudaGetErrorString(e));
           break;
         }
       }
@@ -1133,6 +1200,8 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
   return NSLCT_OK;
 }
 
+static nslct_status launch_large(nslct_plan_t pl, int k, const PassArgs& a, cudaStream_t s);
+
 // one pipe pass: the transposed passes get the tensor map of their output
 static nslct_status launch_pipe_pass(nslct_plan_t pl, int k, const PassArgs& a, cudaStream_t s) {
   const int m = pl->mode[k];
@@ -1170,7 +1239,7 @@ static nslct_status run_images(nslct_plan_t pl, const void* in, void* out, int64
     b.in = in;
     b.out = out;
     b.total = nimg * pl->n * pl->n;
-    const long long blocks = (b.total + 255) / 256;
+    const long long blocks = nimg * pl->n;   // one CTA per output row
     if (in == out) return fail(NSLCT_E_ARG, "the B = 0 gather cannot run in place");
     if (ev) CUDA_TRY(cudaEventRecord(ev[0], s));
     if (ti == 0)
@@ -1274,8 +1343,9 @@ static nslct_status run_images(nslct_plan_t pl, const void* in, void* out, int64
     if (pl->pipe) {
       nslct_status st = launch_pipe_pass(pl, k, a, s);
       if (st != NSLCT_OK) return st;
-    } else if (pl->pair) {
-      CUDA_TRY(table().lpair[pl->slab ? 1 : 0][pl->log2n][pl->mode[k]](a, s));
+    } else if (pl->pair || pl->big) {
+      nslct_status st = launch_large(pl, k, a, s);
+      if (st != NSLCT_OK) return st;
     } else {
       CUDA_TRY(table().l[ti][pl->log2n][pl->mode[k]](a, s));
     }
@@ -1288,14 +1358,33 @@ static nslct_status run_images(nslct_plan_t pl, const void* in, void* out, int64
   return NSLCT_OK;
 }
 
+// One launch of pass k with the large-N kernels (batched or slab): the TMA-pipelined
+// kernel gets the tensor map of its Q16 input (not for the passes reading user rows).
+static nslct_status launch_large(nslct_plan_t pl, int k, const PassArgs& a, cudaStream_t s) {
+  const int sl = pl->slab ? 1 : 0, m = pl->mode[k];
+  if (!pl->big) {
+    CUDA_TRY(table().lpair[sl][pl->log2n][m](a, s));
+    return NSLCT_OK;
+  }
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  if (!(m == 0 || m == 4)) {
+    const long long L = pl->slab ? pl->L : pl->n;
+    const long long C = pl->slab ? a.in_chunk : pl->n;
+    const long long images = pl->slab ? 1 : a.n_lines / pl->n;
+    nslct_status st = make_q16_map(&map, a.in, pl->log2n, L, C, images);
+    if (st != NSLCT_OK) return st;
+  }
+  CUDA_TRY(table().lbig[sl][pl->log2n][m](a, s, map));
+  return NSLCT_OK;
+}
+
 // One launch of pass k of a slab plan (the cluster-pair kernels at N = 8192 / 16384 c64,
 // else the generic line pass), over local lines a.line_base + [0, a.n_lines).
 static nslct_status launch_slab_pass(nslct_plan_t pl, int k, const PassArgs& a, cudaStream_t s) {
   const int ti = (pl->dtype == NSLCT_C64) ? 0 : 1;
-  if (pl->pair)
-    CUDA_TRY(table().lpair[1][pl->log2n][pl->mode[k]](a, s));
-  else
-    CUDA_TRY(table().l[ti][pl->log2n][pl->mode[k]](a, s));
+  if (pl->pair || pl->big) return launch_large(pl, k, a, s);
+  CUDA_TRY(table().l[ti][pl->log2n][pl->mode[k]](a, s));
   return NSLCT_OK;
 }
 
@@ -1417,8 +1506,8 @@ nslct_status nslct_exec_pass(nslct_plan_t pl, int pass, const void* in, void* ou
     CUDA_TRY(cudaMemsetAsync(pl->counters + pass, 0, sizeof(unsigned long long), s));
     nslct_status st = launch_pipe_pass(pl, pass, a, s);
     if (st != NSLCT_OK) return st;
-  } else if (pl->pair) {
-    CUDA_TRY(table().lpair[pl->slab ? 1 : 0][pl->log2n][pl->mode[pass]](a, s));
+  } else if (pl->pair || pl->big) {
+    return launch_large(pl, pass, a, s);
   } else {
     CUDA_TRY(table().l[ti][pl->log2n][pl->mode[pass]](a, s));
   }
@@ -1515,10 +1604,8 @@ nslct_status nslct_exec_pass_peer(nslct_plan_t pl, int pass, const void* in, voi
   a.peer_on = 1;
   a.peer_rank = pl->rank;
   for (int r = 0; r < n_peers; ++r) a.peer_out[r] = peer_out[r];
-  if (pl->pair)
-    CUDA_TRY(table().lpair[pl->slab ? 1 : 0][pl->log2n][pl->mode[pass]](a, s));
-  else
-    CUDA_TRY(table().l[ti][pl->log2n][pl->mode[pass]](a, s));
+  if (pl->pair || pl->big) return launch_large(pl, pass, a, s);
+  CUDA_TRY(table().l[ti][pl->log2n][pl->mode[pass]](a, s));
   return NSLCT_OK;
 }
 
