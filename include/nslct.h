@@ -116,10 +116,12 @@ enum { NSLCT_KERNELS_AUTO = 0,     /* the specialised kernels where they exist: 
                                       TMA pipe (c64, N = 1024..4096), cluster pairs (c64,
                                       N = 8192, 16384), on-chip (see schedule)              */
        NSLCT_KERNELS_GENERIC = 1,  /* one CTA per group of lines everywhere (A/B reference)  */
-       NSLCT_KERNELS_PAIR_V1 = 2   /* as AUTO, but N = 8192 / 16384 c64 with the round-1
+       NSLCT_KERNELS_PAIR_V1 = 2,  /* as AUTO, but N = 8192 / 16384 c64 with the round-1
                                       cluster-pair kernels (per-thread loads, pair-interleaved
                                       intermediates): A/B reference of the TMA-pipelined
                                       large-N kernels                                       */
+       NSLCT_KERNELS_BIG_NOLAND = 3 /* as AUTO, but the large-N kernels load each line into the
+                                      exchange buffer (from L2) instead of a landing buffer  */
 };
 /* schedules of a batched plan (all compute the same operator) */
 enum { NSLCT_SCHEDULE_AUTO = 0,        /* the on-chip kernel for N <= 64 (measured faster at

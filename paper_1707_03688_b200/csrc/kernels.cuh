@@ -1661,15 +1661,17 @@ line_pass_pair_kernel(PassArgs a) {
 //     both fit only with the two-round (real / imaginary) exchange (ExSplit);
 //   * twiddle bases per stage loaded lazily (TwLazy): 64 registers at 1024 threads.
 // ---------------------------------------------------------------------------------
-template <int LOG2N>
+template <int LOG2N, bool LAND = true>
 struct BigCfg {
   static constexpr int N = 1 << LOG2N;
   static constexpr int TL = N / 16;
   static constexpr int THREADS = TL;                      // one line per CTA
-  static constexpr bool SPLIT = (LOG2N >= 14);
+  // LAND: the next line lands in its own buffer while this one computes; else it is loaded
+  // (from L2, prefetched one iteration ahead) into the exchange buffer between lines
+  static constexpr bool SPLIT = LAND && (LOG2N >= 14);
   static constexpr int XELEMS = N + N / 16 + 16;         // padded exchange index i + i/16
   static constexpr size_t XBYTES = (size_t)XELEMS * (SPLIT ? 4 : 8);
-  static constexpr size_t LBYTES = (size_t)N * 8;         // landing buffer: one line
+  static constexpr size_t LBYTES = LAND ? (size_t)N * 8 : 0;   // landing buffer: one line
   static constexpr int ROUNDS = SPLIT ? 2 : 1;            // output staging rounds
   static constexpr size_t SMEM = LBYTES + XBYTES + 64;
   static_assert((size_t)(N / ROUNDS) * 8 <= XBYTES, "staging fits the exchange buffer");
@@ -1690,14 +1692,14 @@ __device__ __forceinline__ void cluster_sync_relaxed() {
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 
-template <int LOG2N, int MODE, bool SLAB>
-__global__ void __launch_bounds__(BigCfg<LOG2N>::THREADS, 1)
+template <int LOG2N, int MODE, bool SLAB, bool LAND>
+__global__ void __launch_bounds__(BigCfg<LOG2N, LAND>::THREADS, 1)
 line_pass_big_kernel(PassArgs a, const __grid_constant__ CUtensorMap imap) {
-  using Cfg = BigCfg<LOG2N>;
+  using Cfg = BigCfg<LOG2N, LAND>;
   constexpr int N = Cfg::N, TL = Cfg::TL, THREADS = Cfg::THREADS, ROUNDS = Cfg::ROUNDS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  cpx<float>* land = reinterpret_cast<cpx<float>*>(smem_raw);
   unsigned char* xraw = smem_raw + Cfg::LBYTES;
+  cpx<float>* land = reinterpret_cast<cpx<float>*>(LAND ? smem_raw : xraw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + Cfg::LBYTES + Cfg::XBYTES);
   uint32_t c;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c));
@@ -1732,6 +1734,20 @@ line_pass_big_kernel(PassArgs a, const __grid_constant__ CUtensorMap imap) {
     }
   };
 
+  // !LAND: the next line's input (this CTA's part of the pair block) into L2
+  auto prefetch_l2 = [&](long long p) {
+    const long long line = a.line_base + 2 * p + c;
+    if constexpr (ModeIO<MODE>::kUserIn) {
+      bulk_prefetch_l2(in + line * N, (uint32_t)(N * sizeof(cpx<float>)));
+    } else {
+      const long long img = line >> lgL;
+      const int ll = (int)(line & (L - 1));
+      const int nck = N >> lgC;
+      for (int k = 0; k < nck; ++k)
+        bulk_prefetch_l2(in + ((img * nck + k) << (lgL + lgC)) + (long long)(ll >> 1) * 2 * C + (long long)c * C,
+                         (uint32_t)(C * sizeof(cpx<float>)));
+    }
+  };
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -1756,8 +1772,12 @@ line_pass_big_kernel(PassArgs a, const __grid_constant__ CUtensorMap imap) {
     for (int e = 0; e < 16; ++e) v[e] = land[j + TL * e];
     __syncthreads();   // the landing buffer is free
     if (tid == 0 && p + ncl < npairs) {
-      fence_proxy_async_smem();
-      issue_load(p + ncl);
+      if constexpr (LAND) {
+        fence_proxy_async_smem();
+        issue_load(p + ncl);
+      } else {
+        prefetch_l2(p + ncl);
+      }
     }
     const long long line = a.line_base + 2 * p + c;
     const long long img = line >> lgL;
@@ -1807,6 +1827,13 @@ line_pass_big_kernel(PassArgs a, const __grid_constant__ CUtensorMap imap) {
           reinterpret_cast<float4*>(d)[1] = make_float4(e0.z, e0.w, e1.z, e1.w);
         }
         cluster_sync_relaxed();   // the partner has read this CTA's staging
+      }
+    }
+    if constexpr (!LAND) {   // the exchange buffer is free: bring in the next line (from L2)
+      __syncthreads();
+      if (tid == 0 && p + ncl < npairs) {
+        fence_proxy_async_smem();
+        issue_load(p + ncl);
       }
     }
   }

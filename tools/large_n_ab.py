@@ -40,7 +40,7 @@ def run(n, batch, kernels, reps=10):
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 ref = None
-for k in ("auto", "pair_v1"):
+for k in ("auto", "big_noland", "pair_v1"):
     r, out = run(n, batch, k)
     if ref is None:
         ref = out.clone()
