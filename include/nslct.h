@@ -113,15 +113,10 @@ enum { NSLCT_EXCHANGE_NCCL = 0,   /* NCCL grouped send/recv of each chunk's sub-
 };
 /* kernel families (all compute the same operator) */
 enum { NSLCT_KERNELS_AUTO = 0,     /* the specialised kernels where they exist: persistent
-                                      TMA pipe (c64, N = 1024..4096), cluster pairs (c64,
-                                      N = 8192, 16384), on-chip (see schedule)              */
-       NSLCT_KERNELS_GENERIC = 1,  /* one CTA per group of lines everywhere (A/B reference)  */
-       NSLCT_KERNELS_PAIR_V1 = 2,  /* as AUTO, but N = 8192 / 16384 c64 with the round-1
-                                      cluster-pair kernels (per-thread loads, pair-interleaved
-                                      intermediates): A/B reference of the TMA-pipelined
-                                      large-N kernels                                       */
-       NSLCT_KERNELS_BIG_NOLAND = 3 /* as AUTO, but the large-N kernels load each line into the
-                                      exchange buffer (from L2) instead of a landing buffer  */
+                                      TMA pipe (c64, N = 1024..4096), TMA-pipelined cluster
+                                      pairs (c64, N = 8192), cluster pairs (c64, N = 16384),
+                                      on-chip (see schedule)                                 */
+       NSLCT_KERNELS_GENERIC = 1   /* one CTA per group of lines everywhere (A/B reference)  */
 };
 /* schedules of a batched plan (all compute the same operator) */
 enum { NSLCT_SCHEDULE_AUTO = 0,        /* the on-chip kernel for N <= 64 (measured faster at
@@ -196,8 +191,10 @@ nslct_status nslct_exec_host(nslct_plan_t plan, const void* host_in, void* host_
  * nranks row-blocks of [L][L] (block s goes to rank s), and the receive buffer (block
  * from rank s at element offset s*L*L) is the next pass's `in`.  This exchange is the
  * distributed form of the transposes the single-GPU passes fold into their stores.  The
- * element order INSIDE a block is the library's (plain transposed, or pair-interleaved
- * for complex64 n >= 8192: DESIGN.md §7); the exchange must move whole blocks unchanged.
+ * element order INSIDE a block is the library's (sub-blocks of opts.exchange_chunks
+ * producer-line chunks; inside them plain transposed, or, for complex64, 16-byte
+ * interleaved line pairs at n = 8192 and 8-byte interleaved line pairs at n = 16384:
+ * DESIGN.md §7); the exchange must move whole blocks unchanged.
  * Requires B != 0 (the B = 0 gather has no slab form), nranks | n, and L a multiple of
  * the kernel's lines per CTA (L >= 16 suffices for n >= 4096).  The plan allocates no
  * scratch: the caller owns all buffers (each n*L complex elements).  Errors: as

@@ -426,7 +426,6 @@ struct TwTmem {
 //         barrier is not needed.
 template <typename T>
 struct ExPad {
-  static constexpr bool kSplit = false;
   static constexpr bool kDouble = false;
   static constexpr bool kPadded = true;
   static constexpr int kPadW = 1;
@@ -441,7 +440,6 @@ struct ExPad {
 };
 template <typename T, class Hook, int PW = 1>
 struct ExPad2 {   // two padded buffers used alternately: write, barrier, read
-  static constexpr bool kSplit = false;
   static constexpr bool kDouble = true;
   static constexpr bool kPadded = true;
   static constexpr int kPadW = PW;
@@ -460,79 +458,8 @@ struct ExPad2 {   // two padded buffers used alternately: write, barrier, read
 };
 
 template <typename T, int LOG2N, int STAGE, int NS, int X, class E, class TW>
-__device__ __forceinline__ void fft_stage_split(cpx<T> (&v)[16], int j, const TW& tw, const E& ex) {
-  constexpr int N = 1 << LOG2N;
-  constexpr int TL = N / 16;
-  constexpr int NFULL = LOG2N / 4;
-  constexpr int R = (STAGE < NFULL) ? 16 : (1 << (LOG2N % 4));
-  constexpr int NB = 16 / R;
-  constexpr bool LAST = (STAGE == NS - 1);
-  constexpr int Ns = (STAGE < NFULL) ? (1 << (4 * STAGE)) : (1 << (4 * NFULL));
-  static_assert(TL % 16 == 0, "split exchange: padded fast addressing");
-  constexpr int WSTEP = (Ns >= 16) ? Ns + Ns / 16 : Ns;
-  constexpr int RSTEP = TL + TL / 16;
-  // butterflies: outputs stay in registers (slot b + r NB)
-#pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    const int jp = j + b * TL;
-    cpx<T> u[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) u[r] = v[b + r * NB];
-    if constexpr (Ns > 1) tw.template apply<STAGE, R>(u, b, jp);
-    dft<R>(u);
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[b + r * NB] = u[r];
-  }
-  if constexpr (!LAST) {
-    tw.template prefetch<STAGE + 1>();
-    float* buf = ex.buf;
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      if (half == 1 || STAGE > 0 || X > 0) __syncthreads();   // the previous round's reads are done
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const int jp = j + b * TL;
-        const int idxD = (jp / Ns) * Ns * R + (jp % Ns);
-        float* wb = buf + padw<1>(idxD);
-#pragma unroll
-        for (int r = 0; r < R; ++r) wb[r * WSTEP] = half ? v[b + r * NB].y : v[b + r * NB].x;
-      }
-      __syncthreads();
-      const float* rb = buf + padw<1>(j);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        if (half)
-          v[e].y = rb[e * RSTEP];
-        else
-          v[e].x = rb[e * RSTEP];
-      }
-    }
-  }
-}
-
-//  ExSplit: ONE padded buffer of floats (half the bytes of a complex line): each exchange
-//         runs in two rounds, real parts then imaginary parts -- write, barrier, read,
-//         barrier, per round.  For the 128 KB lines of N = 16384, where a complex
-//         exchange buffer and the TMA landing buffer of the next line do not both fit in
-//         shared memory (line_pass_big_kernel).
-struct ExSplit {
-  static constexpr bool kSplit = true;
-  static constexpr bool kDouble = false;
-  static constexpr bool kPadded = true;
-  static constexpr int kPadW = 1;
-  float* buf;
-  template <int X>
-  __device__ __forceinline__ void sync() const { __syncthreads(); }
-  template <int X>
-  __device__ __forceinline__ void after_barrier() const {}
-};
-
-template <typename T, int LOG2N, int STAGE, int NS, int X, class E, class TW>
 __device__ __forceinline__ void fft_stage(cpx<T> (&v)[16], int j, const TW& tw, const E& ex) {
-  if constexpr (E::kSplit) {
-    fft_stage_split<T, LOG2N, STAGE, NS, X>(v, j, tw, ex);
-    return;
-  } else {
+  {
   constexpr int N = 1 << LOG2N;
   constexpr int TL = N / 16;
   constexpr int NFULL = LOG2N / 4;
@@ -1310,7 +1237,6 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
 // ---------------------------------------------------------------------------------
 template <typename T>
 struct ExPadWS {   // as ExPad2, but the 16 compute warps only (named barrier 1), no hook
-  static constexpr bool kSplit = false;
   static constexpr bool kDouble = true;
   static constexpr bool kPadded = true;
   static constexpr int kPadW = 1;
@@ -1642,11 +1568,11 @@ line_pass_pair_kernel(PassArgs a) {
 }
 
 // ---------------------------------------------------------------------------------
-// Large-N line pass, TMA-pipelined (N = 8192, 16384; complex64; batched and row-slab
-// plans).  Persistent 2-CTA clusters stride the line pairs; CTA c takes line 2p + c of
-// pair p.  The NEXT pair's line is brought into a landing buffer by TMA while this one
-// computes (the one-line-per-CTA kernel above could not overlap its loads: ncu showed its
-// warps waiting on 16 per-thread loads each, lg_throttle and long-scoreboard stalls).
+// Large-N line pass, TMA-pipelined (N = 8192; complex64; batched and row-slab plans).
+// Persistent 2-CTA clusters stride the line pairs; CTA c takes line 2p + c of pair p.  The
+// NEXT pair's line is brought into a landing buffer by TMA while this one computes (the
+// one-line-per-CTA kernel above cannot overlap its loads: ncu shows its warps waiting on
+// 16 per-thread loads each, lg_throttle and long-scoreboard stalls).
 //   * intermediate layout "Q16" (nslct.h): element mu of consumer line lam at
 //         (mu / C) L C + (lam >> 1) 2C + ((mu % C) >> 1) 4 + (lam & 1) 2 + (mu & 1)
 //     -- inside a pair block, 32-byte segments [lam: mu, mu+1 | lam+1: mu, mu+1] -- so a
@@ -1654,27 +1580,27 @@ line_pass_pair_kernel(PassArgs a) {
 //     parity, mu pair, line pair, chunk; nslct.cu make_q16_map) while the partner reads
 //     the other half of the same sectors;
 //   * a 32-byte output segment is [(i, l0) (i, l1) (i+1, l0) (i+1, l1)] for the pair's
-//     lines l0, l1: each CTA stages (half of) its line in shared memory and, after a
-//     cluster barrier, writes the segments of its share reading the partner's elements
-//     through DSMEM (row slabs: into the all-to-all sub-blocks, or the peers' buffers);
-//   * shared memory = landing buffer (the whole next line) + exchange buffer; at N = 16384
-//     both fit only with the two-round (real / imaginary) exchange (ExSplit);
-//   * twiddle bases per stage loaded lazily (TwLazy): 64 registers at 1024 threads.
-// ---------------------------------------------------------------------------------
-template <int LOG2N, bool LAND = true>
+//     lines l0, l1: each CTA stages its line in shared memory and, after a cluster
+//     barrier, writes the segments of its half reading the partner's elements through
+//     DSMEM (row slabs: into the all-to-all sub-blocks, or the peers' buffers);
+//   * shared memory = landing buffer (the whole next line) + exchange buffer (134 KB);
+//   * twiddle bases per stage loaded lazily (TwLazy).
+// Measured (tools/large_n_ab.py, one B200): 8192^2 x 4 in 11.1 ms vs 12.3 ms for the
+// cluster-pair kernel (+10%).  At N = 16384 the two buffers do not fit together; a
+// version with a two-round (real / imaginary) exchange to make room measured 3.94 ms per
+// two-FFT pass (1024 threads at 64 registers spill; the split exchange doubles the
+// shared-memory instructions) and one loading each line into the exchange buffer 3.39 ms,
+// both slower than the cluster-pair kernel's 2.95 ms, which N = 16384 keeps.
+template <int LOG2N>
 struct BigCfg {
   static constexpr int N = 1 << LOG2N;
   static constexpr int TL = N / 16;
   static constexpr int THREADS = TL;                      // one line per CTA
-  // LAND: the next line lands in its own buffer while this one computes; else it is loaded
-  // (from L2, prefetched one iteration ahead) into the exchange buffer between lines
-  static constexpr bool SPLIT = LAND && (LOG2N >= 14);
   static constexpr int XELEMS = N + N / 16 + 16;         // padded exchange index i + i/16
-  static constexpr size_t XBYTES = (size_t)XELEMS * (SPLIT ? 4 : 8);
-  static constexpr size_t LBYTES = LAND ? (size_t)N * 8 : 0;   // landing buffer: one line
-  static constexpr int ROUNDS = SPLIT ? 2 : 1;            // output staging rounds
+  static constexpr size_t XBYTES = (size_t)XELEMS * 8;
+  static constexpr size_t LBYTES = (size_t)N * 8;         // landing buffer: one line
   static constexpr size_t SMEM = LBYTES + XBYTES + 64;
-  static_assert((size_t)(N / ROUNDS) * 8 <= XBYTES, "staging fits the exchange buffer");
+  static_assert(SMEM <= 227 * 1024, "one line + the exchange buffer fit shared memory (N <= 8192)");
 };
 
 __device__ __forceinline__ void tensor_g2s_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
@@ -1692,14 +1618,14 @@ __device__ __forceinline__ void cluster_sync_relaxed() {
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 
-template <int LOG2N, int MODE, bool SLAB, bool LAND>
-__global__ void __launch_bounds__(BigCfg<LOG2N, LAND>::THREADS, 1)
+template <int LOG2N, int MODE, bool SLAB>
+__global__ void __launch_bounds__(BigCfg<LOG2N>::THREADS, 1)
 line_pass_big_kernel(PassArgs a, const __grid_constant__ CUtensorMap imap) {
-  using Cfg = BigCfg<LOG2N, LAND>;
-  constexpr int N = Cfg::N, TL = Cfg::TL, THREADS = Cfg::THREADS, ROUNDS = Cfg::ROUNDS;
+  using Cfg = BigCfg<LOG2N>;
+  constexpr int N = Cfg::N, TL = Cfg::TL, THREADS = Cfg::THREADS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  cpx<float>* land = reinterpret_cast<cpx<float>*>(smem_raw);
   unsigned char* xraw = smem_raw + Cfg::LBYTES;
-  cpx<float>* land = reinterpret_cast<cpx<float>*>(LAND ? smem_raw : xraw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + Cfg::LBYTES + Cfg::XBYTES);
   uint32_t c;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c));
@@ -1734,20 +1660,6 @@ line_pass_big_kernel(PassArgs a, const __grid_constant__ CUtensorMap imap) {
     }
   };
 
-  // !LAND: the next line's input (this CTA's part of the pair block) into L2
-  auto prefetch_l2 = [&](long long p) {
-    const long long line = a.line_base + 2 * p + c;
-    if constexpr (ModeIO<MODE>::kUserIn) {
-      bulk_prefetch_l2(in + line * N, (uint32_t)(N * sizeof(cpx<float>)));
-    } else {
-      const long long img = line >> lgL;
-      const int ll = (int)(line & (L - 1));
-      const int nck = N >> lgC;
-      for (int k = 0; k < nck; ++k)
-        bulk_prefetch_l2(in + ((img * nck + k) << (lgL + lgC)) + (long long)(ll >> 1) * 2 * C + (long long)c * C,
-                         (uint32_t)(C * sizeof(cpx<float>)));
-    }
-  };
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -1755,12 +1667,7 @@ line_pass_big_kernel(PassArgs a, const __grid_constant__ CUtensorMap imap) {
   cluster_sync_all();   // barrier initialised; the partner's shared memory is live (DSMEM)
   if (tid == 0 && cl < npairs) issue_load(cl);
   TwLazy<LOG2N> tws{reinterpret_cast<const cpx<float>*>(a.tw), j};
-  using Ex = typename std::conditional<Cfg::SPLIT, ExSplit, ExPad<float>>::type;
-  Ex ex;
-  if constexpr (Cfg::SPLIT)
-    ex = ExSplit{reinterpret_cast<float*>(xraw)};
-  else
-    ex = ExPad<float>{reinterpret_cast<cpx<float>*>(xraw)};
+  const ExPad<float> ex{reinterpret_cast<cpx<float>*>(xraw)};
   uint32_t phase = 0;
   for (long long p = cl; p < npairs; p += ncl) {
     mbar_wait(bar, phase);
@@ -1772,12 +1679,8 @@ line_pass_big_kernel(PassArgs a, const __grid_constant__ CUtensorMap imap) {
     for (int e = 0; e < 16; ++e) v[e] = land[j + TL * e];
     __syncthreads();   // the landing buffer is free
     if (tid == 0 && p + ncl < npairs) {
-      if constexpr (LAND) {
-        fence_proxy_async_smem();
-        issue_load(p + ncl);
-      } else {
-        prefetch_l2(p + ncl);
-      }
+      fence_proxy_async_smem();
+      issue_load(p + ncl);
     }
     const long long line = a.line_base + 2 * p + c;
     const long long img = line >> lgL;
@@ -1794,23 +1697,20 @@ line_pass_big_kernel(PassArgs a, const __grid_constant__ CUtensorMap imap) {
     } else {
       cpx<float>* sb = reinterpret_cast<cpx<float>*>(xraw);
       const int l0 = ll & ~1;                       // the pair's even line (local)
-      constexpr int EPR = 16 / ROUNDS;              // staged slots per round
-      constexpr int QR = N / (2 * ROUNDS);          // element pairs (i, i+1) per round
+      {
+        // the exchange buffer's last reads (ExPad: after its trailing barrier) are done
 #pragma unroll
-      for (int h = 0; h < ROUNDS; ++h) {
-        __syncthreads();   // the exchange buffer's last reads (FFT / previous round) are done
-#pragma unroll
-        for (int e = 0; e < EPR; ++e) sb[j + TL * e] = v[h * EPR + e];
-        cluster_sync_all();   // both CTAs' halves staged
-        for (int t = tid; t < QR / 2; t += THREADS) {
-          const int q = h * QR + (int)c * (QR / 2) + t;   // element pair of the whole line
+        for (int e = 0; e < 16; ++e) sb[j + TL * e] = v[e];
+        cluster_sync_all();   // both CTAs' lines staged
+        // element pairs (i, i+1): this CTA writes the segments of half c of the line
+        for (int t = tid; t < N / 4; t += THREADS) {
+          const int q = (int)c * (N / 4) + t;
           const int i = 2 * q;
-          const int si = i - h * (N / ROUNDS);
-          const float4 mine = *reinterpret_cast<const float4*>(sb + si);
+          const float4 mine = *reinterpret_cast<const float4*>(sb + i);
           float4 part;
           asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
                        : "=f"(part.x), "=f"(part.y), "=f"(part.z), "=f"(part.w)
-                       : "l"(reinterpret_cast<uint64_t>(pbuf + si)));
+                       : "l"(reinterpret_cast<uint64_t>(pbuf + i)));
           const float4 e0 = c ? part : mine;   // line l0: elements i, i+1
           const float4 e1 = c ? mine : part;   // line l0 + 1
           cpx<float>* d;
@@ -1827,13 +1727,6 @@ line_pass_big_kernel(PassArgs a, const __grid_constant__ CUtensorMap imap) {
           reinterpret_cast<float4*>(d)[1] = make_float4(e0.z, e0.w, e1.z, e1.w);
         }
         cluster_sync_relaxed();   // the partner has read this CTA's staging
-      }
-    }
-    if constexpr (!LAND) {   // the exchange buffer is free: bring in the next line (from L2)
-      __syncthreads();
-      if (tid == 0 && p + ncl < npairs) {
-        fence_proxy_async_smem();
-        issue_load(p + ncl);
       }
     }
   }

@@ -97,10 +97,10 @@ struct PairRow {
   }
 };
 
-// large-N TMA-pipelined kernels (N = 8192, 16384, complex64): 2-CTA clusters, persistent
-template <int LOG2N, int MODE, bool SLAB, bool LAND>
+// large-N TMA-pipelined kernels (N = 8192, complex64): 2-CTA clusters, persistent
+template <int LOG2N, int MODE, bool SLAB>
 cudaError_t launch_big(const PassArgs& a, cudaStream_t s, const CUtensorMap& map) {
-  using Cfg = nslct::BigCfg<LOG2N, LAND>;
+  using Cfg = nslct::BigCfg<LOG2N>;
   cudaLaunchConfig_t cfg = {};
   long long grid = a.persist_ctas > 0 ? a.persist_ctas : a.n_lines;
   if (grid > a.n_lines) grid = a.n_lines;
@@ -116,23 +116,22 @@ cudaError_t launch_big(const PassArgs& a, cudaStream_t s, const CUtensorMap& map
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, nslct::line_pass_big_kernel<LOG2N, MODE, SLAB, LAND>, a, map);
+  return cudaLaunchKernelEx(&cfg, nslct::line_pass_big_kernel<LOG2N, MODE, SLAB>, a, map);
 }
-template <int LOG2N, int MODE, bool SLAB, bool LAND>
+template <int LOG2N, int MODE, bool SLAB>
 cudaError_t set_attr_big() {
-  return cudaFuncSetAttribute(nslct::line_pass_big_kernel<LOG2N, MODE, SLAB, LAND>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nslct::BigCfg<LOG2N, LAND>::SMEM);
+  return cudaFuncSetAttribute(nslct::line_pass_big_kernel<LOG2N, MODE, SLAB>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nslct::BigCfg<LOG2N>::SMEM);
 }
 typedef cudaError_t (*big_fn)(const PassArgs&, cudaStream_t, const CUtensorMap&);
-template <int LOG2N, bool SLAB, bool LAND>
+template <int LOG2N, bool SLAB>
 struct BigRow {
   static void fill(big_fn* l, attr_fn* at) {
-    l[0] = launch_big<LOG2N, 0, SLAB, LAND>; l[1] = launch_big<LOG2N, 1, SLAB, LAND>;
-    l[2] = launch_big<LOG2N, 2, SLAB, LAND>; l[3] = launch_big<LOG2N, 3, SLAB, LAND>;
-    l[4] = launch_big<LOG2N, 4, SLAB, LAND>; l[5] = launch_big<LOG2N, 5, SLAB, LAND>;
-    at[0] = set_attr_big<LOG2N, 0, SLAB, LAND>; at[1] = set_attr_big<LOG2N, 1, SLAB, LAND>;
-    at[2] = set_attr_big<LOG2N, 2, SLAB, LAND>; at[3] = set_attr_big<LOG2N, 3, SLAB, LAND>;
-    at[4] = set_attr_big<LOG2N, 4, SLAB, LAND>; at[5] = set_attr_big<LOG2N, 5, SLAB, LAND>;
+    l[0] = launch_big<LOG2N, 0, SLAB>; l[1] = launch_big<LOG2N, 1, SLAB>; l[2] = launch_big<LOG2N, 2, SLAB>;
+    l[3] = launch_big<LOG2N, 3, SLAB>; l[4] = launch_big<LOG2N, 4, SLAB>; l[5] = launch_big<LOG2N, 5, SLAB>;
+    at[0] = set_attr_big<LOG2N, 0, SLAB>; at[1] = set_attr_big<LOG2N, 1, SLAB>;
+    at[2] = set_attr_big<LOG2N, 2, SLAB>; at[3] = set_attr_big<LOG2N, 3, SLAB>;
+    at[4] = set_attr_big<LOG2N, 4, SLAB>; at[5] = set_attr_big<LOG2N, 5, SLAB>;
   }
 };
 
@@ -315,8 +314,8 @@ struct Table {
   attr_fn at[2][kMaxLog + 1][kModes] = {};
   launch_fn lpair[2][kMaxLog + 1][kModes] = {};   // c64 N = 8192, 16384 (cluster pairs): [slab]
   attr_fn atpair[2][kMaxLog + 1][kModes] = {};
-  big_fn lbig[2][2][kMaxLog + 1][kModes] = {};     // c64 N = 8192, 16384 (TMA-fed): [land][slab]
-  attr_fn atbig[2][2][kMaxLog + 1][kModes] = {};
+  big_fn lbig[2][kMaxLog + 1][kModes] = {};     // c64 N = 8192 (TMA-pipelined): [slab]
+  attr_fn atbig[2][kMaxLog + 1][kModes] = {};
   pipe_fn lp[kMaxLog + 1][kModes] = {};   // c64 only
   attr_fn atp[kMaxLog + 1][kModes] = {};
   Table() {
@@ -331,14 +330,8 @@ struct Table {
     PairRow<14, false>::fill(lpair[0][14], atpair[0][14]);
     PairRow<13, true>::fill(lpair[1][13], atpair[1][13]);
     PairRow<14, true>::fill(lpair[1][14], atpair[1][14]);
-    BigRow<13, false, true>::fill(lbig[1][0][13], atbig[1][0][13]);
-    BigRow<14, false, true>::fill(lbig[1][0][14], atbig[1][0][14]);
-    BigRow<13, true, true>::fill(lbig[1][1][13], atbig[1][1][13]);
-    BigRow<14, true, true>::fill(lbig[1][1][14], atbig[1][1][14]);
-    BigRow<13, false, false>::fill(lbig[0][0][13], atbig[0][0][13]);
-    BigRow<14, false, false>::fill(lbig[0][0][14], atbig[0][0][14]);
-    BigRow<13, true, false>::fill(lbig[0][1][13], atbig[0][1][13]);
-    BigRow<14, true, false>::fill(lbig[0][1][14], atbig[0][1][14]);
+    BigRow<13, false>::fill(lbig[0][13], atbig[0][13]);
+    BigRow<13, true>::fill(lbig[1][13], atbig[1][13]);
     PipeRow<float, 10>::fill(lp[10], atp[10]);
     PipeRow<float, 11>::fill(lp[11], atp[11]);
     PipeRow<float, 12>::fill(lp[12], atp[12]);
@@ -537,9 +530,8 @@ struct nslct_plan_s {
   bool pipe = false;   // persistent TMA-pipelined kernels
   bool image = false;  // fully on-chip kernel (one launch per exec)
   bool ws = false;     // warp-specialised pipe kernels for modes 1-3
-  bool pair = false;   // large-N cluster-pair line passes, one-line loads (opts.kernels = 2, A/B only)
-  bool big = false;    // large-N TMA-pipelined cluster-pair passes (N = 8192, 16384, complex64)
-  int land = 1;        // ... with the next line landing in its own buffer (0: into the exchange buffer)
+  bool pair = false;   // large-N cluster-pair line passes (N = 16384, complex64)
+  bool big = false;    // large-N TMA-pipelined cluster-pair passes (N = 8192, complex64)
   unsigned long long* counters = nullptr;   // per-pass group counters (pipe mode)
   int num_sms = 148;
   int host_chunk_kb = 0;    // opts.host_chunk_kb (exec_host pipeline chunk; 0 = auto)
@@ -787,7 +779,7 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
   if (batch < 1) return fail(NSLCT_E_ARG, "batch must be >= 1");
   if (o.variant < 0 || o.variant > 3 || o.dispatch < 0 || o.dispatch > 1 || o.schedule < 0 || o.schedule > 2)
     return fail(NSLCT_E_ARG, "bad variant/dispatch option");
-  if (o.kernels < 0 || o.kernels > NSLCT_KERNELS_BIG_NOLAND) return fail(NSLCT_E_ARG, "bad kernels option");
+  if (o.kernels < 0 || o.kernels > NSLCT_KERNELS_GENERIC) return fail(NSLCT_E_ARG, "bad kernels option");
   int lg = 0;
   while ((int64_t(1) << lg) < n && lg < 62) ++lg;
   const bool pow2 = n >= 1 && (int64_t(1) << lg) == n && lg >= kMinLog && lg <= kMaxLog &&
@@ -1128,12 +1120,13 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
         }
       }
       const bool large = plain && ti == 0 && (lg == 13 || lg == 14) && (L % 2 == 0) && (Lc % 16 == 0);
-      pl->big = large && (special || o.kernels == NSLCT_KERNELS_BIG_NOLAND);
-      pl->land = (o.kernels == NSLCT_KERNELS_BIG_NOLAND) ? 0 : 1;
-      pl->pair = large && o.kernels == NSLCT_KERNELS_PAIR_V1;
+      // N = 8192: the TMA-pipelined kernel (Q16 intermediates); N = 16384: the cluster-pair
+      // kernel (pair-interleaved intermediates) -- measured faster at each size (kernels.cuh)
+      pl->big = large && special && lg == 13;
+      pl->pair = large && special && lg == 14;
       for (int k = 0; k < 5 && (pl->pair || pl->big); ++k) pl->args[k].persist_ctas = (pl->num_sms / 2) * 2;
       for (int m = 0; m < kModes && (pl->pair || pl->big); ++m) {
-        cudaError_t e = pl->big ? table().atbig[pl->land][slab ? 1 : 0][lg][m]() : table().atpair[slab ? 1 : 0][lg][m]();
+        cudaError_t e = pl->big ? table().atbig[slab ? 1 : 0][lg][m]() : table().atpair[slab ? 1 : 0][lg][m]();
         if (e != cudaSuccess) {
           result = fail(NSLCT_E_CUDA, std::string("cudaFuncSetAttribute(large N): ") + cudaGetErrorString(e));
           break;
@@ -1382,7 +1375,7 @@ static nslct_status launch_large(nslct_plan_t pl, int k, const PassArgs& a, cuda
     nslct_status st = make_q16_map(&map, a.in, pl->log2n, L, C, images);
     if (st != NSLCT_OK) return st;
   }
-  CUDA_TRY(table().lbig[pl->land][sl][pl->log2n][m](a, s, map));
+  CUDA_TRY(table().lbig[sl][pl->log2n][m](a, s, map));
   return NSLCT_OK;
 }
 

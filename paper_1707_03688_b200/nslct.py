@@ -28,7 +28,7 @@ EXPORTS = ("nslct_opts_default", "nslct_plan", "nslct_plan_ex", "nslct_exec", "n
            "nslct_exec_pass_peer", "nslct_inverse_matrix", "nslct_comm_unique_id", "nslct_comm_init",
            "nslct_comm_info", "nslct_comm_destroy", "nslct_fp32_peak")
 ABI_VERSION = 4
-KERNELS = {"auto": 0, "generic": 1, "pair_v1": 2, "big_noland": 3}
+KERNELS = {"auto": 0, "generic": 1}
 EXCHANGES = {"nccl": 0, "peer": 1}
 
 

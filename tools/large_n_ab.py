@@ -1,4 +1,4 @@
-"""A/B of the large-N kernels (TMA-pipelined vs round-1 cluster pairs vs generic) on one GPU:
+"""A/B of the large-N kernels (the default vs the generic one-CTA-per-line kernels) on one GPU:
 per-pass CUDA-event times of one n x n complex64 transform, and the C5 slab passes of one
 rank.  Usage: python tools/large_n_ab.py [n] [batch]"""
 import json
@@ -40,7 +40,7 @@ def run(n, batch, kernels, reps=10):
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 ref = None
-for k in ("auto", "big_noland", "pair_v1"):
+for k in ("auto", "generic"):
     r, out = run(n, batch, k)
     if ref is None:
         ref = out.clone()
