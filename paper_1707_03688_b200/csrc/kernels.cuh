@@ -1495,13 +1495,11 @@ line_pass_pair_kernel(PassArgs a) {
   };
   if (tid == 0 && cl < npairs) prefetch(cl);
 
-  for (long long p = cl; p < npairs; p += ncl) {
-    if (tid == 0 && p + ncl < npairs) prefetch(p + ncl);
-    const long long line = a.line_base + 2 * p + c;   // over the batch
+  // this CTA's line of pair p into registers (coalesced per-thread loads)
+  auto load_line = [&](long long p, cpx<T> (&v)[16]) {
+    const long long line = a.line_base + 2 * p + c;
     const long long img = line >> lgL;
-    const int ll = (int)(line & (L - 1));              // local line
-    const int l = a.line_offset + ll;                  // global line (chirps)
-    cpx<T> v[16];
+    const int ll = (int)(line & (L - 1));
     if constexpr (ModeIO<MODE>::kUserIn) {   // the user's row-major line
       const cpx<T>* src = in + line * N + j;
 #pragma unroll
@@ -1520,6 +1518,20 @@ line_pass_pair_kernel(PassArgs a) {
         for (int e = 0; e < 16; ++e) v[e] = src[2 * TL * e];
       }
     }
+  };
+  // The loads of the next pair are issued as soon as the current line has left the
+  // registers (staged in shared memory, or stored), so their latency overlaps the output
+  // phase (segment writes through DSMEM, cluster barriers) instead of stalling the next
+  // iteration's first FFT stage.
+  cpx<T> v[16];
+  if (cl < npairs) load_line(cl, v);
+  for (long long p = cl; p < npairs; p += ncl) {
+    if (tid == 0 && p + ncl < npairs) prefetch(p + ncl);
+    const long long line = a.line_base + 2 * p + c;   // over the batch
+    const long long img = line >> lgL;
+    const int ll = (int)(line & (L - 1));              // local line
+    const int l = a.line_offset + ll;                  // global line (chirps)
+    const bool more = p + ncl < npairs;
     pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ExPad<T>{buf});
 
     cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * slab_elems;
@@ -1531,6 +1543,7 @@ line_pass_pair_kernel(PassArgs a) {
       cpx<T>* dst = out + (long long)ll * N;
 #pragma unroll
       for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
+      if (more) load_line(p + ncl, v);
       __syncthreads();   // the next iteration's exchange reuses buf
     } else {
       __syncthreads();   // the FFT's last reads of buf are done
@@ -1538,6 +1551,8 @@ line_pass_pair_kernel(PassArgs a) {
       for (int e = 0; e < 16; ++e) buf[pad16(j + TL * e)] = v[e];
       // both CTAs' lines staged (release/acquire across the cluster)
       asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+      // (issued after the release arrive, which would otherwise wait for them)
+      if (more) load_line(p + ncl, v);
       const int lp = ll & ~1;   // local line 0 of the pair
       // element pairs (e0, e0+1) in this CTA's half of the line: consumer lines
       // lam = e0 % L, lam + 1 of block s = e0 / L; 32-byte segment [lp: lam, lam+1 |

@@ -312,7 +312,7 @@ struct Table {
   attr_fn ati[2][kMaxLog + 1] = {};
   launch_fn l[2][kMaxLog + 1][kModes] = {};
   attr_fn at[2][kMaxLog + 1][kModes] = {};
-  launch_fn lpair[2][kMaxLog + 1][kModes] = {};   // c64 N = 8192, 16384 (cluster pairs): [slab]
+  launch_fn lpair[2][kMaxLog + 1][kModes] = {};   // c64 N = 16384 (cluster pairs): [slab]
   attr_fn atpair[2][kMaxLog + 1][kModes] = {};
   big_fn lbig[2][kMaxLog + 1][kModes] = {};     // c64 N = 8192 (TMA-pipelined): [slab]
   attr_fn atbig[2][kMaxLog + 1][kModes] = {};
@@ -326,9 +326,7 @@ struct Table {
     li[1][5] = launch_img<double, 5, 1>, ati[1][5] = set_attr_img<double, 5, 1>;
     li[1][6] = launch_img<double, 6, 1>, ati[1][6] = set_attr_img<double, 6, 1>;
     li[1][7] = launch_img<double, 7, 4>, ati[1][7] = set_attr_img<double, 7, 4>;
-    PairRow<13, false>::fill(lpair[0][13], atpair[0][13]);
     PairRow<14, false>::fill(lpair[0][14], atpair[0][14]);
-    PairRow<13, true>::fill(lpair[1][13], atpair[1][13]);
     PairRow<14, true>::fill(lpair[1][14], atpair[1][14]);
     BigRow<13, false>::fill(lbig[0][13], atbig[0][13]);
     BigRow<13, true>::fill(lbig[1][13], atbig[1][13]);
