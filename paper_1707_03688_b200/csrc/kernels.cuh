@@ -1421,6 +1421,284 @@ line_pass_ws_kernel(PassArgs a, long long n_groups, unsigned long long* counter,
 }
 
 // ---------------------------------------------------------------------------------
+// V "virtual threads" per thread: the same radix-16 Stockham line FFT and pass body, with
+// each physical thread holding the 16-element register lines of V logical threads
+// j = jv[0..V-1] (elements j + TL e).  Every stage runs the butterflies of all V before the
+// exchange barrier, so the barrier count per line is that of the V = 1 code while the
+// line is held by V times fewer threads (more registers per thread: the N = 16384 pass
+// at 512 threads has 128 registers instead of 64 at 1024 threads).
+// ---------------------------------------------------------------------------------
+template <typename T, int LOG2N, int STAGE, int NS, int X, int V, class E, class TW>
+__device__ __forceinline__ void fft_stage_v(cpx<T> (&v)[V][16], const int (&jv)[V], const TW (&tw)[V], const E& ex) {
+  constexpr int N = 1 << LOG2N;
+  constexpr int TL = N / 16;
+  constexpr int NFULL = LOG2N / 4;
+  constexpr int R = (STAGE < NFULL) ? 16 : (1 << (LOG2N % 4));
+  constexpr int NB = 16 / R;
+  constexpr bool LAST = (STAGE == NS - 1);
+  constexpr int Ns = (STAGE < NFULL) ? (1 << (4 * STAGE)) : (1 << (4 * NFULL));
+  static_assert(E::kPadded && TL % 16 == 0, "padded fast exchange addressing");
+  cpx<T>* buf = ex.template b<X>();
+  constexpr int PW = E::kPadW;
+  constexpr int WSTEP = (Ns >= 16) ? Ns + PW * Ns / 16 : Ns;
+  constexpr int RSTEP = TL + PW * TL / 16;
+#pragma unroll
+  for (int t = 0; t < V; ++t) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int jp = jv[t] + b * TL;
+      cpx<T> u[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) u[r] = v[t][b + r * NB];
+      if constexpr (Ns > 1) tw[t].template apply<STAGE, R>(u, b, jp);
+      dft<R>(u);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[t][b + r * NB] = u[r];
+      if constexpr (!LAST) {
+        const int idxD = (jp / Ns) * Ns * R + (jp % Ns);
+        cpx<T>* wb = buf + padw<PW>(idxD);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int r = (R == 16) ? ((q & 3) * 4 + (q >> 2)) : q;
+          wb[r * WSTEP] = u[r];
+        }
+      }
+    }
+  }
+  if constexpr (!LAST) {
+#pragma unroll
+    for (int t = 0; t < V; ++t) tw[t].template prefetch<STAGE + 1>();
+    ex.template sync<X>();
+    ex.template after_barrier<X>();
+#pragma unroll
+    for (int t = 0; t < V; ++t) {
+      const cpx<T>* rb = buf + padw<PW>(jv[t]);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int e = (q & 3) * 4 + (q >> 2);
+        v[t][e] = rb[e * RSTEP];
+      }
+    }
+    if constexpr (!E::kDouble) __syncthreads();
+  }
+}
+
+template <typename T, int LOG2N, int STAGE, int NS, int X0, int V, class E, class TW>
+struct FftStagesV {
+  __device__ __forceinline__ static void run(cpx<T> (&v)[V][16], const int (&jv)[V], const TW (&tw)[V], const E& ex) {
+    fft_stage_v<T, LOG2N, STAGE, NS, X0 + STAGE, V, E, TW>(v, jv, tw, ex);
+    FftStagesV<T, LOG2N, STAGE + 1, NS, X0, V, E, TW>::run(v, jv, tw, ex);
+  }
+};
+template <typename T, int LOG2N, int NS, int X0, int V, class E, class TW>
+struct FftStagesV<T, LOG2N, NS, NS, X0, V, E, TW> {
+  __device__ __forceinline__ static void run(cpx<T> (&)[V][16], const int (&)[V], const TW (&)[V], const E&) {}
+};
+
+template <typename T, int LOG2N, int X0, int V, class E, class TW>
+__device__ __forceinline__ void line_fft_v(cpx<T> (&v)[V][16], const int (&jv)[V], const TW (&tw)[V], const E& ex) {
+  FftStagesV<T, LOG2N, 0, FftInfo<LOG2N>::NS, X0, V, E, TW>::run(v, jv, tw, ex);
+}
+
+template <int V, typename T>
+__device__ __forceinline__ void conj_all(cpx<T> (&v)[V][16]) {
+#pragma unroll
+  for (int t = 0; t < V; ++t)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[t][e] = cconj(v[t][e]);
+}
+
+// pass_body for V virtual threads (power-of-two FFTs; modes 0-5 as pass_body)
+template <typename T, int LOG2N, int MODE, int V, class E, class TW>
+__device__ __forceinline__ void pass_body_v(cpx<T> (&v)[V][16], const int (&jv)[V], const TW (&tw)[V],
+                                            const PassArgs& a, uint64_t l, const E& ex) {
+  constexpr int TL = (1 << LOG2N) / 16;
+  constexpr int NX = FftInfo<LOG2N>::NX;
+  const T scale = (T)a.scale;
+  auto chirp = [&](const Phase& ph, auto conj_in, auto do_scale, int sign_mode) {
+#pragma unroll
+    for (int t = 0; t < V; ++t)
+      apply_chirp<T, TL, decltype(conj_in)::value, decltype(do_scale)::value>(v[t], ph, l, (uint64_t)jv[t], scale,
+                                                                              sign_mode);
+  };
+  using F = std::false_type;
+  using Tr = std::true_type;
+  if constexpr (MODE == 0) {
+    chirp(a.ph, F{}, F{}, a.sign_only);
+    line_fft_v<T, LOG2N, 0>(v, jv, tw, ex);
+  } else if constexpr (MODE == 1) {
+    line_fft_v<T, LOG2N, 0>(v, jv, tw, ex);
+    conj_all(v);
+    chirp(neg_phase(a.ph), F{}, F{}, 0);
+    line_fft_v<T, LOG2N, NX>(v, jv, tw, ex);
+    conj_all(v);
+  } else if constexpr (MODE == 2) {
+    conj_all(v);
+    line_fft_v<T, LOG2N, 0>(v, jv, tw, ex);
+    chirp(a.ph, Tr{}, F{}, 0);
+    line_fft_v<T, LOG2N, NX>(v, jv, tw, ex);
+  } else if constexpr (MODE == 3) {
+    conj_all(v);
+    line_fft_v<T, LOG2N, 0>(v, jv, tw, ex);
+    chirp(a.ph, Tr{}, Tr{}, a.sign_only);
+  } else if constexpr (MODE == 4) {
+    chirp(a.ph, F{}, F{}, a.sign_only);
+    line_fft_v<T, LOG2N, 0>(v, jv, tw, ex);
+    conj_all(v);
+    chirp(neg_phase(a.ph_b), F{}, F{}, 0);
+    line_fft_v<T, LOG2N, NX>(v, jv, tw, ex);
+    chirp(a.ph_c, Tr{}, F{}, a.sign_c);
+    line_fft_v<T, LOG2N, 2 * NX>(v, jv, tw, ex);
+  } else {
+    static_assert(MODE == 5, "pass mode");
+    conj_all(v);
+    line_fft_v<T, LOG2N, 0>(v, jv, tw, ex);
+    chirp(a.ph, Tr{}, F{}, 0);
+    line_fft_v<T, LOG2N, NX>(v, jv, tw, ex);
+    conj_all(v);
+    chirp(neg_phase(a.ph_b), F{}, F{}, 0);
+    line_fft_v<T, LOG2N, 2 * NX>(v, jv, tw, ex);
+    chirp(a.ph_c, Tr{}, Tr{}, a.sign_c);
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// N = 16384 cluster-pair line pass with 512 threads x 2 virtual threads (V = 2): the same
+// algorithm, layout and output protocol as line_pass_pair_kernel below (which runs 1024
+// threads at 64 registers and spills in its two-FFT passes), with 128 registers per thread.
+// ---------------------------------------------------------------------------------
+constexpr int kPair2Threads = 512;
+template <int MODE, bool SLAB>
+__global__ void __launch_bounds__(kPair2Threads, 1)
+line_pass_pair2_kernel(PassArgs a) {
+  using T = float;
+  constexpr int LOG2N = 14;
+  constexpr int N = 1 << LOG2N, TL = N / 16, THREADS = kPair2Threads, V = TL / THREADS;
+  constexpr int LS = N + N / 16 + 1;   // as LineCfg<14>::LS (G = 1)
+  static_assert(V == 2, "two virtual threads");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  cpx<T>* buf = reinterpret_cast<cpx<T>*>(smem_raw);
+  (void)LS;
+  uint32_t c;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c));
+  const int tid = threadIdx.x;
+  int jv[V];
+#pragma unroll
+  for (int t = 0; t < V; ++t) jv[t] = tid + t * THREADS;
+  const int lgL = SLAB ? __ffs(a.lines_per_img) - 1 : LOG2N;
+  const int lgC = SLAB ? __ffs(a.in_chunk) - 1 : LOG2N;
+  const int lgLc = SLAB ? __ffs(a.out_chunk) - 1 : LOG2N;
+  const int L = 1 << lgL, C = 1 << lgC, Lc = 1 << lgLc;
+  const long long slab_elems = (long long)L * N;
+  const long long npairs = a.n_lines / 2;
+  const long long ncl = gridDim.x / 2;
+  const long long cl = blockIdx.x / 2;
+  const cpx<T>* __restrict__ tw = reinterpret_cast<const cpx<T>*>(a.tw);
+  const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in);
+  TwSet<T, LOG2N> tws[V];
+#pragma unroll
+  for (int t = 0; t < V; ++t) tws[t].load(tw, jv[t]);
+  uint64_t ra[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(ra[r]) : "l"(reinterpret_cast<uint64_t>(buf)), "r"(r));
+  const cpx<T>* b0 = reinterpret_cast<const cpx<T>*>(ra[0]);
+  const cpx<T>* b1 = reinterpret_cast<const cpx<T>*>(ra[1]);
+  const bool contiguous = !SLAB || ModeIO<MODE>::kUserIn || C == N;
+  auto prefetch = [&](long long p) {
+    if (!SLAB || contiguous) {
+      const long long line = a.line_base + 2 * p + c;
+      const cpx<T>* src = ModeIO<MODE>::kUserIn ? in + line * N : in + (a.line_base + 2 * p) * N + (long long)c * N;
+      bulk_prefetch_l2(src, (uint32_t)(N * sizeof(cpx<T>)));
+    } else if constexpr (SLAB) {
+      const long long line = a.line_base + 2 * p;
+      const long long img = line / L;
+      const int lp = (int)(line % L);
+      for (int sb = (int)c; sb < N / C; sb += 2)
+        bulk_prefetch_l2(in + img * slab_elems + (long long)sb * L * C + (long long)(lp / 2) * 2 * C,
+                         (uint32_t)(2 * C * sizeof(cpx<T>)));
+    }
+  };
+  if (tid == 0 && cl < npairs) prefetch(cl);
+  auto load_line = [&](long long p, cpx<T> (&v)[V][16]) {
+    const long long line = a.line_base + 2 * p + c;
+    const long long img = line >> lgL;
+    const int ll = (int)(line & (L - 1));
+#pragma unroll
+    for (int t = 0; t < V; ++t) {
+      const int j = jv[t];
+      if constexpr (ModeIO<MODE>::kUserIn) {
+        const cpx<T>* src = in + line * N + j;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[t][e] = src[TL * e];
+      } else {
+        const cpx<T>* src = in + img * slab_elems + (long long)(ll / 2) * 2 * C + (ll % 2);
+        if constexpr (SLAB) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int i = j + TL * e;
+            v[t][e] = src[((long long)(i >> lgC) << (lgL + lgC)) + 2 * (i & (C - 1))];
+          }
+        } else {
+          src += 2 * j;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[t][e] = src[2 * TL * e];
+        }
+      }
+    }
+  };
+  cpx<T> v[V][16];
+  if (cl < npairs) load_line(cl, v);
+  for (long long p = cl; p < npairs; p += ncl) {
+    if (tid == 0 && p + ncl < npairs) prefetch(p + ncl);
+    const long long line = a.line_base + 2 * p + c;
+    const long long img = line >> lgL;
+    const int ll = (int)(line & (L - 1));
+    const int l = a.line_offset + ll;
+    const bool more = p + ncl < npairs;
+    pass_body_v<T, LOG2N, MODE, V>(v, jv, tws, a, (uint64_t)l, ExPad<T>{buf});
+
+    cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * slab_elems;
+    if constexpr (ModeIO<MODE>::kStraightOut) {
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+      cpx<T>* dst = out + (long long)ll * N;
+#pragma unroll
+      for (int t = 0; t < V; ++t)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) dst[jv[t] + TL * e] = v[t][e];
+      if (more) load_line(p + ncl, v);
+      __syncthreads();
+    } else {
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < V; ++t)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) buf[pad16(jv[t] + TL * e)] = v[t][e];
+      asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+      if (more) load_line(p + ncl, v);
+      const int lp = ll & ~1;
+      for (int q = (int)c * (N / 4) + tid; q < ((int)c + 1) * (N / 4); q += THREADS) {
+        const int e0 = 2 * q;
+        const cpx<T> a0 = b0[pad16(e0)], a1 = b0[pad16(e0 + 1)];
+        const cpx<T> c0 = b1[pad16(e0)], c1 = b1[pad16(e0 + 1)];
+        cpx<T>* d;
+        if constexpr (SLAB) {
+          const int sblk = e0 >> lgL, lam = e0 & (L - 1);
+          cpx<T>* base = a.peer_on ? reinterpret_cast<cpx<T>*>(a.peer_out[sblk]) + (long long)a.peer_rank * L * L
+                                   : out + (long long)sblk * L * L;
+          d = base + ((long long)(lp >> lgLc) << (lgL + lgLc)) + (long long)(lam / 2) * 2 * Lc + 2 * (lp & (Lc - 1));
+        } else {
+          d = out + (long long)q * 2 * N + 2 * lp;
+        }
+        reinterpret_cast<float4*>(d)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
+        reinterpret_cast<float4*>(d)[1] = make_float4(c0.x, c0.y, c1.x, c1.y);
+      }
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // Large-N line pass (N = 8192, 16384; complex64, batched plans): a line is 64-128 KB, so
 // one CTA holds ONE line (G = 1) and the persistent pipe kernels' group of two lines per
 // CTA does not fit.  A CLUSTER of two CTAs takes the two lines of a pair-interleaved

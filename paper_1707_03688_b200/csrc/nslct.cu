@@ -80,6 +80,41 @@ cudaError_t launch_pair(const PassArgs& a, cudaStream_t s) {
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair_kernel<float, LOG2N, MODE, SLAB>, a);
 }
+// N = 16384: 512 threads x 2 virtual threads (kernels.cuh line_pass_pair2_kernel)
+template <int MODE, bool SLAB>
+cudaError_t launch_pair2(const PassArgs& a, cudaStream_t s) {
+  using Cfg = nslct::LineCfg<14>;
+  cudaLaunchConfig_t cfg = {};
+  long long grid = a.persist_ctas > 0 ? a.persist_ctas : a.n_lines;
+  if (grid > a.n_lines) grid = a.n_lines;
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(nslct::kPair2Threads);
+  cfg.dynamicSmemBytes = (size_t)Cfg::LS * sizeof(nslct::cpx<float>);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair2_kernel<MODE, SLAB>, a);
+}
+template <int MODE, bool SLAB>
+cudaError_t set_attr_pair2() {
+  using Cfg = nslct::LineCfg<14>;
+  return cudaFuncSetAttribute(nslct::line_pass_pair2_kernel<MODE, SLAB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(Cfg::LS * sizeof(nslct::cpx<float>)));
+}
+template <bool SLAB>
+struct Pair2Row {
+  static void fill(launch_fn* l, attr_fn* at) {
+    l[0] = launch_pair2<0, SLAB>; l[1] = launch_pair2<1, SLAB>; l[2] = launch_pair2<2, SLAB>;
+    l[3] = launch_pair2<3, SLAB>; l[4] = launch_pair2<4, SLAB>; l[5] = launch_pair2<5, SLAB>;
+    at[0] = set_attr_pair2<0, SLAB>; at[1] = set_attr_pair2<1, SLAB>; at[2] = set_attr_pair2<2, SLAB>;
+    at[3] = set_attr_pair2<3, SLAB>; at[4] = set_attr_pair2<4, SLAB>; at[5] = set_attr_pair2<5, SLAB>;
+  }
+};
 template <int LOG2N, int MODE, bool SLAB>
 cudaError_t set_attr_pair() {
   using Cfg = nslct::LineCfg<LOG2N>;
@@ -326,8 +361,13 @@ struct Table {
     li[1][5] = launch_img<double, 5, 1>, ati[1][5] = set_attr_img<double, 5, 1>;
     li[1][6] = launch_img<double, 6, 1>, ati[1][6] = set_attr_img<double, 6, 1>;
     li[1][7] = launch_img<double, 7, 4>, ati[1][7] = set_attr_img<double, 7, 4>;
+#ifdef NSLCT_AB_PAIR1
     PairRow<14, false>::fill(lpair[0][14], atpair[0][14]);
     PairRow<14, true>::fill(lpair[1][14], atpair[1][14]);
+#else
+    Pair2Row<false>::fill(lpair[0][14], atpair[0][14]);
+    Pair2Row<true>::fill(lpair[1][14], atpair[1][14]);
+#endif
     BigRow<13, false>::fill(lbig[0][13], atbig[0][13]);
     BigRow<13, true>::fill(lbig[1][13], atbig[1][13]);
     PipeRow<float, 10>::fill(lp[10], atp[10]);
