@@ -21,7 +21,8 @@ def launches(path, tag):
     for row in r[1:]:
         per.setdefault(int(row[ii]), {"k": row[ki]})[row[mi]] = float(row[vi].replace(",", ""))
     ids = sorted(per)
-    ours = [i for i in ids if "nslct" in per[i]["k"]]
+    # the C4 step's kernels (log2 N = 12; the sub-records of other configs launch others)
+    ours = [i for i in ids if "nslct" in per[i]["k"] and ("<float, 12," in per[i]["k"] or "<12," in per[i]["k"])]
     last = ours[-5:]   # one step = the last 5 launches
     tot = sum(per[i]["gpu__time_duration.sum"] for i in last)
     print("# %s ncu launch list (bench.py --steps 1 --warmup 3, C4 4096^2 c64 batch 32, 1 B200)" % tag)
