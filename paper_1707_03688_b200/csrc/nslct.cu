@@ -80,10 +80,18 @@ cudaError_t launch_pair(const PassArgs& a, cudaStream_t s) {
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair_kernel<float, LOG2N, MODE, SLAB>, a);
 }
-// N = 16384: 512 threads x 2 virtual threads (kernels.cuh line_pass_pair2_kernel)
+nslct_status make_store_map(CUtensorMap* m, void* out, int log2n, long long images);
+// N = 16384: 512 threads x 2 virtual threads (kernels.cuh line_pass_pair2_kernel); the
+// batched transposing passes write through TMA tensor stores (map of the pair-interleaved
+// output, G = 2)
 template <int MODE, bool SLAB>
 cudaError_t launch_pair2(const PassArgs& a, cudaStream_t s) {
   using Cfg = nslct::LineCfg<14>;
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  if (!SLAB && !nslct::ModeIO<MODE>::kStraightOut &&
+      make_store_map(&map, a.out, 14, a.n_lines >> 14) != NSLCT_OK)
+    return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   long long grid = a.persist_ctas > 0 ? a.persist_ctas : a.n_lines;
   if (grid > a.n_lines) grid = a.n_lines;
@@ -98,7 +106,7 @@ cudaError_t launch_pair2(const PassArgs& a, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair2_kernel<MODE, SLAB>, a);
+  return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair2_kernel<MODE, SLAB>, a, map);
 }
 template <int MODE, bool SLAB>
 cudaError_t set_attr_pair2() {
@@ -245,7 +253,7 @@ nslct_status make_store_map(CUtensorMap* m, void* out, int log2n, long long imag
   auto fn = encode_tiled();
   if (!fn) return fail(NSLCT_E_CUDA, "cuTensorMapEncodeTiled entry point not available");
   const cuuint64_t n = 1ull << log2n;
-  const cuuint64_t G = 8192 / n, IL = 2;
+  const cuuint64_t G = n <= 4096 ? 8192 / n : 2, IL = 2;   // pipe groups; the pair kernels' 2 lines
   const cuuint64_t dims[4] = {2 * IL * G, n / IL, n / G, (cuuint64_t)images};
   const cuuint64_t strides[3] = {IL * n * 8, IL * G * 8, n * n * 8};
   const cuuint32_t box[4] = {(cuuint32_t)(2 * IL * G), (cuuint32_t)(n / IL < 256 ? n / IL : 256), 1, 1};
