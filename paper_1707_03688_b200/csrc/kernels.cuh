@@ -1027,6 +1027,13 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
                : "memory");
 }
 // 4D tensor store from shared memory (box at coordinates c0..c3 of the tensor map)
+__device__ __forceinline__ void tensor_s2g_5d(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                              int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
 __device__ __forceinline__ void tensor_s2g_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
                                               int c3) {
   asm volatile(
@@ -1552,9 +1559,194 @@ struct FftStagesV<T, LOG2N, NS, NS, X0, V, E, TW> {
   __device__ __forceinline__ static void run(cpx<T> (&)[V][16], const int (&)[V], const TW (&)[V], const E&) {}
 };
 
+// ---------------------------------------------------------------------------------
+// N = 16384 line FFT with radix-32 stages (32 x 32 x 16): 2 shared-memory exchanges per
+// FFT instead of the radix-16 schedule's 3 (16 x 16 x 16 x 4).  512 threads per line, the
+// register line of thread j is the V = 2 view above: slot k = 2e + t (v[t][e]) holds
+// element j + 512 k, before and after (Stockham, decimation in time).  Exchange buffer
+// index i + i/32 (conflict-free for the radix-32 stores).  Stage twiddle powers come from
+// TENSOR MEMORY (TwTmem32: 31 + 2 x 15 complex = 122 of the thread's 128 columns), loaded
+// in 16-column chunks one chunk ahead.
+// ---------------------------------------------------------------------------------
+// u[32] -> DFT32(u), natural order in and out: two DFT16 (even / odd inputs), W32^k on
+// the odd half, radix-2.
+template <int K, typename T>
+__device__ __forceinline__ cpx<T> w32(cpx<T> a) {
+  if constexpr ((K & 1) == 0) {
+    return w16<K / 2>(a);
+  } else {
+    constexpr double PI = 3.14159265358979323846;
+    // exp(-2 pi i K / 32) = cos(K pi / 16) - j sin(K pi / 16); crot(a, c, s) = a (c - j s)
+    constexpr double c = (K == 1) ? 0.98078528040323044913 : (K == 3) ? 0.83146961230254523708
+                         : (K == 5) ? 0.55557023301960222474 : (K == 7) ? 0.19509032201612826785
+                         : (K == 9) ? -0.19509032201612826785 : (K == 11) ? -0.55557023301960222474
+                         : (K == 13) ? -0.83146961230254523708 : -0.98078528040323044913;
+    constexpr double sn = (K == 1 || K == 15) ? 0.19509032201612826785 : (K == 3 || K == 13) ? 0.55557023301960222474
+                          : (K == 5 || K == 11) ? 0.83146961230254523708 : 0.98078528040323044913;
+    (void)PI;
+    return crot(a, T(c), T(sn));
+  }
+}
+template <typename T>
+__device__ __forceinline__ void dft32(cpx<T> (&u)[32]) {
+  cpx<T> e[16], o[16];
+#pragma unroll
+  for (int n = 0; n < 16; ++n) {
+    e[n] = u[2 * n];
+    o[n] = u[2 * n + 1];
+  }
+  dft<16>(e);
+  dft<16>(o);
+  o[1] = w32<1>(o[1]);   o[2] = w32<2>(o[2]);   o[3] = w32<3>(o[3]);   o[4] = w32<4>(o[4]);
+  o[5] = w32<5>(o[5]);   o[6] = w32<6>(o[6]);   o[7] = w32<7>(o[7]);   o[8] = w32<8>(o[8]);
+  o[9] = w32<9>(o[9]);   o[10] = w32<10>(o[10]); o[11] = w32<11>(o[11]); o[12] = w32<12>(o[12]);
+  o[13] = w32<13>(o[13]); o[14] = w32<14>(o[14]); o[15] = w32<15>(o[15]);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    u[k] = cadd(e[k], o[k]);
+    u[k + 16] = csub(e[k], o[k]);
+  }
+}
+
+struct TwTmem32 {
+  uint32_t ta;          // this thread's TMEM address (lane quadrant | warp's column block)
+  mutable float h[2][16];
+  // stage 1 (radix 32): w^r, r = 1..31, k0 = (j % 32) * 16, columns 2(r-1), 2(r-1)+1
+  // stage 2 (radix 16, butterflies b = 0, 1): w^r, r = 1..15, k0 = j + 512 b, columns
+  // 64 + 32 b + 2(r-1), +1
+  __device__ __forceinline__ void fill(const cpx<float>* __restrict__ tw, int j) const {
+    float f[16];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        int k;   // power index of complex column slot c*8 + q
+        if (c < 4) {
+          const int r = c * 8 + q + 1;
+          k = (r <= 31) ? ((j & 31) * 16) * r : 0;
+        } else {
+          const int b = (c - 4) >> 1, r = ((c - 4) & 1) * 8 + q + 1;
+          k = (r <= 15) ? (j + 512 * b) * r : 0;
+        }
+        const cpx<float> w = tw[k & 16383];
+        f[2 * q] = w.x;
+        f[2 * q + 1] = w.y;
+      }
+      tmem_st16(ta + (uint32_t)(16 * c), f);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  __device__ __forceinline__ void ld(int chunk, int buf) const {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(ta + (uint32_t)(16 * chunk))
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) h[buf][i] = __uint_as_float(r[i]);
+  }
+  __device__ __forceinline__ void wait() const { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+  // u[r0 + q] *= (complex q of buffer buf), q < cnt
+  template <int R0, int CNT>
+  __device__ __forceinline__ void mul(cpx<float>* u, int buf) const {
+#pragma unroll
+    for (int q = 0; q < CNT; ++q) u[R0 + q] = cmul(u[R0 + q], cpx<float>{h[buf][2 * q], h[buf][2 * q + 1]});
+  }
+};
+template <class TW>
+struct IsR32 : std::false_type {};
+template <>
+struct IsR32<TwTmem32> : std::true_type {};
+
+__device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
+
+template <int X0, int V, class E>
+__device__ __forceinline__ void line_fft_r32(cpx<float> (&v)[V][16], int j, const TwTmem32& tw, const E& ex) {
+  static_assert(V == 2, "N = 16384 at 512 threads");
+  constexpr int TL = 512;
+  cpx<float>* buf0 = ex.template b<X0>();
+  cpx<float>* buf1 = ex.template b<X0 + 1>();
+  cpx<float> u[32];
+  // ---- stage 0: radix 32 on elements j + 512 r (no twiddles), outputs to 32 j + r
+#pragma unroll
+  for (int r = 0; r < 32; ++r) u[r] = v[r & 1][r >> 1];
+  dft32(u);
+  ex.template before_write<X0>();
+  {
+    cpx<float>* wb = buf0 + pad32(32 * j);
+#pragma unroll
+    for (int r = 0; r < 32; ++r) wb[r + (r >> 5)] = u[r];
+  }
+  tw.ld(0, 0);   // stage 1's first twiddle chunk
+  ex.template sync<X0>();
+  ex.template after_barrier<X0>();
+  {
+    const cpx<float>* rb = buf0 + pad32(j);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) u[k] = rb[k * (TL + TL / 32)];
+  }
+  if constexpr (!E::kDouble) __syncthreads();
+  // ---- stage 1: radix 32, Ns = 32: twiddles w^r (k0 = (j % 32) 16), outputs to
+  //      (j / 32) 1024 + j % 32 + 32 r
+  tw.wait();
+  tw.ld(1, 1);
+  tw.template mul<1, 8>(u, 0);
+  tw.wait();
+  tw.ld(2, 0);
+  tw.template mul<9, 8>(u, 1);
+  tw.wait();
+  tw.ld(3, 1);
+  tw.template mul<17, 8>(u, 0);
+  tw.wait();
+  tw.template mul<25, 7>(u, 1);
+  dft32(u);
+  ex.template before_write<X0 + 1>();
+  {
+    const int idxD = (j >> 5) * 1024 + (j & 31);
+    cpx<float>* wb = buf1 + pad32(idxD);
+#pragma unroll
+    for (int r = 0; r < 32; ++r) wb[r * 33] = u[r];
+  }
+  tw.ld(4, 0);   // stage 2, butterfly 0, powers 1..8
+  ex.template sync<X0 + 1>();
+  ex.template after_barrier<X0 + 1>();
+  {
+    const cpx<float>* rb = buf1 + pad32(j);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) u[k] = rb[k * (TL + TL / 32)];
+  }
+  if constexpr (!E::kDouble) __syncthreads();
+  // ---- stage 2 (last): radix 16, Ns = 1024, butterflies b = 0, 1 on elements
+  //      j + 512 b + 1024 r (slots b + 2 r), twiddles k0 = j + 512 b; outputs in place
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    cpx<float> w[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) w[r] = u[b + 2 * r];
+    tw.wait();
+    tw.ld(5 + 2 * b, 1);
+    tw.template mul<1, 8>(w, 0);
+    tw.wait();
+    if (b == 0) tw.ld(6, 0);
+    tw.template mul<9, 7>(w, 1);
+    dft<16>(w);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) u[b + 2 * r] = w[r];
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k & 1][k >> 1] = u[k];
+}
+
 template <typename T, int LOG2N, int X0, int V, class E, class TW>
 __device__ __forceinline__ void line_fft_v(cpx<T> (&v)[V][16], const int (&jv)[V], const TW (&tw)[V], const E& ex) {
-  FftStagesV<T, LOG2N, 0, FftInfo<LOG2N>::NS, X0, V, E, TW>::run(v, jv, tw, ex);
+  if constexpr (IsR32<TW>::value) {
+    static_assert(LOG2N == 14, "radix-32 schedule: N = 16384");
+    line_fft_r32<X0>(v, jv[0], tw[0], ex);
+  } else {
+    FftStagesV<T, LOG2N, 0, FftInfo<LOG2N>::NS, X0, V, E, TW>::run(v, jv, tw, ex);
+  }
 }
 
 template <int V, typename T>
@@ -1570,7 +1762,7 @@ template <typename T, int LOG2N, int MODE, int V, class E, class TW>
 __device__ __forceinline__ void pass_body_v(cpx<T> (&v)[V][16], const int (&jv)[V], const TW (&tw)[V],
                                             const PassArgs& a, uint64_t l, const E& ex) {
   constexpr int TL = (1 << LOG2N) / 16;
-  constexpr int NX = FftInfo<LOG2N>::NX;
+  constexpr int NX = IsR32<TW>::value ? 2 : FftInfo<LOG2N>::NX;   // exchanges per FFT
   const T scale = (T)a.scale;
   auto chirp = [&](const Phase& ph, auto conj_in, auto do_scale, int sign_mode) {
 #pragma unroll
@@ -1620,9 +1812,11 @@ __device__ __forceinline__ void pass_body_v(cpx<T> (&v)[V][16], const int (&jv)[
 }
 
 // ---------------------------------------------------------------------------------
-// N = 16384 cluster-pair line pass with 512 threads x 2 virtual threads (V = 2): the same
-// algorithm, layout and output protocol as line_pass_pair_kernel below (which runs 1024
-// threads at 64 registers and spills in its two-FFT passes), with 128 registers per thread.
+// N = 16384 cluster-pair line pass, 512 threads holding 32 elements each (the V = 2
+// register view): the pair-interleaved layout of line_pass_pair_kernel below, the
+// radix-32 line FFT (line_fft_r32: 2 exchanges per FFT, twiddle powers in tensor memory,
+// no spills at 128 registers), and for the transposing passes the output staged in
+// segment order (local + DSMEM stores) and written by TMA tensor stores.
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -1674,16 +1868,31 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
   const long long cl = blockIdx.x / 2;
   const cpx<T>* __restrict__ tw = reinterpret_cast<const cpx<T>*>(a.tw);
   const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in);
-  TwSet<T, LOG2N> tws[V];
-#pragma unroll
-  for (int t = 0; t < V; ++t) tws[t].load(tw, jv[t]);
+  // radix-32 schedule (line_fft_r32), twiddle powers in tensor memory
+  uint32_t* s_taddr = reinterpret_cast<uint32_t*>(smem_raw + (size_t)LS * sizeof(cpx<T>));
+  const int warp = tid >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_taddr)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *s_taddr;
+  TwTmem32 tws[V];
+  tws[0].ta = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 128);
+  tws[0].fill(tw, tid);
+  tws[1].ta = tws[0].ta;
   uint64_t ra[2];
 #pragma unroll
   for (int r = 0; r < 2; ++r)
     asm volatile("mapa.u64 %0, %1, %2;" : "=l"(ra[r]) : "l"(reinterpret_cast<uint64_t>(buf)), "r"(r));
   const cpx<T>* b0 = reinterpret_cast<const cpx<T>*>(ra[0]);
   const cpx<T>* b1 = reinterpret_cast<const cpx<T>*>(ra[1]);
-  constexpr bool kTmaOut = !SLAB && !ModeIO<MODE>::kStraightOut;
+  // transposing passes write through TMA tensor stores (batched, and row slabs unless the
+  // exchange is fused into peer stores)
+  constexpr bool kTmaOut = !ModeIO<MODE>::kStraightOut;
+  const bool tma_out = kTmaOut && (!SLAB || !a.peer_on);
   uint32_t pbuf_u32;   // the partner's buffer, shared::cluster address
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(pbuf_u32) : "r"(smem_u32(buf)), "r"(c ^ 1u));
   const bool contiguous = !SLAB || ModeIO<MODE>::kUserIn || C == N;
@@ -1745,14 +1954,15 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
     }
 
     cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * slab_elems;
-    if constexpr (kTmaOut) {
-      // Output through TMA (batched transposed passes): the 32-byte segments
+    if (tma_out) {
+      // Output through TMA (transposing passes): the 32-byte segments
       // [lp: i, i+1 | lp+1: i, i+1] of element pairs i in half h of the line are staged in
       // CTA h's buffer (segment q - h N/4 of q = i/2), each CTA storing its own line's
       // elements locally or into the partner's buffer (DSMEM stores), then each CTA writes
-      // its N/4 segments with tensor stores (map: make_store_map with G = 2).  Both CTAs'
-      // exchange buffers are free (ExPad ends every exchange with a CTA barrier) once the
-      // cluster barrier below is passed.
+      // its N/4 segments with tensor stores (maps: make_store_map with G = 2; row slabs:
+      // make_slab_store_map, rows of block s = q / (L/2)).  Both CTAs' exchange buffers are
+      // free (ExPad ends every exchange with a CTA barrier) once the cluster barrier below is
+      // passed.
       cluster_sync_all();
 #pragma unroll
       for (int t = 0; t < V; ++t)
@@ -1771,9 +1981,18 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
       cluster_sync_all();                                 // both halves of every segment staged
       if (tid == 0) {
         const int lp = ll & ~1;
+        if constexpr (SLAB) {
+          const int box = (L / 2) < 256 ? (L / 2) : 256;
 #pragma unroll 1
-        for (int r0 = 0; r0 < N / 4; r0 += 256)
-          tensor_s2g_4d(&omap, buf + 4 * r0, 0, (int)c * (N / 4) + r0, lp >> 1, (int)img);
+          for (int r0 = 0; r0 < N / 4; r0 += box) {
+            const int q = (int)c * (N / 4) + r0;
+            tensor_s2g_5d(&omap, buf + 4 * r0, 0, q & (L / 2 - 1), (lp & (Lc - 1)) >> 1, lp >> lgLc, q >> (lgL - 1));
+          }
+        } else {
+#pragma unroll 1
+          for (int r0 = 0; r0 < N / 4; r0 += 256)
+            tensor_s2g_4d(&omap, buf + 4 * r0, 0, (int)c * (N / 4) + r0, lp >> 1, (int)img);
+        }
         bulk_commit();
       }
     } else if constexpr (ModeIO<MODE>::kStraightOut) {
@@ -1813,9 +2032,10 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
       asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
     }
   }
-  if constexpr (kTmaOut) {
-    if (tid == 0) bulk_wait0();
-  }
+  if (tma_out && tid == 0) bulk_wait0();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
 }
 
 // ---------------------------------------------------------------------------------

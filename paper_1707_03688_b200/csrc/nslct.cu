@@ -81,6 +81,7 @@ cudaError_t launch_pair(const PassArgs& a, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair_kernel<float, LOG2N, MODE, SLAB>, a);
 }
 nslct_status make_store_map(CUtensorMap* m, void* out, int log2n, long long images);
+nslct_status make_slab_store_map(CUtensorMap* m, void* out, int log2n, long long L, long long Lc);
 // N = 16384: 512 threads x 2 virtual threads (kernels.cuh line_pass_pair2_kernel); the
 // batched transposing passes write through TMA tensor stores (map of the pair-interleaved
 // output, G = 2)
@@ -89,15 +90,17 @@ cudaError_t launch_pair2(const PassArgs& a, cudaStream_t s) {
   using Cfg = nslct::LineCfg<14>;
   CUtensorMap map;
   std::memset(&map, 0, sizeof(map));
-  if (!SLAB && !nslct::ModeIO<MODE>::kStraightOut &&
-      make_store_map(&map, a.out, 14, a.n_lines >> 14) != NSLCT_OK)
-    return cudaErrorInvalidValue;
+  if (!nslct::ModeIO<MODE>::kStraightOut) {
+    if (!SLAB && make_store_map(&map, a.out, 14, a.n_lines >> 14) != NSLCT_OK) return cudaErrorInvalidValue;
+    if (SLAB && !a.peer_on && make_slab_store_map(&map, a.out, 14, a.lines_per_img, a.out_chunk) != NSLCT_OK)
+      return cudaErrorInvalidValue;
+  }
   cudaLaunchConfig_t cfg = {};
   long long grid = a.persist_ctas > 0 ? a.persist_ctas : a.n_lines;
   if (grid > a.n_lines) grid = a.n_lines;
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(nslct::kPair2Threads);
-  cfg.dynamicSmemBytes = (size_t)Cfg::LS * sizeof(nslct::cpx<float>);
+  cfg.dynamicSmemBytes = (size_t)Cfg::LS * sizeof(nslct::cpx<float>) + 16;   // + the TMEM address slot
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -112,7 +115,7 @@ template <int MODE, bool SLAB>
 cudaError_t set_attr_pair2() {
   using Cfg = nslct::LineCfg<14>;
   return cudaFuncSetAttribute(nslct::line_pass_pair2_kernel<MODE, SLAB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(Cfg::LS * sizeof(nslct::cpx<float>)));
+                              (int)(Cfg::LS * sizeof(nslct::cpx<float>) + 16));
 }
 template <bool SLAB>
 struct Pair2Row {
@@ -262,6 +265,25 @@ nslct_status make_store_map(CUtensorMap* m, void* out, int log2n, long long imag
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(NSLCT_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return NSLCT_OK;
+}
+
+// Tensor map of a row-slab transposing pass's output as the N = 16384 pair kernel's TMA
+// stores see it (kernels.cuh line_pass_pair2_kernel; layout in PassArgs): 5D view
+// {32-byte segment (8 floats), consumer line pair lam/2 (row, 2 Lc elements), producer
+// line pair within the sub-block (32 B), sub-block (L Lc elements), block s (L^2)};
+// box = one segment x min(L/2, 256) rows.
+nslct_status make_slab_store_map(CUtensorMap* m, void* out, int log2n, long long L, long long Lc) {
+  auto fn = encode_tiled();
+  if (!fn) return fail(NSLCT_E_CUDA, "cuTensorMapEncodeTiled entry point not available");
+  const cuuint64_t n = 1ull << log2n;
+  const cuuint64_t dims[5] = {8, (cuuint64_t)L / 2, (cuuint64_t)Lc / 2, (cuuint64_t)(L / Lc), n / (cuuint64_t)L};
+  const cuuint64_t strides[4] = {(cuuint64_t)Lc * 16, 32, (cuuint64_t)(L * Lc) * 8, (cuuint64_t)(L * L) * 8};
+  const cuuint32_t box[5] = {8, (cuuint32_t)(L / 2 < 256 ? L / 2 : 256), 1, 1, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NSLCT_E_CUDA, "cuTensorMapEncodeTiled (slab store) failed (" + std::to_string((int)r) + ")");
   return NSLCT_OK;
 }
 
