@@ -1049,6 +1049,9 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait_read1() {   // all but the most recent bulk group read out
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -1077,7 +1080,11 @@ struct PipeCfg {
   // padded line stride of the exchange layout (index i + i/16): LS = 16/G (mod 16) so
   // the G lines read together hit distinct banks
   static constexpr int LS = N + N / 16 + ((G >= 16) ? 1 : 16 / G);
-  static constexpr int BUF_ELEMS = ((G * LS + 15) / 16) * 16;   // >= G*N (TMA staging)
+  // user-row lines land LSU apart: a bulk copy's destination must be 16-byte aligned, so LS
+  // rounded up to even (N <= 512: odd LS; the first read of such a group is 2-way
+  // bank-conflicted, the exchanges keep LS)
+  static constexpr int LSU = LS + (LS & 1);
+  static constexpr int BUF_ELEMS = ((G * LSU + 15) / 16) * 16;   // >= G*N (TMA staging)
   static constexpr int ROWS = N / IL;                           // output rows per group (transposed)
   static constexpr int BOX_ROWS = ROWS < 256 ? ROWS : 256;      // tensor-store box height
   static_assert(G % IL == 0, "pipe kernels need an even number of lines per group");
@@ -1103,7 +1110,7 @@ __device__ __forceinline__ void load_group(cpx<T>* dst, const cpx<T>* src, uint6
   mbar_expect_tx(bar, Cfg::G * LINE_BYTES);
   if constexpr (ModeIO<MODE>::kUserIn) {
 #pragma unroll
-    for (int ll = 0; ll < Cfg::G; ++ll) bulk_g2s(dst + ll * Cfg::LS, src + ll * Cfg::N, LINE_BYTES, bar);
+    for (int ll = 0; ll < Cfg::G; ++ll) bulk_g2s(dst + ll * Cfg::LSU, src + ll * Cfg::N, LINE_BYTES, bar);
   } else {
     bulk_g2s(dst, src, Cfg::G * LINE_BYTES, bar);
   }
@@ -1199,7 +1206,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int e = (q & 3) * 4 + (q >> 2);
-        v[e] = sb[gl * LS + j + TL * e];
+        v[e] = sb[gl * Cfg::LSU + j + TL * e];
       }
     } else {                     // pair-interleaved intermediate
       const cpx<T>* src = sb + (gl / IL) * (IL * N) + (gl % IL);
@@ -1439,7 +1446,7 @@ line_pass_ws_kernel(PassArgs a, long long n_groups, unsigned long long* counter,
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int e = (q & 3) * 4 + (q >> 2);
-        v[e] = sb[gl * LS + j + TL * e];
+        v[e] = sb[gl * Cfg::LSU + j + TL * e];
       }
     } else {
       const cpx<T>* src = sb + (gl / IL) * (IL * N) + (gl % IL);
@@ -1825,15 +1832,31 @@ __device__ __forceinline__ void cluster_sync_relaxed() {
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 constexpr int kPair2Threads = 512;
-// ExPad whose first exchange write of a line waits until the TMA store of the previous
-// line's output (staged in the same buffer) has been read out of shared memory.
+// Output staging of the N = 16384 pair kernel (segment order, 4 complex per 32-byte
+// segment, N/4 segments = 16 tensor-store boxes of 256 per CTA): the first kStageXBoxes
+// boxes in the exchange buffer, the rest in the shared memory behind it, so only the first
+// part of the previous line's store has to be read out before the next line's first
+// exchange write.
+constexpr int kPair2LS = 16384 + 16384 / 16 + 1;      // exchange buffer (complex), as LineCfg<14>::LS
+constexpr int kStageXBoxes = 9;                       // boxes staged in the exchange buffer
+constexpr size_t kPair2XtraOff = ((size_t)kPair2LS * 8 + 16 + 127) / 128 * 128;   // byte offset of the rest
+constexpr size_t kPair2Smem = kPair2XtraOff + (size_t)(16 - kStageXBoxes) * 256 * 32;
+// <= 196 KB: the next shared-memory carve-out step (228 KB) would shrink L1 to 28 KB, and
+// the per-thread line loads need L1 room for their requests in flight
+static_assert(kPair2Smem <= 196 * 1024, "pair2 shared memory");
+constexpr size_t kPair2SmemSmall = (size_t)kPair2LS * 8 + 16;   // straight-out passes (no staging)
+// per-thread line loads (plain: an L1::no_allocate variant measured 3% slower)
+__device__ __forceinline__ cpx<float> ldg_stream(const cpx<float>* p) { return *p; }
+// ExPad whose first exchange write of a line waits until the TMA stores of the previous
+// line's output staged in the exchange buffer (the older of its two bulk groups) have been
+// read out of shared memory.
 template <typename T>
 struct ExPadTmaOut : ExPad<T> {
   int tid;
   template <int X>
   __device__ __forceinline__ void before_write() const {
     if constexpr (X == 0) {
-      if (tid == 0) bulk_wait_read0();
+      if (tid == 0) bulk_wait_read1();
       __syncthreads();
     }
   }
@@ -1847,7 +1870,7 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
   using T = float;
   constexpr int LOG2N = 14;
   constexpr int N = 1 << LOG2N, TL = N / 16, THREADS = kPair2Threads, V = TL / THREADS;
-  constexpr int LS = N + N / 16 + 1;   // as LineCfg<14>::LS (G = 1)
+  constexpr int LS = kPair2LS;
   static_assert(V == 2, "two virtual threads");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   cpx<T>* buf = reinterpret_cast<cpx<T>*>(smem_raw);
@@ -1921,19 +1944,19 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
       if constexpr (ModeIO<MODE>::kUserIn) {
         const cpx<T>* src = in + line * N + j;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) v[t][e] = src[TL * e];
+        for (int e = 0; e < 16; ++e) v[t][e] = ldg_stream(src + TL * e);
       } else {
         const cpx<T>* src = in + img * slab_elems + (long long)(ll / 2) * 2 * C + (ll % 2);
         if constexpr (SLAB) {
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             const int i = j + TL * e;
-            v[t][e] = src[((long long)(i >> lgC) << (lgL + lgC)) + 2 * (i & (C - 1))];
+            v[t][e] = ldg_stream(src + ((long long)(i >> lgC) << (lgL + lgC)) + 2 * (i & (C - 1)));
           }
         } else {
           src += 2 * j;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) v[t][e] = src[2 * TL * e];
+          for (int e = 0; e < 16; ++e) v[t][e] = ldg_stream(src + 2 * TL * e);
         }
       }
     }
@@ -1963,37 +1986,53 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
       // make_slab_store_map, rows of block s = q / (L/2)).  Both CTAs' exchange buffers are
       // free (ExPad ends every exchange with a CTA barrier) once the cluster barrier below is
       // passed.
+      // (both CTAs' staging areas behind the exchange buffer are free: the previous line's
+      // stores from there have been read out)
+      if (tid == 0) bulk_wait_read0();
       cluster_sync_all();
+      // staged element s (0 .. N/2) of this CTA: exchange buffer below kStageXBoxes boxes,
+      // the area behind it above
+      constexpr int SX = kStageXBoxes * 256 * 4;
+      constexpr uint32_t XOFF = (uint32_t)(kPair2XtraOff / 8) - SX;   // element offset of s >= SX
 #pragma unroll
       for (int t = 0; t < V; ++t)
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int i = jv[t] + TL * e;                 // element (jv < TL: half = e / 8)
-          const int idx = (((i & (N / 2 - 1)) >> 1) << 2) | ((int)c << 1) | (i & 1);
+          int idx = (((i & (N / 2 - 1)) >> 1) << 2) | ((int)c << 1) | (i & 1);
+          idx += (idx >= SX) ? (int)XOFF : 0;
           if ((e >> 3) == (int)c) {
             buf[idx] = v[t][e];
           } else {
             st_cluster_v2(pbuf_u32 + (uint32_t)idx * 8u, v[t][e]);
           }
         }
-      if (more) load_line(p + ncl, v);
       asm volatile("fence.proxy.async;" ::: "memory");   // generic (local + remote) writes -> TMA
-      cluster_sync_all();                                 // both halves of every segment staged
+      // both halves of every segment staged; the next line's loads are issued between the
+      // arrive (release: would wait for them) and the wait
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+      if (more) load_line(p + ncl, v);
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
       if (tid == 0) {
         const int lp = ll & ~1;
-        if constexpr (SLAB) {
-          const int box = (L / 2) < 256 ? (L / 2) : 256;
+        // boxes in the exchange buffer first (bulk group 1, waited for by the next line's
+        // first exchange), then the rest (group 2, waited for before the next staging)
 #pragma unroll 1
-          for (int r0 = 0; r0 < N / 4; r0 += box) {
-            const int q = (int)c * (N / 4) + r0;
-            tensor_s2g_5d(&omap, buf + 4 * r0, 0, q & (L / 2 - 1), (lp & (Lc - 1)) >> 1, lp >> lgLc, q >> (lgL - 1));
+        for (int bx = 0; bx < 16; ++bx) {
+          const int r0 = bx * 256;
+          const cpx<T>* src = buf + 4 * r0 + (bx >= kStageXBoxes ? (int)XOFF : 0);
+          if constexpr (SLAB) {
+            const int box = (L / 2) < 256 ? (L / 2) : 256;
+            for (int rr = 0; rr < 256; rr += box) {
+              const int q = (int)c * (N / 4) + r0 + rr;
+              tensor_s2g_5d(&omap, src + 4 * rr, 0, q & (L / 2 - 1), (lp & (Lc - 1)) >> 1, lp >> lgLc,
+                            q >> (lgL - 1));
+            }
+          } else {
+            tensor_s2g_4d(&omap, src, 0, (int)c * (N / 4) + r0, lp >> 1, (int)img);
           }
-        } else {
-#pragma unroll 1
-          for (int r0 = 0; r0 < N / 4; r0 += 256)
-            tensor_s2g_4d(&omap, buf + 4 * r0, 0, (int)c * (N / 4) + r0, lp >> 1, (int)img);
+          if (bx == kStageXBoxes - 1 || bx == 15) bulk_commit();
         }
-        bulk_commit();
       }
     } else if constexpr (ModeIO<MODE>::kStraightOut) {
       asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
