@@ -1491,81 +1491,11 @@ line_pass_ws_kernel(PassArgs a, long long n_groups, unsigned long long* counter,
 }
 
 // ---------------------------------------------------------------------------------
-// V "virtual threads" per thread: the same radix-16 Stockham line FFT and pass body, with
-// each physical thread holding the 16-element register lines of V logical threads
-// j = jv[0..V-1] (elements j + TL e).  Every stage runs the butterflies of all V before the
-// exchange barrier, so the barrier count per line is that of the V = 1 code while the
-// line is held by V times fewer threads (more registers per thread: the N = 16384 pass
-// at 512 threads has 128 registers instead of 64 at 1024 threads).
+// V "virtual threads" per thread: each physical thread holds the 16-element register lines
+// of V logical threads j = jv[0..V-1] (elements j + TL e), so chirps, loads and stores are
+// those of the 16-element code while the line is held by V times fewer threads (the
+// N = 16384 pass: 512 threads, 128 registers).  Its line FFT is line_fft_r32 below.
 // ---------------------------------------------------------------------------------
-template <typename T, int LOG2N, int STAGE, int NS, int X, int V, class E, class TW>
-__device__ __forceinline__ void fft_stage_v(cpx<T> (&v)[V][16], const int (&jv)[V], const TW (&tw)[V], const E& ex) {
-  constexpr int N = 1 << LOG2N;
-  constexpr int TL = N / 16;
-  constexpr int NFULL = LOG2N / 4;
-  constexpr int R = (STAGE < NFULL) ? 16 : (1 << (LOG2N % 4));
-  constexpr int NB = 16 / R;
-  constexpr bool LAST = (STAGE == NS - 1);
-  constexpr int Ns = (STAGE < NFULL) ? (1 << (4 * STAGE)) : (1 << (4 * NFULL));
-  static_assert(E::kPadded && TL % 16 == 0, "padded fast exchange addressing");
-  cpx<T>* buf = ex.template b<X>();
-  constexpr int PW = E::kPadW;
-  constexpr int WSTEP = (Ns >= 16) ? Ns + PW * Ns / 16 : Ns;
-  constexpr int RSTEP = TL + PW * TL / 16;
-#pragma unroll
-  for (int t = 0; t < V; ++t) {
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int jp = jv[t] + b * TL;
-      cpx<T> u[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) u[r] = v[t][b + r * NB];
-      if constexpr (Ns > 1) tw[t].template apply<STAGE, R>(u, b, jp);
-      dft<R>(u);
-#pragma unroll
-      for (int r = 0; r < R; ++r) v[t][b + r * NB] = u[r];
-      if constexpr (!LAST) {
-        if (t == 0 && b == 0) ex.template before_write<X>();
-        const int idxD = (jp / Ns) * Ns * R + (jp % Ns);
-        cpx<T>* wb = buf + padw<PW>(idxD);
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const int r = (R == 16) ? ((q & 3) * 4 + (q >> 2)) : q;
-          wb[r * WSTEP] = u[r];
-        }
-      }
-    }
-  }
-  if constexpr (!LAST) {
-#pragma unroll
-    for (int t = 0; t < V; ++t) tw[t].template prefetch<STAGE + 1>();
-    ex.template sync<X>();
-    ex.template after_barrier<X>();
-#pragma unroll
-    for (int t = 0; t < V; ++t) {
-      const cpx<T>* rb = buf + padw<PW>(jv[t]);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int e = (q & 3) * 4 + (q >> 2);
-        v[t][e] = rb[e * RSTEP];
-      }
-    }
-    if constexpr (!E::kDouble) __syncthreads();
-  }
-}
-
-template <typename T, int LOG2N, int STAGE, int NS, int X0, int V, class E, class TW>
-struct FftStagesV {
-  __device__ __forceinline__ static void run(cpx<T> (&v)[V][16], const int (&jv)[V], const TW (&tw)[V], const E& ex) {
-    fft_stage_v<T, LOG2N, STAGE, NS, X0 + STAGE, V, E, TW>(v, jv, tw, ex);
-    FftStagesV<T, LOG2N, STAGE + 1, NS, X0, V, E, TW>::run(v, jv, tw, ex);
-  }
-};
-template <typename T, int LOG2N, int NS, int X0, int V, class E, class TW>
-struct FftStagesV<T, LOG2N, NS, NS, X0, V, E, TW> {
-  __device__ __forceinline__ static void run(cpx<T> (&)[V][16], const int (&)[V], const TW (&)[V], const E&) {}
-};
-
 // ---------------------------------------------------------------------------------
 // N = 16384 line FFT with radix-32 stages (32 x 32 x 16): 2 shared-memory exchanges per
 // FFT instead of the radix-16 schedule's 3 (16 x 16 x 16 x 4).  512 threads per line, the
@@ -1748,12 +1678,8 @@ __device__ __forceinline__ void line_fft_r32(cpx<float> (&v)[V][16], int j, cons
 
 template <typename T, int LOG2N, int X0, int V, class E, class TW>
 __device__ __forceinline__ void line_fft_v(cpx<T> (&v)[V][16], const int (&jv)[V], const TW (&tw)[V], const E& ex) {
-  if constexpr (IsR32<TW>::value) {
-    static_assert(LOG2N == 14, "radix-32 schedule: N = 16384");
-    line_fft_r32<X0>(v, jv[0], tw[0], ex);
-  } else {
-    FftStagesV<T, LOG2N, 0, FftInfo<LOG2N>::NS, X0, V, E, TW>::run(v, jv, tw, ex);
-  }
+  static_assert(IsR32<TW>::value && LOG2N == 14, "the V-thread passes run the radix-32 N = 16384 schedule");
+  line_fft_r32<X0>(v, jv[0], tw[0], ex);
 }
 
 template <int V, typename T>
@@ -1819,11 +1745,21 @@ __device__ __forceinline__ void pass_body_v(cpx<T> (&v)[V][16], const int (&jv)[
 }
 
 // ---------------------------------------------------------------------------------
-// N = 16384 cluster-pair line pass, 512 threads holding 32 elements each (the V = 2
-// register view): the pair-interleaved layout of line_pass_pair_kernel below, the
-// radix-32 line FFT (line_fft_r32: 2 exchanges per FFT, twiddle powers in tensor memory,
-// no spills at 128 registers), and for the transposing passes the output staged in
-// segment order (local + DSMEM stores) and written by TMA tensor stores.
+// N = 16384 line pass (complex64; batched plans and row slabs).  A line is 128 KB, so one
+// CTA holds ONE line and the pipe kernels' two-line groups do not fit: a CLUSTER of two
+// CTAs takes the two lines of a pair-interleaved group instead (element mu of line lambda
+// at (lambda/2) 2N + 2 mu + lambda%2; row slabs: the chunked sub-block form in PassArgs),
+// persistent (grid = the SMs, clusters stride the line pairs), each CTA prefetching its
+// next input into L2.  512 threads hold 32 elements each (the V = 2 register view);
+//   * input: coalesced per-thread loads of the CTA's line (the user's rows in the first
+//     pass; in the others every 8 B of 16, the partner reading the other 8 B of the same
+//     sectors at the same time), issued while the previous line's output is in flight;
+//   * the radix-32 line FFT (line_fft_r32: 2 exchanges per FFT, twiddle powers in tensor
+//     memory, no spills at 128 registers);
+//   * transposing passes: the 32-byte segments [l0: i, i+1 | l0+1: i, i+1] are staged in
+//     segment order (local + DSMEM stores), half of them in each CTA, and written by TMA
+//     tensor stores; straight-output passes store their row directly (in place in the
+//     batched schedule, after a cluster barrier).  DESIGN.md §6.2b.
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -2077,167 +2013,6 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
 }
 
-// ---------------------------------------------------------------------------------
-// Large-N line pass (N = 8192, 16384; complex64, batched plans): a line is 64-128 KB, so
-// one CTA holds ONE line (G = 1) and the persistent pipe kernels' group of two lines per
-// CTA does not fit.  A CLUSTER of two CTAs takes the two lines of a pair-interleaved
-// group instead; persistent (grid = the SMs, clusters stride the pairs), each CTA
-// prefetching its input of the next iteration into L2 while it computes (same intermediate layout as the pipe kernels: element mu of line
-// lambda at (lambda/2) 2N + 2 mu + lambda%2):
-//   * input: CTA c reads its line with coalesced per-thread loads (the user's rows in
-//     the first pass; in the others every 8 B of 16, the partner CTA reading the other 8 B
-//     of the same sectors at the same time, so DRAM moves each byte once);
-//   * output: each CTA stages its line in shared memory and, after a cluster barrier,
-//     writes the 32-byte segments [line 0: lambda, lambda+1 | line 1: lambda, lambda+1] of
-//     its half of the lambda pairs, reading the partner's two elements through DSMEM --
-//     full-sector writes, as the pipe kernels' TMA tensor stores (the G = 1
-//     line_pass_kernel wrote scattered 8-byte elements: 1.4 TB/s at N = 16384).
-// ---------------------------------------------------------------------------------
-template <typename T, int LOG2N, int MODE, bool SLAB>
-__global__ void __launch_bounds__(LineCfg<LOG2N>::THREADS)
-line_pass_pair_kernel(PassArgs a) {
-  using Cfg = LineCfg<LOG2N>;
-  constexpr int N = Cfg::N, TL = Cfg::TL, THREADS = Cfg::THREADS;
-  static_assert(Cfg::G == 1, "one line per CTA");
-  static_assert(sizeof(T) == 4, "complex64 (the 32-byte segments are 2 x float4)");
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  cpx<T>* buf = reinterpret_cast<cpx<T>*>(smem_raw);
-  uint32_t c;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(c));
-  const int tid = threadIdx.x;
-  const int j = tid;
-  // Layout (batched: L = C = N, one block per image; row slabs: L = N/P lines per rank,
-  // chunks of C = L elements, blocks of L x L -- the all-to-all's unit): element i of
-  // local line lam of image img sits at
-  //   img L N + (i / C) L C + (lam / 2) 2C + 2 (i % C) + lam % 2.
-  // batched plans: L = C = N at compile time (the 1024-thread kernel has 64 registers);
-  // slab plans: powers of two from the arguments, divisions as shifts
-  const int lgL = SLAB ? __ffs(a.lines_per_img) - 1 : LOG2N;
-  const int lgC = SLAB ? __ffs(a.in_chunk) - 1 : LOG2N;
-  const int L = 1 << lgL, C = 1 << lgC;
-  const long long slab_elems = (long long)L * N;
-  const long long npairs = a.n_lines / 2;   // this launch: local lines line_base + [0, n_lines)
-  const int lgLc = SLAB ? __ffs(a.out_chunk) - 1 : LOG2N;   // output sub-block width (PassArgs)
-  const int Lc = 1 << lgLc;
-  const long long ncl = gridDim.x / 2;              // persistent: clusters stride the pairs
-  const long long cl = blockIdx.x / 2;
-  const cpx<T>* __restrict__ tw = reinterpret_cast<const cpx<T>*>(a.tw);
-  const cpx<T>* __restrict__ in = reinterpret_cast<const cpx<T>*>(a.in);
-  TwSet<T, LOG2N> tws;
-  tws.load(tw, j);
-  uint64_t ra[2];
-#pragma unroll
-  for (int r = 0; r < 2; ++r)
-    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(ra[r]) : "l"(reinterpret_cast<uint64_t>(buf)), "r"(r));
-  const cpx<T>* b0 = reinterpret_cast<const cpx<T>*>(ra[0]);
-  const cpx<T>* b1 = reinterpret_cast<const cpx<T>*>(ra[1]);
-  // this CTA's input bytes of pair p when contiguous (its own row in the first pass, its
-  // half of the pair's interleaved block otherwise) -- prefetched into L2 one iteration
-  // ahead; chunked slab inputs are not prefetched
-  const bool contiguous = !SLAB || ModeIO<MODE>::kUserIn || C == N;
-  auto prefetch = [&](long long p) {
-    if (!SLAB || contiguous) {
-      const long long line = a.line_base + 2 * p + c;
-      const cpx<T>* src = ModeIO<MODE>::kUserIn ? in + line * N : in + (a.line_base + 2 * p) * N + (long long)c * N;
-      bulk_prefetch_l2(src, (uint32_t)(N * sizeof(cpx<T>)));
-    } else if constexpr (SLAB) {   // chunked (slab) input: the pair's 2C-element run in every
-                                   // block, CTA c taking every other block
-      const long long line = a.line_base + 2 * p;
-      const long long img = line / L;
-      const int lp = (int)(line % L);
-      for (int sb = (int)c; sb < N / C; sb += 2)
-        bulk_prefetch_l2(in + img * slab_elems + (long long)sb * L * C + (long long)(lp / 2) * 2 * C,
-                         (uint32_t)(2 * C * sizeof(cpx<T>)));
-    }
-  };
-  if (tid == 0 && cl < npairs) prefetch(cl);
-
-  // this CTA's line of pair p into registers (coalesced per-thread loads)
-  auto load_line = [&](long long p, cpx<T> (&v)[16]) {
-    const long long line = a.line_base + 2 * p + c;
-    const long long img = line >> lgL;
-    const int ll = (int)(line & (L - 1));
-    if constexpr (ModeIO<MODE>::kUserIn) {   // the user's row-major line
-      const cpx<T>* src = in + line * N + j;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = src[TL * e];
-    } else {                                  // pair-interleaved (chunked) intermediate
-      const cpx<T>* src = in + img * slab_elems + (long long)(ll / 2) * 2 * C + (ll % 2);
-      if constexpr (SLAB) {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int i = j + TL * e;
-          v[e] = src[((long long)(i >> lgC) << (lgL + lgC)) + 2 * (i & (C - 1))];
-        }
-      } else {   // one block per image: constant offsets
-        src += 2 * j;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) v[e] = src[2 * TL * e];
-      }
-    }
-  };
-  // The loads of the next pair are issued as soon as the current line has left the
-  // registers (staged in shared memory, or stored), so their latency overlaps the output
-  // phase (segment writes through DSMEM, cluster barriers) instead of stalling the next
-  // iteration's first FFT stage.
-  cpx<T> v[16];
-  if (cl < npairs) load_line(cl, v);
-  for (long long p = cl; p < npairs; p += ncl) {
-    if (tid == 0 && p + ncl < npairs) prefetch(p + ncl);
-    const long long line = a.line_base + 2 * p + c;   // over the batch
-    const long long img = line >> lgL;
-    const int ll = (int)(line & (L - 1));              // local line
-    const int l = a.line_offset + ll;                  // global line (chirps)
-    const bool more = p + ncl < npairs;
-    pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ExPad<T>{buf});
-
-    cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * slab_elems;
-    if constexpr (ModeIO<MODE>::kStraightOut) {
-      // in place in the batched schedule (the last pass writes where it read): rows 2p,
-      // 2p+1 ARE the pair's interleaved input block, so neither CTA may store before both
-      // have read it
-      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
-      cpx<T>* dst = out + (long long)ll * N;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) dst[j + TL * e] = v[e];
-      if (more) load_line(p + ncl, v);
-      __syncthreads();   // the next iteration's exchange reuses buf
-    } else {
-      __syncthreads();   // the FFT's last reads of buf are done
-#pragma unroll
-      for (int e = 0; e < 16; ++e) buf[pad16(j + TL * e)] = v[e];
-      // both CTAs' lines staged (release/acquire across the cluster)
-      asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-      // (issued after the release arrive, which would otherwise wait for them)
-      if (more) load_line(p + ncl, v);
-      const int lp = ll & ~1;   // local line 0 of the pair
-      // element pairs (e0, e0+1) in this CTA's half of the line: consumer lines
-      // lam = e0 % L, lam + 1 of block s = e0 / L; 32-byte segment [lp: lam, lam+1 |
-      // lp+1: lam, lam+1] at s L^2 + (lam / 2) 2L + 2 lp (in rank s's receive buffer at
-      // block offset peer_rank L^2 when the exchange is fused)
-      for (int q = (int)c * (N / 4) + tid; q < ((int)c + 1) * (N / 4); q += THREADS) {
-        const int e0 = 2 * q;
-        const cpx<T> a0 = b0[pad16(e0)], a1 = b0[pad16(e0 + 1)];
-        const cpx<T> c0 = b1[pad16(e0)], c1 = b1[pad16(e0 + 1)];
-        cpx<T>* d;
-        if constexpr (SLAB) {
-          const int sblk = e0 >> lgL, lam = e0 & (L - 1);
-          cpx<T>* base = a.peer_on ? reinterpret_cast<cpx<T>*>(a.peer_out[sblk]) + (long long)a.peer_rank * L * L
-                                   : out + (long long)sblk * L * L;
-          d = base + ((long long)(lp >> lgLc) << (lgL + lgLc)) + (long long)(lam / 2) * 2 * Lc + 2 * (lp & (Lc - 1));
-        } else {
-          d = out + (long long)q * 2 * N + 2 * lp;
-        }
-        reinterpret_cast<float4*>(d)[0] = make_float4(a0.x, a0.y, a1.x, a1.y);
-        reinterpret_cast<float4*>(d)[1] = make_float4(c0.x, c0.y, c1.x, c1.y);
-      }
-      // the partner may still read this CTA's buffer (next iteration / exit).  Relaxed
-      // arrive: the DSMEM loads above are complete (their values were stored), and a
-      // release would make every thread wait for its outstanding GLOBAL stores.
-      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------------
 // Large-N line pass, TMA-pipelined (N = 8192; complex64; batched and row-slab plans).

@@ -60,26 +60,6 @@ cudaError_t set_attr() {
                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-// large-N pair kernels (N = 8192, 16384, complex64): a 2-CTA cluster per line pair
-template <int LOG2N, int MODE, bool SLAB>
-cudaError_t launch_pair(const PassArgs& a, cudaStream_t s) {
-  using Cfg = nslct::LineCfg<LOG2N>;
-  cudaLaunchConfig_t cfg = {};
-  long long grid = a.persist_ctas > 0 ? a.persist_ctas : a.n_lines;   // persistent: one CTA per SM
-  if (grid > a.n_lines) grid = a.n_lines;
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(Cfg::THREADS);
-  cfg.dynamicSmemBytes = (size_t)Cfg::LS * sizeof(nslct::cpx<float>);
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair_kernel<float, LOG2N, MODE, SLAB>, a);
-}
 nslct_status make_store_map(CUtensorMap* m, void* out, int log2n, long long images);
 nslct_status make_slab_store_map(CUtensorMap* m, void* out, int log2n, long long L, long long Lc);
 // N = 16384: 512 threads x 2 virtual threads (kernels.cuh line_pass_pair2_kernel); the
@@ -125,22 +105,6 @@ struct Pair2Row {
     l[3] = launch_pair2<3, SLAB>; l[4] = launch_pair2<4, SLAB>; l[5] = launch_pair2<5, SLAB>;
     at[0] = set_attr_pair2<0, SLAB>; at[1] = set_attr_pair2<1, SLAB>; at[2] = set_attr_pair2<2, SLAB>;
     at[3] = set_attr_pair2<3, SLAB>; at[4] = set_attr_pair2<4, SLAB>; at[5] = set_attr_pair2<5, SLAB>;
-  }
-};
-template <int LOG2N, int MODE, bool SLAB>
-cudaError_t set_attr_pair() {
-  using Cfg = nslct::LineCfg<LOG2N>;
-  return cudaFuncSetAttribute(nslct::line_pass_pair_kernel<float, LOG2N, MODE, SLAB>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Cfg::LS * sizeof(nslct::cpx<float>)));
-}
-template <int LOG2N, bool SLAB>
-struct PairRow {
-  static void fill(launch_fn* l, attr_fn* at) {
-    l[0] = launch_pair<LOG2N, 0, SLAB>; l[1] = launch_pair<LOG2N, 1, SLAB>; l[2] = launch_pair<LOG2N, 2, SLAB>;
-    l[3] = launch_pair<LOG2N, 3, SLAB>; l[4] = launch_pair<LOG2N, 4, SLAB>; l[5] = launch_pair<LOG2N, 5, SLAB>;
-    at[0] = set_attr_pair<LOG2N, 0, SLAB>; at[1] = set_attr_pair<LOG2N, 1, SLAB>;
-    at[2] = set_attr_pair<LOG2N, 2, SLAB>; at[3] = set_attr_pair<LOG2N, 3, SLAB>;
-    at[4] = set_attr_pair<LOG2N, 4, SLAB>; at[5] = set_attr_pair<LOG2N, 5, SLAB>;
   }
 };
 
@@ -394,13 +358,8 @@ struct Table {
     li[1][5] = launch_img<double, 5, 1>, ati[1][5] = set_attr_img<double, 5, 1>;
     li[1][6] = launch_img<double, 6, 1>, ati[1][6] = set_attr_img<double, 6, 1>;
     li[1][7] = launch_img<double, 7, 4>, ati[1][7] = set_attr_img<double, 7, 4>;
-#ifdef NSLCT_AB_PAIR1
-    PairRow<14, false>::fill(lpair[0][14], atpair[0][14]);
-    PairRow<14, true>::fill(lpair[1][14], atpair[1][14]);
-#else
     Pair2Row<false>::fill(lpair[0][14], atpair[0][14]);
     Pair2Row<true>::fill(lpair[1][14], atpair[1][14]);
-#endif
     BigRow<13, false>::fill(lbig[0][13], atbig[0][13]);
     BigRow<13, true>::fill(lbig[1][13], atbig[1][13]);
     PipeRow<float, 10>::fill(lp[10], atp[10]);
