@@ -622,11 +622,29 @@ def measure_e2e(nslct, torch, dev, stream, n, batch, dtype, M, x, args, world, b
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t1)
         t_dir.append(min(ts))
-    del dbuf
+    # both directions at once (what the pipelined call needs: PCIe is full duplex, but the
+    # host memory system and the copy engines are shared)
+    dbuf2 = torch.empty_like(dbuf)
+    s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    ts = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        with torch.cuda.stream(s_in):
+            dbuf.copy_(hin, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            hout.copy_(dbuf2, non_blocking=True)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t1)
+    t_bidir = min(ts)
+    del dbuf, dbuf2
     return {"value": units / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(hin.numel() * S),
             "d2h_bytes_per_step": int(hout.numel() * S), "steps": nst,
             "h2d_gbs": hin.numel() * S / t_dir[0] / 1e9, "d2h_gbs": hout.numel() * S / t_dir[1] / 1e9,
             "pcie_bound_value": units / max(t_dir),
+            "pcie_bidir_gbs": 2 * hin.numel() * S / t_bidir / 1e9,
+            "pcie_bidir_bound_value": units / t_bidir,
+            "frac_of_bidir_bound": t_bidir / t_e2e,
             "how": "nslct_exec_host per rank: pinned host in -> device, passes, device -> pinned host out, "
                    "pipelined in ~64 MiB image chunks over two copy streams; wall clock per call, max over ranks"}
 
