@@ -690,6 +690,10 @@ struct Phase {
   // the anchors, the recurrence adds <= 14 fp32 roundings.
   float zr[8], zi[8];
   int rec;
+  // complex64 chirp structure (set by the host with rec): 0 general; 1 no element-quadratic
+  // step (dd = 0: Z_k = 1); 2 constant along the line (cB = cC = 0, cE TL = 0: one factor
+  // per thread and line)
+  int kind;
 };
 // conj(chirp of t) = chirp of -t
 __device__ __forceinline__ Phase neg_phase(Phase p) {
@@ -729,6 +733,32 @@ __device__ __forceinline__ void apply_chirp(cpx<T> (&v)[16], const Phase& ph, ui
   uint64_t d = gamma * (uint64_t)TL + 2ull * ph.cC * j * (uint64_t)TL + ph.cC * (uint64_t)TL * (uint64_t)TL;
   if constexpr (sizeof(T) == 4) {
     if (ph.rec) {   // anchors k = 0, 8; recurrences P <- P w (see struct Phase)
+      if (ph.kind == 2) {   // the same factor for the thread's 16 elements
+        const cpx<T> P = chirp_of<T>(t, SCALE ? scale : T(1));
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          cpx<T> x = v[k];
+          if (CONJ_IN) x = cconj(x);
+          v[k] = cmul(x, P);
+        }
+        return;
+      }
+      if (ph.kind == 1) {   // Z_k = 1
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          cpx<T> P = chirp_of<T>(t, SCALE ? scale : T(1));
+          const cpx<T> w = chirp_of<T>(d, T(1));
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            cpx<T> x = v[8 * h + m];
+            if (CONJ_IN) x = cconj(x);
+            v[8 * h + m] = cmul(x, P);
+            if (m < 7) P = cmul(P, w);
+          }
+          t += 8ull * d;
+        }
+        return;
+      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         cpx<T> P = chirp_of<T>(t, SCALE ? scale : T(1));

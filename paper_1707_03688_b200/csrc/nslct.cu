@@ -430,6 +430,9 @@ Poly chirp_poly(const nslct::Sym& q, double d, int n, bool checker) {
 // of complex64 chirps (kernels.cuh struct Phase).
 void set_rec(Phase* ph, int tl) {
   const uint64_t dd = 2ull * ph->cC * (uint64_t)tl * (uint64_t)tl;
+  // structure the kernel exploits (struct Phase::kind): constant along the line, or no
+  // element-quadratic step
+  ph->kind = (ph->cB == 0 && ph->cC == 0 && ph->cE * (uint64_t)tl == 0) ? 2 : (dd == 0) ? 1 : 0;
   for (int m = 0; m < 8; ++m) {
     const uint64_t t = (uint64_t)(m * (m - 1) / 2) * dd;
     const double ang = 2.0 * M_PI * ((double)(int64_t)t * 5.42101086242752217e-20);   // 2^-64 turns
@@ -437,6 +440,21 @@ void set_rec(Phase* ph, int tl) {
     ph->zi[m] = (float)std::sin(ang);
   }
   ph->rec = 1;
+}
+// complex64 plans: chirp coefficients whose largest phase over the N x N grid is below
+// kSnapRad are dropped (set to 0) -- far below the fp32 phase evaluation's own error (the
+// complex64 transform's relL2 against the oracle is ~2e-6), and it lets the kernels use the
+// cheaper chirp forms of struct Phase::kind.  The HA search often ends on such a point
+// (e.g. C4's Q4 has q12, q22 ~ 1e-11 next to q11 = -1.53: a chirp constant along each
+// line).  DESIGN.md §6.3.
+constexpr double kSnapRad = 1e-6;
+nslct::Sym snap_c64(nslct::Sym q, double d, int n) {
+  const double m2 = 0.25 * (double)n * (double)n * d * d;   // (n/2 d)^2: largest |z_a z_b|
+  auto cut = [&](double v, double w) { return std::fabs(v) * w * m2 < kSnapRad ? 0.0 : v; };
+  q.q11 = cut(q.q11, 0.5);
+  q.q22 = cut(q.q22, 0.5);
+  q.q12 = cut(q.q12, 1.0);
+  return q;
 }
 // roles: line index = i (x) or j (y)
 Phase to_phase(const Poly& P, bool line_is_x) {
@@ -1026,11 +1044,12 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
     // checkerboards S ride on the first and last chirps.  Bluestein DFTs are centred
     // by construction: no checkerboard.
     const bool ck = !pl->bluestein;
-    Poly P0 = chirp_poly(p.q_active[0] ? p.Q[0] : zero, dx, (int)n, ck);
-    Poly P1 = chirp_poly(p.Q[1], dw, (int)n, false);
-    Poly P2 = chirp_poly(p.Q[2], dx, (int)n, false);
-    Poly P3 = chirp_poly(p.Q[3], dw, (int)n, false);
-    Poly P4 = chirp_poly(p.q_active[4] ? p.Q[4] : zero, dx, (int)n, ck);
+    auto qs = [&](const nslct::Sym& q, double d) { return ti == 0 ? snap_c64(q, d, (int)n) : q; };
+    Poly P0 = chirp_poly(p.q_active[0] ? qs(p.Q[0], dx) : zero, dx, (int)n, ck);
+    Poly P1 = chirp_poly(qs(p.Q[1], dw), dw, (int)n, false);
+    Poly P2 = chirp_poly(qs(p.Q[2], dx), dx, (int)n, false);
+    Poly P3 = chirp_poly(qs(p.Q[3], dw), dw, (int)n, false);
+    Poly P4 = chirp_poly(p.q_active[4] ? qs(p.Q[4], dx) : zero, dx, (int)n, ck);
     const Phase ph[5] = {to_phase(P0, true), to_phase(P1, false), to_phase(P2, true),
                          to_phase(P3, false), to_phase(P4, true)};
     // inverse FFTs are unnormalised; the last pass applies 1/N^4 (two 2D inverses)
