@@ -1114,7 +1114,12 @@ struct PipeCfg {
   // rounded up to even (N <= 512: odd LS; the first read of such a group is 2-way
   // bank-conflicted, the exchanges keep LS)
   static constexpr int LSU = LS + (LS & 1);
+  // straight-output staging: line gl at gl * SLS, SLS = N + 16/G, so the G lines written
+  // together by a half-warp (lanes gl = 0..G-1 at 16/G consecutive j) hit distinct banks
+  // (at SLS = N they share banks: a G-way conflict); one bulk store per line
+  static constexpr int SLS = N + 16 / G;
   static constexpr int BUF_ELEMS = ((G * LSU + 15) / 16) * 16;   // >= G*N (TMA staging)
+  static_assert(G * SLS <= BUF_ELEMS, "straight staging fits the buffer");
   static constexpr int ROWS = N / IL;                           // output rows per group (transposed)
   static constexpr int BOX_ROWS = ROWS < 256 ? ROWS : 256;      // tensor-store box height
   static_assert(G % IL == 0, "pipe kernels need an even number of lines per group");
@@ -1284,7 +1289,7 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     // last exchange barrier.
     cpx<T>* ob = ODD ? sb : xb;
     if constexpr (ModeIO<MODE>::kStraightOut) {
-      cpx<T>* o = ob + gl * N;   // the G lines, contiguous as in the output
+      cpx<T>* o = ob + gl * Cfg::SLS;   // line gl staged SLS apart (bank-conflict free)
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int e = (q & 3) * 4 + (q >> 2);
@@ -1303,7 +1308,9 @@ line_pass_pipe_kernel(PassArgs a, long long n_groups, unsigned long long* counte
     __syncthreads();
     if (tid == 0) {
       if constexpr (ModeIO<MODE>::kStraightOut) {
-        bulk_s2g(out + line0 * N, ob, (uint32_t)(GE * sizeof(cpx<T>)));
+#pragma unroll
+        for (int ll = 0; ll < G; ++ll)
+          bulk_s2g(out + (line0 + ll) * N, ob + ll * Cfg::SLS, (uint32_t)(N * sizeof(cpx<T>)));
       } else {
         const int gi = (int)(g % (N / G)), img = (int)(g / (N / G));
 #pragma unroll 1
@@ -1427,7 +1434,9 @@ line_pass_ws_kernel(PassArgs a, long long n_groups, unsigned long long* counter,
       cpx<T>* ob = bufs + bx * BE;
       if (lead) {
         if constexpr (ModeIO<MODE>::kStraightOut) {
-          bulk_s2g(out + g * G * N, ob, (uint32_t)(GE * sizeof(cpx<T>)));
+#pragma unroll
+          for (int ll = 0; ll < G; ++ll)
+            bulk_s2g(out + (g * G + ll) * N, ob + ll * Cfg::SLS, (uint32_t)(N * sizeof(cpx<T>)));
         } else {
           const int gi = (int)(g % (N / G)), img = (int)(g / (N / G));
 #pragma unroll 1
@@ -1490,7 +1499,7 @@ line_pass_ws_kernel(PassArgs a, long long n_groups, unsigned long long* counter,
     pass_body<T, LOG2N, MODE>(v, j, tws, a, (uint64_t)l, ex);
     cpx<T>* ob = xb;   // even exchange count: the spare buffer is free
     if constexpr (ModeIO<MODE>::kStraightOut) {
-      cpx<T>* o = ob + gl * N;
+      cpx<T>* o = ob + gl * Cfg::SLS;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int e = (q & 3) * 4 + (q >> 2);
