@@ -144,12 +144,16 @@ class ClockSampler:
         self.f.seek(0)
         rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
         os.unlink(self.f.name)
-        sm, smax, reasons = [], 0.0, set()
+        sm, smax, reasons, pw = [], 0.0, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             try:
                 sm.append(float(r[1]))
                 smax = max(smax, float(r[2]))
+                try:
+                    pw.append(float(r[3]))
+                except Exception:
+                    pass
                 for nm, v in zip(names, r[5:9]):
                     if "Active" in v and "Not" not in v:
                         reasons.add(nm)
@@ -158,8 +162,10 @@ class ClockSampler:
         if not sm:
             return None
         sm.sort()
+        pw.sort()
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w_median": pw[len(pw) // 2] if pw else None,
+                "power_w_max": pw[-1] if pw else None}
 
 
 def traffic_from_profiles(cfg_id):

@@ -1637,6 +1637,11 @@ template <>
 struct IsR32<TwTmem32> : std::true_type {};
 
 __device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
+// exchange policies with a split read-out barrier (after_read arrives, the next write waits)
+template <class E, class = void>
+struct IsSplitEx : std::false_type {};
+template <class E>
+struct IsSplitEx<E, std::void_t<decltype(E::kSplit)>> : std::true_type {};
 
 template <int X0, int V, class E>
 __device__ __forceinline__ void line_fft_r32(cpx<float> (&v)[V][16], int j, const TwTmem32& tw, const E& ex) {
@@ -1663,7 +1668,8 @@ __device__ __forceinline__ void line_fft_r32(cpx<float> (&v)[V][16], int j, cons
 #pragma unroll
     for (int k = 0; k < 32; ++k) u[k] = rb[k * (TL + TL / 32)];
   }
-  if constexpr (!E::kDouble) __syncthreads();
+  if constexpr (IsSplitEx<E>::value) ex.template after_read<X0>();
+  else if constexpr (!E::kDouble) __syncthreads();
   // ---- stage 1: radix 32, Ns = 32: twiddles w^r (k0 = (j % 32) 16), outputs to
   //      (j / 32) 1024 + j % 32 + 32 r
   tw.wait();
@@ -1693,7 +1699,8 @@ __device__ __forceinline__ void line_fft_r32(cpx<float> (&v)[V][16], int j, cons
 #pragma unroll
     for (int k = 0; k < 32; ++k) u[k] = rb[k * (TL + TL / 32)];
   }
-  if constexpr (!E::kDouble) __syncthreads();
+  if constexpr (IsSplitEx<E>::value) ex.template after_read<X0 + 1>();
+  else if constexpr (!E::kDouble) __syncthreads();
   // ---- stage 2 (last): radix 16, Ns = 1024, butterflies b = 0, 1 on elements
   //      j + 512 b + 1024 r (slots b + 2 r), twiddles k0 = j + 512 b; outputs in place
 #pragma unroll
@@ -1828,8 +1835,23 @@ __device__ __forceinline__ cpx<float> ldg_stream(const cpx<float>* p) { return *
 template <typename T>
 struct ExPadTmaOut : ExPad<T> {
   int tid;
+  // The barrier after an exchange's reads (the single buffer is rewritten by the next
+  // exchange) is split: each warp arrives on an mbarrier once it has read its elements and
+  // only waits for the 16 arrivals before its NEXT exchange write, a butterfly stage later
+  // -- no warp waits for the others' reads.  The round after a pass's last exchange is not
+  // waited for (the cluster barriers before the output staging cover it).
+  static constexpr bool kSplit = true;
+  uint64_t* rd;
+  mutable uint32_t nrd;   // arrive rounds this thread has passed
+  template <int X>
+  __device__ __forceinline__ void after_read() const {
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(rd);
+    ++nrd;
+  }
   template <int X>
   __device__ __forceinline__ void before_write() const {
+    if constexpr (X > 0) mbar_wait(rd, (nrd - 1u) & 1u);
     if constexpr (X == 0) {
       if (tid == 0) bulk_wait_read1();
       __syncthreads();
@@ -1872,6 +1894,11 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_taddr)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  uint64_t* rd_bar = reinterpret_cast<uint64_t*>(smem_raw + (size_t)LS * sizeof(cpx<T>) + 8);
+  if (tid == 0) {
+    mbar_init(rd_bar, 16);
+    fence_mbar_init();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -1938,6 +1965,7 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
   };
   cpx<T> v[V][16];
   if (cl < npairs) load_line(cl, v);
+  const ExPadTmaOut<T> ex_tma{{buf}, tid, rd_bar, 0u};
   for (long long p = cl; p < npairs; p += ncl) {
     if (tid == 0 && p + ncl < npairs) prefetch(p + ncl);
     const long long line = a.line_base + 2 * p + c;
@@ -1946,7 +1974,7 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
     const int l = a.line_offset + ll;
     const bool more = p + ncl < npairs;
     if constexpr (kTmaOut) {
-      pass_body_v<T, LOG2N, MODE, V>(v, jv, tws, a, (uint64_t)l, ExPadTmaOut<T>{{buf}, tid});
+      pass_body_v<T, LOG2N, MODE, V>(v, jv, tws, a, (uint64_t)l, ex_tma);
     } else {
       pass_body_v<T, LOG2N, MODE, V>(v, jv, tws, a, (uint64_t)l, ExPad<T>{buf});
     }
@@ -1964,7 +1992,8 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
       // (both CTAs' staging areas behind the exchange buffer are free: the previous line's
       // stores from there have been read out)
       if (tid == 0) bulk_wait_read0();
-      cluster_sync_all();
+      // execution ordering only (the partner is past its last exchange reads): no release
+      cluster_sync_relaxed();
       // staged element s (0 .. N/2) of this CTA: exchange buffer below kStageXBoxes boxes,
       // the area behind it above
       constexpr int SX = kStageXBoxes * 256 * 4;
@@ -1982,7 +2011,7 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
             st_cluster_v2(pbuf_u32 + (uint32_t)idx * 8u, v[t][e]);
           }
         }
-      asm volatile("fence.proxy.async;" ::: "memory");   // generic (local + remote) writes -> TMA
+      asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");   // generic (local + remote) writes -> TMA
       // both halves of every segment staged; the next line's loads are issued between the
       // arrive (release: would wait for them) and the wait
       asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");

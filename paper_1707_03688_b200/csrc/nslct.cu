@@ -1157,6 +1157,9 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       // (the group this CTA most likely claims next).  Measured on the C4 bench (DESIGN.md
       // §6.6): K1 1.51 -> 1.32 ms, K2-K5 +0.5-1% -- so on the first pass only.
       if (pl->pipe) pl->args[0].l2_ahead = pl->num_sms;
+      // ... and on the last pass (one FFT + a chirp; K5 1.47 -> 1.37 ms at C4 since the chirps
+      // became cheaper, profiles/r02f_l2ahead_ab.txt)
+      if (pl->pipe) pl->args[pl->n_passes - 1].l2_ahead = pl->num_sms;
       // complex64 chirps by anchored rotation recurrences (kernels.cuh struct Phase) on
       // every pass: measured K5 1.71 -> 1.66 ms, K2-K4 -1.4..-2% on the C4 bench (DESIGN.md
       // §6.3)

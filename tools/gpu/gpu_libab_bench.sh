@@ -9,7 +9,7 @@ if [ -n "$PYTEST_K" ]; then
   timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -k "$PYTEST_K" > gpurun_out/${TAG}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_pytest.log
 fi
 for rep in $(seq $REPS); do
-  for f in alt/libnslct_*.so; do
+  for f in ${LIBS:-alt/libnslct_*.so}; do
     n=$(basename $f .so)
     NSLCT_LIB=$f timeout 600 python bench.py $ARGS > gpurun_out/${TAG}_${n}_${rep}.json 2> gpurun_out/${TAG}_${n}_${rep}.err
   done

@@ -8,7 +8,7 @@ if [ -n "$PYTEST_K" ]; then
   timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 -k "$PYTEST_K" > gpurun_out/${TAG}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${TAG}_pytest.log
 fi
 for rep in 1 2; do
-  for f in alt/libnslct_*.so; do
+  for f in ${LIBS:-alt/libnslct_*.so}; do
     n=$(basename $f .so)
     NSLCT_LIB=$f timeout 300 python tools/large_n_ab.py ${N:-16384} ${B:-1} 2>&1 | sed "s/^/$n $rep /" >> gpurun_out/${TAG}_large.txt
   done
