@@ -84,9 +84,11 @@ def test_planner_parity_with_oracle(variant):
         assert abs(d["objective"] - p["J"]) <= 1e-9 * p["J"]
         assert d["recomposition_residual"] <= 1e-9
         assert d["lc_axis"] == p["axis"]
-        if np.abs(d["h"] - p["h"]).max() < 1e-7:
-            for qc, qo in zip(d["Q"], _oracle_Q(p)):
-                assert np.abs(qc - qo).max() <= 1e-6 * max(1.0, np.abs(qo).max())
+        # both searches follow reading R5 and end on the same optimum (to the Nelder-Mead
+        # tolerance): H and every executed chirp agree, unconditionally
+        assert np.abs(d["h"] - p["h"]).max() < 1e-7, (d["h"], p["h"])
+        for qc, qo in zip(d["Q"], _oracle_Q(p)):
+            assert np.abs(qc - qo).max() <= 1e-6 * max(1.0, np.abs(qo).max())
 
 
 def test_fixed_h_reproduces_oracle_chain():
