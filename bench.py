@@ -511,7 +511,8 @@ def run_ours(args):
         ro, e2e, info = main["roofline"], None, None
         launches = main["launches"]
         cfg = {"workload": desc + ", row slabs of %d x %d per GPU" % (n // world, n), "n": n, "global_batch": 1,
-               "parallelism": "row-slab x%d: comm plan, %s" % (world, main["exchange"])}
+               "parallelism": "row-slab x%d: comm plan, %s" % (world, main["exchange"]),
+               "ms_by_exchange": main["ms_by_exchange"], "exchange_errors": main.get("errors")}
         scaling = "strong"
     else:
         if gbatch % world:
@@ -572,9 +573,11 @@ def run_ours(args):
     if not args.no_sub and world == 1 and args.config == 4:
         sub.update(sub_records(nslct, torch, dev, stream, peak, peak_src, fp32_peak, args))
     if not args.no_sub and world > 1 and args.config == 4:
-        mr5, _ = synth.config_streams(5)
-        sub["C5_slab"] = run_slab(args, nslct, torch, dev, stream, 16384, synth.random_symplectic(mr5), world,
-                                  rank, barrier, steps=max(5, args.steps // 2))
+        # C5 as row slabs over the same GPUs, in CHILD processes (one per rank, their own
+        # rendezvous): the comm plans have only ever run on one GPU, and a fault or a hang
+        # there must not cost the C4 line
+        port = int(max_over_ranks(_free_port() if rank == 0 else 0, world, dev))
+        sub["C5_slab"] = slab_child(args, world, rank, local, port)
 
     cpu, cpu_recs = None, None
     if rank == 0 and not args.no_cpu_baseline:
@@ -701,6 +704,34 @@ def sub_records(nslct, torch, dev, stream, peak, peak_src, fp32_peak, args):
     return out
 
 
+def slab_child(args, world, rank, local, port, timeout=300, extra=()):
+    """`bench.py --config 5 --gpus world` as a child of every rank (rank 0's child prints the
+    line, returned here as the sub-record); killed after `timeout` seconds.  Never raises."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+               LOCAL_RANK=str(local), WORLD_SIZE=str(world))
+    for k in [k for k in env if k.startswith("TORCHELASTIC_")]:
+        env.pop(k)   # the child ranks rendezvous among themselves (no agent store)
+    cmd = [sys.executable, os.path.abspath(__file__), "--config", "5", "--gpus", str(world),
+           "--steps", str(max(5, args.steps // 2)), "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--no-sub"]
+    cmd += list(extra)
+    try:
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout)
+    except subprocess.TimeoutExpired:
+        return {"error": "timeout after %d s (child killed)" % timeout}
+    except Exception as e:   # noqa: BLE001
+        return {"error": repr(e)}
+    if rank != 0:
+        return None
+    for line in reversed(r.stdout.strip().splitlines()):
+        try:
+            d = json.loads(line)
+            return {"value": d["value"], "ms": d["ms_per_step"], "n_gpus": d["n_gpus"], "steps": d["steps"],
+                    "config": d.get("config"), "roofline": d.get("roofline"), "launches": d.get("gpu_launches")}
+        except Exception:   # noqa: BLE001
+            continue
+    return {"error": "child rc=%d: %s" % (r.returncode, (r.stderr or r.stdout)[-400:])}
+
+
 def run_slab(args, nslct, torch, dev, stream, n, M, world, rank, barrier, steps=None):
     """C5: ONE n x n transform as row slabs over `world` GPUs through the library's comm
     plans (nslct_exec runs every pass and exchange): NCCL chunked send/recv and the fused
@@ -714,13 +745,26 @@ def run_slab(args, nslct, torch, dev, stream, n, M, world, rank, barrier, steps=
     x = torch.randn((L, n), dtype=torch.complex64, device=dev, generator=gen)
     out = torch.empty_like(x)
     comm = nslct.Communicator()
-    res = {}
+    res, errors, np_ = {}, {}, 5
     for exch in ("nccl", "peer"):
-        plan = nslct.Plan(n, M, 1, comm=comm, exchange=exch, device=dev.index)
+        # a plan-time failure (e.g. no CUDA IPC between the GPUs) is the same on every rank:
+        # record it and go on with the other exchange; the flag is agreed over the ranks
+        plan, err = None, None
+        try:
+            plan = nslct.Plan(n, M, 1, comm=comm, exchange=exch, device=dev.index)
+        except Exception as e:   # noqa: BLE001
+            err = repr(e)
+        if max_over_ranks(1.0 if err else 0.0, world, dev) > 0:
+            errors[exch] = err or "failed on another rank"
+            if plan is not None:
+                plan.close()
+            continue
         np_ = plan.info()["n_passes"]
         ms_l = time_exec(plan, x, out, stream, steps, 3, None, barrier)
         plan.close()
         res[exch] = max_over_ranks(ms_l, world, dev)
+    if not res:
+        raise SystemExit("slab mode: no exchange available: %r" % errors)
     # the bare exchange: (n_passes - 1) all-to-alls of the same [L][n] slabs
     send, recv = torch.empty_like(x), torch.empty_like(x)
     for _ in range(3):
@@ -740,7 +784,7 @@ def run_slab(args, nslct, torch, dev, stream, n, M, world, rank, barrier, steps=
     ms = res[best]
     a2a_bytes = (np_ - 1) * (world - 1) / world * n * L * 8.0    # per GPU per direction
     hbm_bytes = np_ * 2.0 * n * L * 8
-    return {"value": 1.0 / (ms * 1e-3), "ms": ms, "exchange": best, "ms_by_exchange": res,
+    return {"value": 1.0 / (ms * 1e-3), "ms": ms, "exchange": best, "ms_by_exchange": res, "errors": errors or None,
             "launches": np_ * steps,
             "roofline": {"bound": "nvlink (all-to-all)", "achieved": a2a_bytes / (ms * 1e-3) / 1e9,
                          "peak": a2a_bytes / (a2a_ms * 1e-3) / 1e9, "unit": "GB/s", "frac": a2a_ms / ms,
@@ -782,8 +826,13 @@ def run_dry(args):
     ms = max_over_ranks((time.perf_counter() - t0) / args.steps * 1e3, world)
     units = sum_over_ranks(batch, world)
     ranks = sum_over_ranks(1, world)
+    sub = {}
+    if world > 1 and args.config == 4 and not args.no_sub:   # the child-process plumbing of run_ours
+        port = int(max_over_ranks(_free_port() if rank == 0 else 0, world))
+        sub["C5_slab"] = slab_child(args, world, rank, int(os.environ.get("LOCAL_RANK", "0")), port,
+                                    timeout=120, extra=("--dry-run",))
     if rank == 0:
-        print(json.dumps({"metric": METRIC, "value": units / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        print(json.dumps({"metric": METRIC, "value": units / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "sub": sub,
                           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                           "scaling": "strong", "dry_run": True, "ranks_reporting": int(ranks),
                           "config": {"global_batch": int(units), "per_gpu_batch": batch}}), flush=True)

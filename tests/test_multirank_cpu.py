@@ -122,3 +122,8 @@ def test_bench_gpus_flag_spawns_ranks():
     assert d["n_gpus"] == 2 and d["ranks_reporting"] == 2
     assert d["config"]["global_batch"] == 32 and d["config"]["per_gpu_batch"] == 16
     assert d["scaling"] == "strong" and d["value"] > 0
+    # the C5 slab sub-record runs in child processes of the ranks (their own rendezvous, a
+    # timeout; a failure there cannot cost the main line): here the dry-run child, 2 ranks
+    c5 = d["sub"]["C5_slab"]
+    assert "error" not in c5, c5
+    assert c5["n_gpus"] == 2
