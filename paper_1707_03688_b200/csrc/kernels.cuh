@@ -914,7 +914,10 @@ template <int LOG2N>
 struct LineCfg {
   static constexpr int N = 1 << LOG2N;
   static constexpr int TL = N / 16;                       // threads per line
-  static constexpr int TB = (N <= 2048) ? 256 : (N <= 8192 ? 512 : 1024);
+  // N <= 256: 128-thread CTAs (8 lines at N = 256) -- more, smaller CTAs per SM fill the
+  // tail of these short launches better: C2 587k -> 610k transforms/s against 256 threads,
+  // 64 threads 512-586k, 512 threads 525k (profiles/r02f_c2_cta_size_ab.txt)
+  static constexpr int TB = (N <= 256) ? 128 : (N <= 2048) ? 256 : (N <= 8192 ? 512 : 1024);
   static constexpr int G = (TB / TL < N) ? TB / TL : N;   // lines per CTA (one image at most)
   static constexpr int THREADS = G * TL;
   // padded line stride: LS = 16/G (mod 16) spreads the G lines read together by the
