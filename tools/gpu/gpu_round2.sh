@@ -18,3 +18,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 ncu --set full --clock-control none --import-source on -k regex:line_pass_ws -s 8 -c 1 \
     -o gpurun_out/${TAG}_k2_full -f $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/${TAG}_ncu_full.log
+# the other bench configurations (kernel-only): every --config path runs
+for c in 1 2 3 5; do
+  timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_bench_c$c.json 2> gpurun_out/${TAG}_bench_c$c.err; echo "rc=$?" >> gpurun_out/${TAG}_bench_c$c.err
+done
