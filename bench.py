@@ -621,7 +621,7 @@ def measure_e2e(nslct, torch, dev, stream, n, batch, dtype, M, x, args, world, b
     t_dir = []
     for direction in ("h2d", "d2h"):
         ts = []
-        for _ in range(2):
+        for _ in range(3):
             torch.cuda.synchronize()
             t1 = time.perf_counter()
             if direction == "h2d":
@@ -636,7 +636,7 @@ def measure_e2e(nslct, torch, dev, stream, n, batch, dtype, M, x, args, world, b
     dbuf2 = torch.empty_like(dbuf)
     s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     ts = []
-    for _ in range(2):
+    for _ in range(4):   # the first repetition warms the two streams' copy engines up
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         with torch.cuda.stream(s_in):
