@@ -1993,10 +1993,22 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
       } else {
         const cpx<T>* src = in + img * slab_elems + (long long)(ll / 2) * 2 * C + (ll % 2);
         if constexpr (SLAB) {
+          if (lgC >= 10) {
+            // chunks of C >= TL elements: i = j + TL e with j < TL never crosses a chunk, so
+            // chunk index e >> s and offset j + TL (e mod 2^s) (s = lgC - 10): the chunk
+            // arithmetic is the same for every thread (uniform registers), the thread adds 2 j
+            const int sh = lgC - 10;
+            const cpx<T>* base = src + 2 * j;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int i = j + TL * e;
-            v[t][e] = ldg_stream(src + ((long long)(i >> lgC) << (lgL + lgC)) + 2 * (i & (C - 1)));
+            for (int e = 0; e < 16; ++e)
+              v[t][e] = ldg_stream(base + ((long long)(e >> sh) << (lgL + lgC)) +
+                                   ((long long)(e & ((1 << sh) - 1)) << 11));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int i = j + TL * e;
+              v[t][e] = ldg_stream(src + ((long long)(i >> lgC) << (lgL + lgC)) + 2 * (i & (C - 1)));
+            }
           }
         } else {
           src += 2 * j;
