@@ -878,6 +878,12 @@ struct PassArgs {
   // reads its lines with in_chunk = Lc, in_chunk_stride = L Lc.
   int line_base;
   int out_chunk;
+  // N = 16384 row slabs with in_chunk C >= 1024 (line_pass_pair2_kernel): the element offset
+  // of register slot e (elements j + 1024 e, j < 1024, never cross a chunk) relative to the
+  // line's base + 2 j in the chunked pair-interleaved input, computed on the host:
+  //   ((1024 e) / C) L C + 2 ((1024 e) mod C)
+  // so the loads take a constant-bank offset instead of per-load shifts and masks.
+  long long in_eoff[16];
 };
 
 // The per-line work of one pass (registers v hold elements j + TL*e of line l).
@@ -1904,9 +1910,14 @@ struct ExPadTmaOut : ExPad<T> {
 __device__ __forceinline__ void st_cluster_v2(uint32_t addr, cpx<float> v) {
   asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
 }
-template <int MODE, bool SLAB>
+// PEER (row slabs only): the transposing store goes straight into the peers' receive buffers
+// (PassArgs::peer_out) instead of through TMA -- a separate instantiation, so the TMA kernels
+// do not carry the peer-store code (the slab kernels with both paths compiled in measured
+// 7-8% slower than the batched ones on the same lines).
+template <int MODE, bool SLAB, bool PEER = false>
 __global__ void __launch_bounds__(kPair2Threads, 1)
 line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
+  static_assert(SLAB || !PEER, "peer stores exist in row-slab mode");
   using T = float;
   constexpr int LOG2N = 14;
   constexpr int N = 1 << LOG2N, TL = N / 16, THREADS = kPair2Threads, V = TL / THREADS;
@@ -1960,7 +1971,7 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
   // transposing passes write through TMA tensor stores (batched, and row slabs unless the
   // exchange is fused into peer stores)
   constexpr bool kTmaOut = !ModeIO<MODE>::kStraightOut;
-  const bool tma_out = kTmaOut && (!SLAB || !a.peer_on);
+  constexpr bool tma_out = kTmaOut && !PEER;
   uint32_t pbuf_u32;   // the partner's buffer, shared::cluster address
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(pbuf_u32) : "r"(smem_u32(buf)), "r"(c ^ 1u));
   const bool contiguous = !SLAB || ModeIO<MODE>::kUserIn || C == N;
@@ -1995,14 +2006,10 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
         if constexpr (SLAB) {
           if (lgC >= 10) {
             // chunks of C >= TL elements: i = j + TL e with j < TL never crosses a chunk, so
-            // chunk index e >> s and offset j + TL (e mod 2^s) (s = lgC - 10): the chunk
-            // arithmetic is the same for every thread (uniform registers), the thread adds 2 j
-            const int sh = lgC - 10;
+            // the chunk arithmetic depends on e only: host-computed offsets (PassArgs::in_eoff)
             const cpx<T>* base = src + 2 * j;
 #pragma unroll
-            for (int e = 0; e < 16; ++e)
-              v[t][e] = ldg_stream(base + ((long long)(e >> sh) << (lgL + lgC)) +
-                                   ((long long)(e & ((1 << sh) - 1)) << 11));
+            for (int e = 0; e < 16; ++e) v[t][e] = ldg_stream(base + a.in_eoff[e]);
           } else {
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
@@ -2118,7 +2125,7 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
         cpx<T>* d;
         if constexpr (SLAB) {
           const int sblk = e0 >> lgL, lam = e0 & (L - 1);
-          cpx<T>* base = a.peer_on ? reinterpret_cast<cpx<T>*>(a.peer_out[sblk]) + (long long)a.peer_rank * L * L
+          cpx<T>* base = PEER ? reinterpret_cast<cpx<T>*>(a.peer_out[sblk]) + (long long)a.peer_rank * L * L
                                    : out + (long long)sblk * L * L;
           d = base + ((long long)(lp >> lgLc) << (lgL + lgLc)) + (long long)(lam / 2) * 2 * Lc + 2 * (lp & (Lc - 1));
         } else {

@@ -90,13 +90,22 @@ cudaError_t launch_pair2(const PassArgs& a, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair2_kernel<MODE, SLAB>, a, map);
+  if constexpr (SLAB && !nslct::ModeIO<MODE>::kStraightOut) {
+    if (a.peer_on) return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair2_kernel<MODE, true, true>, a, map);
+  }
+  return cudaLaunchKernelEx(&cfg, nslct::line_pass_pair2_kernel<MODE, SLAB, false>, a, map);
 }
 template <int MODE, bool SLAB>
 cudaError_t set_attr_pair2() {
   using Cfg = nslct::LineCfg<14>;
-  return cudaFuncSetAttribute(nslct::line_pass_pair2_kernel<MODE, SLAB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(nslct::ModeIO<MODE>::kStraightOut ? nslct::kPair2SmemSmall : nslct::kPair2Smem));
+  const int smem = (int)(nslct::ModeIO<MODE>::kStraightOut ? nslct::kPair2SmemSmall : nslct::kPair2Smem);
+  if constexpr (SLAB && !nslct::ModeIO<MODE>::kStraightOut) {
+    cudaError_t e = cudaFuncSetAttribute(nslct::line_pass_pair2_kernel<MODE, true, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaFuncSetAttribute(nslct::line_pass_pair2_kernel<MODE, SLAB, false>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 template <bool SLAB>
 struct Pair2Row {
@@ -1102,6 +1111,13 @@ static nslct_status plan_internal(nslct_plan_t* plan, int64_t n, const double ab
       pl->args[k].line_offset = slab ? (int)(rank * L) : 0;
       pl->args[k].in_chunk = (slab && k > 0) ? (int)Lc : (int)n;
       pl->args[k].in_chunk_stride = (slab && k > 0) ? L * Lc : n * n;
+      {   // PassArgs::in_eoff (N = 16384 pair kernel, chunks of >= 1024 elements)
+        const long long C = pl->args[k].in_chunk, CS = (slab && k > 0) ? L * Lc : 0;
+        for (int e = 0; e < 16; ++e) {
+          const long long i0 = 1024ll * e;
+          pl->args[k].in_eoff[e] = (C >= 1024) ? (i0 / C) * CS + 2 * (i0 % C) : 0;
+        }
+      }
       pl->args[k].out_chunk = (int)Lc;
       pl->args[k].line_base = 0;
       pl->args[k].n_lines = slab ? L : batch * n;

@@ -2,7 +2,7 @@
 passes one after another (the all-to-all replaced by device block copies, as in
 tests/slab_emulation.py).  Prints one JSON line: per-pass ms summed over ranks (= one GPU doing
 all ranks' HBM work) and divided by P (the per-GPU HBM time of a P-GPU run, without the
-exchange).  Usage: python tools/slab_pass_timing.py [n] [P] [reps]"""
+exchange).  Usage: python tools/slab_pass_timing.py [n] [P] [reps] [exchange_chunks]"""
 import json
 import os
 import sys
@@ -18,10 +18,11 @@ def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
     P = int(sys.argv[2]) if len(sys.argv) > 2 else 8
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    chunks = int(sys.argv[4]) if len(sys.argv) > 4 else 0
     L = n // P
     mr, _ = synth.config_streams(5)
     M = synth.random_symplectic(mr)
-    plans = [nslct.SlabPlan(n, M, P, r) for r in range(P)]
+    plans = [nslct.SlabPlan(n, M, P, r, exchange_chunks=chunks) for r in range(P)]
     g = torch.Generator(device="cuda")
     g.manual_seed(5)
     x = [torch.randn((L, n), dtype=torch.complex64, device="cuda", generator=g) for _ in range(P)]
@@ -42,7 +43,7 @@ def main():
             cur = out   # layout-only stand-in for the exchange: the timing is what matters
             out = [torch.empty_like(t) for t in x]
     hbm = 2.0 * n * n * 8
-    res = {"n": n, "P": P, "pair_kernels": True,
+    res = {"n": n, "P": P, "exchange_chunks": chunks, "pair_kernels": True,
            "pass_ms_all_ranks": [round(t, 3) for t in tot],
            "per_gpu_ms": round(sum(tot) / P, 3),
            "hbm_TBps_per_pass": [round(hbm / (t * 1e-3) / 1e12, 2) for t in tot]}
