@@ -1907,6 +1907,19 @@ struct ExPadTmaOut : ExPad<T> {
     }
   }
 };
+// ExPad for the straight-output passes: the previous line's row leaves through ONE bulk store
+// from the exchange buffer, so the first exchange write of a line waits for its read-out.
+template <typename T>
+struct ExPadBulkOut : ExPad<T> {
+  int tid;
+  template <int X>
+  __device__ __forceinline__ void before_write() const {
+    if constexpr (X == 0) {
+      if (tid == 0) bulk_wait_read0();
+      __syncthreads();
+    }
+  }
+};
 __device__ __forceinline__ void st_cluster_v2(uint32_t addr, cpx<float> v) {
   asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
 }
@@ -2038,7 +2051,7 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
     if constexpr (kTmaOut) {
       pass_body_v<T, LOG2N, MODE, V>(v, jv, tws, a, (uint64_t)l, ex_tma);
     } else {
-      pass_body_v<T, LOG2N, MODE, V>(v, jv, tws, a, (uint64_t)l, ExPad<T>{buf});
+      pass_body_v<T, LOG2N, MODE, V>(v, jv, tws, a, (uint64_t)l, ExPadBulkOut<T>{{buf}, tid});
     }
 
     cpx<T>* out = reinterpret_cast<cpx<T>*>(a.out) + img * slab_elems;
@@ -2101,14 +2114,23 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
         }
       }
     } else if constexpr (ModeIO<MODE>::kStraightOut) {
+      // in place: both CTAs have consumed their input lines before either row is written
       asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
-      cpx<T>* dst = out + (long long)ll * N;
+      // the row is staged contiguously in the exchange buffer (free: ExPad ends every
+      // exchange with a CTA barrier) and leaves as one TMA bulk store that drains while the
+      // next line loads and computes -- 32 per-thread 8-byte global stores per line filled the
+      // LSU queue (ncu: lg_throttle 27-30% of the stall samples of this pass)
 #pragma unroll
       for (int t = 0; t < V; ++t)
 #pragma unroll
-        for (int e = 0; e < 16; ++e) dst[jv[t] + TL * e] = v[t][e];
+        for (int e = 0; e < 16; ++e) buf[jv[t] + TL * e] = v[t][e];
+      fence_proxy_async_smem();
       if (more) load_line(p + ncl, v);
       __syncthreads();
+      if (tid == 0) {
+        bulk_s2g(out + (long long)ll * N, buf, (uint32_t)(N * sizeof(cpx<T>)));
+        bulk_commit();
+      }
     } else {
       __syncthreads();
 #pragma unroll
@@ -2137,7 +2159,7 @@ line_pass_pair2_kernel(PassArgs a, const __grid_constant__ CUtensorMap omap) {
       asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
     }
   }
-  if (tma_out && tid == 0) bulk_wait0();
+  if ((tma_out || ModeIO<MODE>::kStraightOut) && tid == 0) bulk_wait0();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
